@@ -1,0 +1,284 @@
+"""Benchmark: train target tokens/sec of one fwd+bwd+clipped-SGD step of the
+CytonMT attention LSTM (BASELINE.json metric) on the paper-scale config
+(configs[2]: 4-layer bi-encoder LSTM, emb/hidden 1024, vocab 50k, batch 128,
+len 50) — the largest single-GPU config the metric is quoted on.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  ``value`` is device-timed with the batch
+resident in HBM; ``e2e`` times the public API call (host ids/masks staged and
+copied H2D, loss read back D2H) every step.  ``--impl reference`` times the
+reference algorithm's CPU implementation (the numpy oracle port, the
+reference itself being Python that cannot travel) on the host cores.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (V, E, H, L, B, S, T)
+    "c3": (50000, 1024, 1024, 4, 128, 50, 50),
+    "c2": (30000, 512, 512, 2, 64, 50, 50),
+    "tiny": (1000, 128, 128, 1, 16, 20, 20),
+    "c5": (100000, 1024, 1024, 2, 256, 80, 80),
+}
+METRIC = "train target tokens/sec (fwd+bwd+update)"
+CPU_SAMPLE_B = 16  # sentences per CPU-baseline step (bounded sample of the B=128 batch)
+
+
+def flops_per_step(V, E, H, L, B, S, T):
+    """Algorithmic FLOPs: F_step = 3 F_fwd."""
+    f = 8 * H * B * (2 * S * (E + H) + (L - 1) * S * 2 * H + T * (E + H) + (L - 1) * T * 2 * H)
+    f += 6 * T * B * H * H + 4 * H * S * T * B + 2 * T * B * H * V
+    return 3 * f
+
+
+def synthetic_batch(V, S, T, B, seed):
+    """ids uniform in [4, V), last target row EOS(3), masks all ones."""
+    g = np.random.default_rng(seed)
+    src = g.integers(4, V, (S, B)).astype(np.int64)
+    tgt = g.integers(4, V, (T, B)).astype(np.int64)
+    tgt[T - 1, :] = 3
+    return src, np.ones((S, B), np.float32), tgt, np.ones((T, B), np.float32)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops_sustained"], p["hbm_gbs"], "measured (MEASURED_PEAKS.json, sustained bf16)"
+    except Exception:
+        return 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for n, v in zip(names, r[2:]):
+                    if "Active" in v and "Not" not in v:
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                pass
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_rate(cfg_t, params, steps, warmup, sample_b=CPU_SAMPLE_B):
+    """Reference algorithm on host cores (numpy oracle port) on a bounded sample."""
+    from oracle import minmt_oracle as O
+    V, E, H, L, B, S, T = cfg_t
+    d = O.Dims(V, E, H, L, 0.2)
+    names = [n for n, _ in O.registry(d)]
+    src, sm, tgt, tm = synthetic_batch(V, S, T, sample_b, seed=0)
+    gen = np.random.Generator(np.random.PCG64(5))
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        loss, g, _ = O.forward_backward(params, d, src, sm, tgt, tm, 0.1, gen=gen)
+        O.sgd_step(params, g, names, 1.0, 5.0)
+        del g
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    ntok = float(tm.sum())
+    return ntok / statistics.median(times), times
+
+
+def run_reference(args, cfg_t):
+    """--impl reference: the reference's CPU implementation of the path, timed here."""
+    from paper_1802_07170_b200.model import Model, ModelConfig, Rng
+    V, E, H, L, B, S, T = cfg_t
+    model = Model.new(ModelConfig(V, E, H, L, 0.2), Rng(1))
+    params = {b.name: b.var.data for b in model.params.blocks()}
+    rate, times = cpu_oracle_rate(cfg_t, params, args.steps, args.warmup)
+    cores = os.cpu_count()
+    sample = f"{CPU_SAMPLE_B} of {B} sentences (S=T={S}) per step, {args.steps} steps after {args.warmup} warm-up"
+    out = {
+        "metric": METRIC, "value": rate, "unit": "tgt_tok/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times) * B / CPU_SAMPLE_B,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": args.config, "vocab": V, "emb": E, "hidden": H, "depth": L, "batch": B,
+                   "src_len": S, "tgt_len": T},
+        "cpu_baseline": {"value": rate, "unit": "tgt_tok/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": "tgt_tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=list(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg_t = CONFIGS[args.config]
+    V, E, H, L, B, S, T = cfg_t
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, cfg_t)
+        return
+
+    import torch
+    from paper_1802_07170_b200.engine import Engine, launch_count
+    from paper_1802_07170_b200.model import Batch, Model, ModelConfig, Rng
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = ModelConfig(V, E, H, L, 0.2)
+    model = Model.new(cfg, Rng(1))
+    eng = Engine(cfg, mode="bf16", device=local)
+    eng.upload(model.params)
+    if world > 1:
+        eng.set_dp(dist, rank, world)
+    src, sm, tgt, tm = synthetic_batch(V, S, T, B, seed=rank)
+    batch = Batch(src, tgt, sm, tm)
+    rng = Rng(5 + rank)
+    ntok_local = float(tm.sum())
+    ntok_global = ntok_local * world
+    lr, clip, eps = 1.0, 5.0, 0.1
+
+    eng.stage(src, sm, tgt, tm)
+    for _ in range(args.warmup):
+        eng.run(lr, clip, eps, rng, global_ntok=ntok_global)
+
+    # ---- device-resident timing ----
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(local)
+    clocks = ClockSampler(local)
+    eng.set_option("time_dominant", 1)
+    l0 = launch_count()
+    eng.record(0)
+    for _ in range(args.steps):
+        eng.run(lr, clip, eps, rng, global_ntok=ntok_global, asynchronous=True)
+    eng.record(1)
+    r = eng.wait()
+    ms_total = eng.elapsed_ms(0, 1)
+    launches = (launch_count() - l0) // args.steps
+    dom_ms, dom_n = eng.stat("dominant_ms")
+    eng.set_option("time_dominant", 0)
+    ck = clocks.stop()
+
+    # ---- end-to-end through the public API (host buffers, H2D + D2H inside) ----
+    if dist:
+        dist.barrier()
+    eng.record(2)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        loss, _ = eng.step(batch, lr, clip, eps, rng)
+    t_e2e = time.perf_counter() - t0
+    eng.record(3)
+    ms_e2e_dev = eng.elapsed_ms(2, 3)
+    ms_e2e = max(1e3 * t_e2e, ms_e2e_dev)
+
+    ms_step = ms_total / args.steps
+    if dist:
+        t = torch.tensor([ms_step, ms_e2e / args.steps], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, ms_e2e_step = t.tolist()
+    else:
+        ms_e2e_step = ms_e2e / args.steps
+    value = world * ntok_local / (ms_step / 1e3)
+    e2e_value = world * ntok_local / (ms_e2e_step / 1e3)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peak_tf, peak_hbm, peak_src = peaks()
+    dom_flops = 2.0 * T * B * H * V
+    achieved = dom_flops / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dominant_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    fstep = flops_per_step(*cfg_t)
+    h2d = (S * B * 4 + 2 * T * B * 4 + S * B * 4 + T * B * 4) + 4 * (3 * (S + T) * B + 2)
+    out = {
+        "metric": METRIC, "value": value, "unit": "tgt_tok/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded ids, random-init weights)",
+        "config": {"workload": args.config, "vocab": V, "emb": E, "hidden": H, "depth": L, "batch_per_gpu": B,
+                   "global_batch": B * world, "src_len": S, "tgt_len": T, "dropout": 0.2, "label_smoothing": eps,
+                   "clip": clip, "parallelism": f"dp{world}",
+                   "l2": "working set > L2 (bf16 logits alone 0.64 GB per step)"},
+        "e2e": {"value": e2e_value, "unit": "tgt_tok/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "kernel": "logits GEMM (tanh(W_o^T H_o + b_o), K13) tcgen05",
+                     "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": (achieved / peak_tf) if achieved else None, "traffic": traffic,
+                     "flops_per_launch": dom_flops, "launch_ms": dom_ms, "launches_timed": dom_n,
+                     "peak_source": peak_src},
+        "step_roofline": {"flops_per_step": fstep, "achieved_tflops": fstep / (ms_step / 1e3) / 1e12,
+                          "frac": fstep / (ms_step / 1e3) / 1e12 / peak_tf},
+        "src_tok_per_s": world * float(sm.sum()) / (ms_step / 1e3),
+        "loss_last": loss,
+        "clocks": ck,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        params = {b.name: b.var.data for b in model.params.blocks()}
+        rate, times = cpu_oracle_rate(cfg_t, params, 2, 0)
+        out["cpu_baseline"] = {"value": rate, "unit": "tgt_tok/s", "cores": os.cpu_count(), "kind": "port",
+                               "sample": f"numpy oracle, {CPU_SAMPLE_B} of {B} sentences (S=T={S}), "
+                                         f"median of 2 steps ({sum(times):.1f} s)"}
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

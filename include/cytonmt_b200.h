@@ -1,0 +1,122 @@
+/*
+ * cytonmt_b200.h — C ABI of the B200-native CytonMT train-step engine.
+ *
+ * The reference has no FFI: its only operator interface is the Python
+ * train step `minmt.training.train_step(model, batch, cfg, lr, rng) -> float`
+ * (/root/reference/pkg/src/minmt/training.py:145-159) built on the Layer
+ * contract (graph.py:34-62).  These entry points are what a ctypes (or cgo /
+ * JNI) binding of that function needs; the Python drop-in in
+ * paper_1802_07170_b200/training.py binds them.
+ *
+ * All pointers are plain host pointers; no torch types cross the boundary.
+ * Every function returns 0 on success or a cmt_status code; the message of the
+ * last failure is available from cmt_last_error().
+ */
+#ifndef CYTONMT_B200_H
+#define CYTONMT_B200_H
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* status codes (mapped to the reference's exception types by the wrapper) */
+enum cmt_status {
+  CMT_OK = 0,
+  CMT_ERR_CONFIG = 1,      /* ConfigError: bad token id (model.py:146-151), empty target mask (training.py:108-110) */
+  CMT_ERR_MASK = 2,        /* MaskError: fully masked source column (attention.py:153-154) */
+  CMT_ERR_SHAPE = 3,       /* ShapeError */
+  CMT_ERR_NUM_SCORES = 4,  /* NumericError: non-finite attention scores (tensor.py:139-140) */
+  CMT_ERR_NUM_LOGITS = 5,  /* NumericError: non-finite logits (tensor.py:148-149) */
+  CMT_ERR_NUM_LOSS = 6,    /* NumericError: non-finite loss (training.py:154-155) */
+  CMT_ERR_NUM_NORM = 7,    /* NumericError: non-finite grad norm (training.py:133-134) */
+  CMT_ERR_CUDA = 8,
+  CMT_ERR_INTERNAL = 9
+};
+
+/* precision modes */
+enum cmt_mode {
+  CMT_MODE_FP32 = 0, /* fp32 validation mode: fp32 SIMT GEMMs, 1e-4 parity */
+  CMT_MODE_BF16 = 1  /* production: tcgen05 bf16 GEMMs, fp32 accumulate/state, 2e-2 parity */
+};
+
+/* step flags */
+enum cmt_flags {
+  CMT_FLAG_NO_UPDATE = 1, /* compute loss + grads, skip clip/SGD (grads kept for cmt_download_grad) */
+  CMT_FLAG_ASYNC = 2      /* do not wait for the step; result filled by cmt_wait() */
+};
+
+/* mirrors ModelConfig (model.py:46-62) */
+typedef struct {
+  int vocab_size, embedding_size, hidden_size, depth;
+  int output_tanh, shared_embeddings;
+  double dropout;
+  int mode; /* cmt_mode */
+} cmt_config;
+
+/* per-step arguments: TrainConfig fields used by train_step + the dropout RNG */
+typedef struct {
+  double lr;          /* learning rate (train_step arg) */
+  double clip_norm;   /* TrainConfig.grad_clip_norm; <= 0 means None */
+  double epsilon;     /* TrainConfig.label_smoothing */
+  unsigned long long pcg_state_hi, pcg_state_lo, pcg_inc_hi, pcg_inc_lo; /* numpy PCG64 state */
+  double global_ntok; /* data-parallel: sum of tgt_mask over all ranks (<= 0: this batch) */
+  int flags;          /* cmt_flags */
+} cmt_step_args;
+
+typedef struct {
+  double loss;                  /* smoothed loss (training.py:113) */
+  double grad_norm;             /* global L2 norm before clipping (training.py:128-131) */
+  unsigned long long draws;     /* PCG64 doubles consumed by dropout; caller advances its generator */
+  int status;                   /* cmt_status of the step */
+} cmt_step_result;
+
+typedef struct cmt_engine cmt_engine;
+
+int cmt_create(const cmt_config* cfg, int device, cmt_engine** out);
+void cmt_destroy(cmt_engine* e);
+const char* cmt_last_error(cmt_engine* e);           /* e may be NULL (create failures) */
+
+/* parameter registry in the reference's order (model.py:86-95) */
+int cmt_num_blocks(cmt_engine* e);
+int cmt_block_info(cmt_engine* e, int idx, char* name, int name_cap, long long* rows, long long* cols);
+int cmt_upload_param(cmt_engine* e, int idx, const float* host_rowmajor, long long rows, long long cols);
+int cmt_download_param(cmt_engine* e, int idx, float* host_rowmajor, long long rows, long long cols);
+int cmt_download_grad(cmt_engine* e, int idx, float* host_rowmajor, long long rows, long long cols);
+
+/* batch (data.py:108-122): ids int64 (steps, batch) C order; masks float32 {0,1} */
+int cmt_stage_batch(cmt_engine* e, const long long* src_ids, const float* src_mask, int S,
+                    const long long* tgt_ids, const float* tgt_mask, int T, int B);
+/* run one train step on the staged batch (inputs already in HBM) */
+int cmt_run_step(cmt_engine* e, const cmt_step_args* args, cmt_step_result* res);
+/* stage + run: the reference-facing call (host buffers, H2D/D2H inside) */
+int cmt_train_step(cmt_engine* e, const long long* src_ids, const float* src_mask, int S,
+                   const long long* tgt_ids, const float* tgt_mask, int T, int B,
+                   const cmt_step_args* args, cmt_step_result* res);
+int cmt_wait(cmt_engine* e, cmt_step_result* res);
+
+/* data parallel: NCCL communicator from a 128-byte ncclUniqueId */
+int cmt_set_comm(cmt_engine* e, const void* nccl_unique_id, int rank, int world);
+
+/* timing / introspection */
+int cmt_event_record(cmt_engine* e, int slot);               /* slot 0..15 on the engine stream */
+int cmt_event_elapsed(cmt_engine* e, int a, int b, float* ms);
+unsigned long long cmt_launch_count(void);                   /* kernels launched by this library */
+int cmt_set_option(cmt_engine* e, const char* key, long long value); /* "time_dominant": CUDA-event the logits GEMM */
+int cmt_get_stat(cmt_engine* e, const char* key, double* value, double* count); /* "dominant_ms": mean launch ms */
+
+/* test hooks (parity tests only; device pointers): one GEMM C = A B^T (fp32 out), one dropout site */
+int cmt_test_gemm(int mode, int M, int N, int K, const void* A, long long lda, int a_mn, const void* B, long long ldb,
+                  int b_mn, float* C, long long ldc, int bn, int beta);
+int cmt_test_dropout(unsigned long long state_hi, unsigned long long state_lo, unsigned long long inc_hi,
+                     unsigned long long inc_lo, unsigned long long base, int N, int H, double p, const float* x,
+                     float* y, unsigned char* keep);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif

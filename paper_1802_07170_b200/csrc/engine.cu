@@ -1,0 +1,1132 @@
+// CytonMT B200 train-step engine: device memory layout, step orchestration
+// and the C ABI declared in include/cytonmt_b200.h.
+//
+// The step implemented is reference training.py:145-159 (see SURVEY §8(a)
+// "Exact step semantics").  Layout in HBM:
+//   activations token-major [n][dim], n = t*B + b (the reference's (dim, N)
+//   C-order arrays read column-wise);  LSTM weights of a layer merged into
+//   one [Din+H][4H] matrix with gate-interleaved columns (4j+q = gate q of
+//   unit j) so any 32-column GEMM chunk holds whole units for the fused cell
+//   epilogues; every other weight keeps the reference's (dim_in, dim_out)
+//   layout.  Dense params / grads / bf16 shadows live in three parallel
+//   arenas (identical offsets) so clip-norm + SGD + shadow refresh are single
+//   passes; embedding grads are row-compact (only touched rows exist).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <dlfcn.h>
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/cytonmt_b200.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace cmt {
+unsigned long long g_launches = 0;
+
+// ---------------------------------------------------------------------------
+// TMA descriptor creation (driver entry point fetched through the runtime)
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    CMT_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw Error(CMT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// bf16 2-D map: dim0 contiguous (extent d0), dim1 (extent d1, stride ld elems)
+static void make_map(CUtensorMap* m, const void* ptr, long long d0, long long d1, long long ld, int box0, int box1) {
+  if (((uintptr_t)ptr & 15) || ((ld * 2) & 15))
+    throw Error(CMT_ERR_SHAPE, "bf16 GEMM operand not 16-byte aligned (dims must be multiples of 8 in bf16 mode)");
+  cuuint64_t gdim[2] = {(cuuint64_t)d0, (cuuint64_t)d1};
+  cuuint64_t gstr[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)box1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = get_encode()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstr, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(CMT_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+struct Mat {
+  const void* p;
+  long long ld;
+  int mn;  // 1: MN-major (m/n contiguous), 0: K-major
+};
+
+static int g_num_sms = 148;
+
+template <int BN, int AMN, int BMN, class Epi>
+static void launch_tc(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const Epi& e) {
+  using C = tc::Cfg<BN>;
+  static bool attr = false;
+  auto kfn = gemm_tc_kernel<BN, AMN, BMN, Epi>;
+  if (!attr) {
+    CMT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  CUtensorMap ta, tb;
+  const void* ap = A.p ? A.p : B.p;
+  long long Kx = std::max(K, 64);
+  if (AMN) make_map(&ta, ap, M, Kx, A.ld, 64, tc::BK);
+  else make_map(&ta, ap, Kx, M, A.ld, tc::BK, tc::BM);
+  if (BMN) make_map(&tb, B.p, N, Kx, B.ld, 64, tc::BK);
+  else make_map(&tb, B.p, Kx, N, B.ld, tc::BK, BN);
+  int tiles = ceil_div(M, tc::BM) * ceil_div(N, BN);
+  int grid = std::min(tiles, g_num_sms);
+  gemm_tc_kernel<BN, AMN, BMN, Epi><<<grid, tc::NUM_THREADS, C::SMEM, st>>>(ta, tb, M, N, K, e);
+  CMT_LAUNCHED();
+  CMT_CUDA(cudaGetLastError());
+}
+
+static int pick_bn(int M, int N) {
+  if (N <= 64) return 64;
+  if (N <= 128) return 128;
+  auto eff = [&](int bn) {
+    long long t = (long long)ceil_div(M, 128) * ceil_div(N, bn);
+    long long waves = (t + g_num_sms - 1) / g_num_sms;
+    return (double)t / (double)(waves * g_num_sms);
+  };
+  return eff(256) + 0.05 >= eff(128) ? 256 : 128;
+}
+
+// ---------------------------------------------------------------------------
+// Engine
+// ---------------------------------------------------------------------------
+enum BlockKind { BK_EMB = 0, BK_LSTM_W = 1, BK_LSTM_B = 2, BK_DENSE = 3 };
+struct BlockInfo {
+  std::string name;
+  long long rows, cols;
+  int kind;
+  int table;      // BK_EMB: 0 src, 1 tgt
+  int layer;      // BK_LSTM_*
+  int gate;       // 0..3 (i,f,g,o)
+  size_t off;     // BK_DENSE: arena offset
+};
+
+struct Layer {
+  int din;
+  size_t w_off, b_off;  // arena offsets: W [din+H][4H], bias [4H]
+};
+
+struct Pinned {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t n) {
+    if (n > cap) {
+      if (p) cudaFreeHost(p);
+      CMT_CUDA(cudaMallocHost(&p, n));
+      cap = n;
+    }
+    return p;
+  }
+  ~Pinned() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+struct StepScalars {  // device-side step parameters (graph-capture friendly)
+  Pcg pcg;
+  double lr, clip;
+  float eps, inv_ntok;
+};
+struct StepOut {  // device -> host step result
+  double loss_sum;
+  double scal[2];  // sumsq, norm
+  int status;
+  int pad;
+};
+
+class Engine {
+ public:
+  cmt_config cfg;
+  int V, E, H, L;
+  bool bf;  // bf16 mode
+  int asz;  // activation element size
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[16];
+  std::string err;
+
+  std::vector<BlockInfo> blocks;
+  std::vector<Layer> layers;  // 0: enc.l1.fwd, 1: enc.l1.bwd, k (2..L): enc.lk, L+k (1..L): dec.lk
+  size_t off_wa, off_wc, off_wo, off_bo;
+  size_t dense_n = 0;
+  float* dw = nullptr;   // dense masters
+  float* dg = nullptr;   // dense grads
+  bf16* dsh = nullptr;   // dense bf16 shadows
+  float* emb_w[2] = {nullptr, nullptr};
+  bf16* emb_sh[2] = {nullptr, nullptr};
+  int n_tables;
+
+  // workspace
+  char* ws = nullptr;
+  size_t ws_cap = 0;
+  int S = 0, T = 0, B = 0;
+  bool staged = false;
+  double ntok_local = 0;
+
+  // per-shape carved pointers
+  struct LayerWS {
+    void* yext;
+    float* cext;
+    float* acts;
+    float* tc;
+    float* dy;
+  };
+  std::vector<LayerWS> lw;
+  int *src_ids_d, *tgt_in_d, *tgt_out_d;
+  float *src_mask_d, *tgt_mask_d;
+  void *Xs, *Xt, *top, *u_att, *cst_att, *hod, *Y, *dhpre, *du_att, *dU;
+  float *ux, *alpha, *ho, *losstok, *dcst, *dXemb, *dtop, *dhc, *dcc, *colpart;
+  std::vector<void*> drop_enc, drop_dec;
+  std::vector<uint8_t*> keep_enc, keep_dec;
+  uint8_t* keep_o;
+  std::vector<float*> fin_dh, fin_dc;
+  // embedding compact grads
+  int* seg_off_d[2];
+  int* seg_pos_d[2];
+  int* uniq_d[2];
+  float* gcomp[2];
+  int nuniq[2] = {0, 0};
+  int nseg_pos[2] = {0, 0};
+  double* normpart;
+  StepScalars* scal_d;
+  StepOut* out_d;
+  float* s32_d;
+  int* status_d;
+  double* losssum_d;
+  double* normscal_d;
+  Pinned pin_in, pin_out;
+  StepOut* out_h = nullptr;
+  // host copies of the staged segment info (for grad download)
+  std::vector<int> uniq_h[2];
+
+  Engine(const cmt_config& c, int device) : cfg(c) {
+    CMT_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CMT_CUDA(cudaGetDeviceProperties(&prop, device));
+    g_num_sms = prop.multiProcessorCount;
+    V = c.vocab_size; E = c.embedding_size; H = c.hidden_size; L = c.depth;
+    if (V < 1 || E < 1 || H < 1 || L < 1) throw Error(CMT_ERR_CONFIG, "model dims must be positive");
+    if (!(c.dropout >= 0.0 && c.dropout < 1.0)) throw Error(CMT_ERR_CONFIG, "dropout must be in [0, 1)");
+    bf = c.mode == CMT_MODE_BF16;
+    if (bf && prop.major < 10) throw Error(CMT_ERR_CUDA, "bf16 tcgen05 mode needs an sm_100 GPU");
+    if (bf && ((E % 8) || (H % 8) || (V % 8)))
+      throw Error(CMT_ERR_SHAPE, "bf16 mode needs vocab/embedding/hidden sizes that are multiples of 8");
+    asz = bf ? 2 : 4;
+    CMT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto& e : ev) CMT_CUDA(cudaEventCreate(&e));
+    build_registry();
+    alloc_params();
+    out_h = (StepOut*)pin_out.get(sizeof(StepOut));
+  }
+  ~Engine() {
+    cudaStreamSynchronize(st);
+    cudaFree(dw); cudaFree(dg); cudaFree(dsh);
+    for (int i = 0; i < 2; ++i) {
+      if (i == 0 || !cfg.shared_embeddings) { cudaFree(emb_w[i]); cudaFree(emb_sh[i]); }
+    }
+    cudaFree(ws);
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(st);
+  }
+
+  static size_t al(size_t x) { return (x + 63) & ~(size_t)63; }
+
+  void build_registry() {
+    n_tables = cfg.shared_embeddings ? 1 : 2;
+    blocks.push_back({"src_embed", V, E, BK_EMB, 0, -1, -1, 0});
+    if (!cfg.shared_embeddings) blocks.push_back({"tgt_embed", V, E, BK_EMB, 1, -1, -1, 0});
+    size_t off = 0;
+    auto add_layer = [&](const std::string& prefix, int din) {
+      Layer ly;
+      ly.din = din;
+      ly.w_off = off; off = al(off + (size_t)(din + H) * 4 * H);
+      ly.b_off = off; off = al(off + (size_t)4 * H);
+      int li = (int)layers.size();
+      layers.push_back(ly);
+      const char* g = "ifgo";
+      for (int q = 0; q < 4; ++q)
+        blocks.push_back({prefix + ".w_" + g[q], din + H, H, BK_LSTM_W, -1, li, q, 0});
+      for (int q = 0; q < 4; ++q) blocks.push_back({prefix + ".b_" + g[q], H, 1, BK_LSTM_B, -1, li, q, 0});
+    };
+    add_layer("enc.l1.fwd", E);
+    add_layer("enc.l1.bwd", E);
+    for (int k = 2; k <= L; ++k) add_layer("enc.l" + std::to_string(k), H);
+    for (int k = 1; k <= L; ++k) add_layer("dec.l" + std::to_string(k), k == 1 ? E : H);
+    off_wa = off; off = al(off + (size_t)H * H);
+    off_wc = off; off = al(off + (size_t)2 * H * H);
+    off_wo = off; off = al(off + (size_t)H * V);
+    off_bo = off; off = al(off + (size_t)V);
+    dense_n = off;
+    blocks.push_back({"att.w_a.w", H, H, BK_DENSE, -1, -1, -1, off_wa});
+    blocks.push_back({"att.w_c.w", 2LL * H, H, BK_DENSE, -1, -1, -1, off_wc});
+    blocks.push_back({"out.w", H, V, BK_DENSE, -1, -1, -1, off_wo});
+    blocks.push_back({"out.b", V, 1, BK_DENSE, -1, -1, -1, off_bo});
+  }
+
+  void alloc_params() {
+    CMT_CUDA(cudaMalloc(&dw, dense_n * 4));
+    CMT_CUDA(cudaMalloc(&dg, dense_n * 4));
+    CMT_CUDA(cudaMemset(dw, 0, dense_n * 4));
+    CMT_CUDA(cudaMemset(dg, 0, dense_n * 4));
+    if (bf) {
+      CMT_CUDA(cudaMalloc(&dsh, dense_n * 2));
+      CMT_CUDA(cudaMemset(dsh, 0, dense_n * 2));
+    }
+    for (int i = 0; i < n_tables; ++i) {
+      CMT_CUDA(cudaMalloc(&emb_w[i], (size_t)V * E * 4));
+      CMT_CUDA(cudaMemset(emb_w[i], 0, (size_t)V * E * 4));
+      if (bf) CMT_CUDA(cudaMalloc(&emb_sh[i], (size_t)V * E * 2));
+    }
+    if (n_tables == 1) { emb_w[1] = emb_w[0]; emb_sh[1] = emb_sh[0]; }
+  }
+
+  // ---- weight views used by the GEMMs (bf16 shadow or fp32 master) ----
+  const void* wv(size_t off) const { return bf ? (const void*)(dsh + off) : (const void*)(dw + off); }
+  const void* table_v(int t) const { return bf ? (const void*)emb_sh[t] : (const void*)emb_w[t]; }
+  int tgt_table() const { return cfg.shared_embeddings ? 0 : 1; }
+
+  // ---- upload / download ----
+  void check_block(int idx, long long rows, long long cols) {
+    if (idx < 0 || idx >= (int)blocks.size()) throw Error(CMT_ERR_SHAPE, "block index out of range");
+    if (blocks[idx].rows != rows || blocks[idx].cols != cols)
+      throw Error(CMT_ERR_SHAPE, "shape mismatch for " + blocks[idx].name);
+  }
+  void upload(int idx, const float* h, long long rows, long long cols) {
+    check_block(idx, rows, cols);
+    const BlockInfo& b = blocks[idx];
+    CMT_CUDA(cudaStreamSynchronize(st));
+    if (b.kind == BK_EMB) {
+      CMT_CUDA(cudaMemcpy(emb_w[b.table], h, (size_t)rows * cols * 4, cudaMemcpyHostToDevice));
+      if (bf) refresh_shadow(emb_w[b.table], emb_sh[b.table], (size_t)rows * cols);
+      return;
+    }
+    if (b.kind == BK_DENSE) {
+      CMT_CUDA(cudaMemcpy(dw + b.off, h, (size_t)rows * cols * 4, cudaMemcpyHostToDevice));
+      if (bf) refresh_shadow(dw + b.off, dsh + b.off, (size_t)rows * cols);
+      return;
+    }
+    const Layer& ly = layers[b.layer];
+    size_t n4 = (size_t)4 * H;
+    if (b.kind == BK_LSTM_W) {
+      // gather the current interleaved matrix, patch gate q, write back
+      size_t rowsW = ly.din + H;
+      std::vector<float> tmp(rowsW * n4);
+      CMT_CUDA(cudaMemcpy(tmp.data(), dw + ly.w_off, tmp.size() * 4, cudaMemcpyDeviceToHost));
+      for (size_t r = 0; r < rowsW; ++r)
+        for (int j = 0; j < H; ++j) tmp[r * n4 + 4 * j + b.gate] = h[r * H + j];
+      CMT_CUDA(cudaMemcpy(dw + ly.w_off, tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice));
+      if (bf) refresh_shadow(dw + ly.w_off, dsh + ly.w_off, tmp.size());
+    } else {
+      std::vector<float> tmp(n4);
+      CMT_CUDA(cudaMemcpy(tmp.data(), dw + ly.b_off, n4 * 4, cudaMemcpyDeviceToHost));
+      for (int j = 0; j < H; ++j) tmp[4 * j + b.gate] = h[j];
+      CMT_CUDA(cudaMemcpy(dw + ly.b_off, tmp.data(), n4 * 4, cudaMemcpyHostToDevice));
+      if (bf) refresh_shadow(dw + ly.b_off, dsh + ly.b_off, n4);
+    }
+  }
+  void refresh_shadow(const float* s, bf16* d, size_t n) {
+    to_bf16_kernel<<<std::min<long long>(4096, ceil_div(n, 256)), 256, 0, st>>>(s, d, (long long)n);
+    CMT_LAUNCHED();
+    CMT_CUDA(cudaStreamSynchronize(st));
+  }
+  void download(int idx, float* h, long long rows, long long cols, bool grad) {
+    check_block(idx, rows, cols);
+    CMT_CUDA(cudaStreamSynchronize(st));
+    const BlockInfo& b = blocks[idx];
+    const float* base = grad ? dg : dw;
+    if (b.kind == BK_EMB) {
+      if (!grad) {
+        CMT_CUDA(cudaMemcpy(h, emb_w[b.table], (size_t)rows * cols * 4, cudaMemcpyDeviceToHost));
+      } else {
+        std::memset(h, 0, (size_t)rows * cols * 4);
+        int t = b.table;
+        int n = nuniq[t];
+        if (n > 0) {
+          std::vector<float> gc((size_t)n * E);
+          CMT_CUDA(cudaMemcpy(gc.data(), gcomp[t], gc.size() * 4, cudaMemcpyDeviceToHost));
+          for (int u = 0; u < n; ++u) std::memcpy(h + (size_t)uniq_h[t][u] * E, &gc[(size_t)u * E], E * 4);
+        }
+      }
+      return;
+    }
+    if (b.kind == BK_DENSE) {
+      CMT_CUDA(cudaMemcpy(h, base + b.off, (size_t)rows * cols * 4, cudaMemcpyDeviceToHost));
+      return;
+    }
+    const Layer& ly = layers[b.layer];
+    size_t n4 = (size_t)4 * H;
+    if (b.kind == BK_LSTM_W) {
+      size_t rowsW = ly.din + H;
+      std::vector<float> tmp(rowsW * n4);
+      CMT_CUDA(cudaMemcpy(tmp.data(), base + ly.w_off, tmp.size() * 4, cudaMemcpyDeviceToHost));
+      for (size_t r = 0; r < rowsW; ++r)
+        for (int j = 0; j < H; ++j) h[r * H + j] = tmp[r * n4 + 4 * j + b.gate];
+    } else {
+      std::vector<float> tmp(n4);
+      CMT_CUDA(cudaMemcpy(tmp.data(), base + ly.b_off, n4 * 4, cudaMemcpyDeviceToHost));
+      for (int j = 0; j < H; ++j) h[j] = tmp[4 * j + b.gate];
+    }
+  }
+
+  // ---- workspace carving for (S, T, B) ----
+  template <typename P>
+  P* carve(char*& cur, size_t bytes) {
+    P* p = (P*)cur;
+    cur += (bytes + 255) & ~(size_t)255;
+    return p;
+  }
+  size_t layout(char* base) {
+    char* cur = base;
+    long long NS = (long long)S * B, NT = (long long)T * B;
+    long long Nmax = std::max(NS, NT);
+    int nl = (int)layers.size();
+    lw.assign(nl, {});
+    for (int l = 0; l < nl; ++l) {
+      long long steps = (l <= L) ? S : T;  // layers 0..L are encoder
+      long long N = steps * B;
+      lw[l].yext = carve<char>(cur, (steps + 1) * B * H * asz);
+      lw[l].cext = carve<float>(cur, (steps + 1) * B * H * 4);
+      lw[l].acts = carve<float>(cur, N * 4 * H * 4);
+      lw[l].tc = carve<float>(cur, N * H * 4);
+      lw[l].dy = carve<float>(cur, N * H * 4);
+    }
+    src_ids_d = carve<int>(cur, NS * 4);
+    tgt_in_d = carve<int>(cur, NT * 4);
+    tgt_out_d = carve<int>(cur, NT * 4);
+    src_mask_d = carve<float>(cur, NS * 4);
+    tgt_mask_d = carve<float>(cur, NT * 4);
+    Xs = carve<char>(cur, NS * E * asz);
+    Xt = carve<char>(cur, NT * E * asz);
+    top = carve<char>(cur, NS * H * asz);
+    ux = carve<float>(cur, Nmax * 4 * H * 4);
+    dU = carve<char>(cur, Nmax * 4 * H * asz);
+    drop_enc.assign(L + 1, nullptr); keep_enc.assign(L + 1, nullptr);
+    drop_dec.assign(L + 1, nullptr); keep_dec.assign(L + 1, nullptr);
+    for (int k = 2; k <= L; ++k) {
+      drop_enc[k] = carve<char>(cur, NS * H * asz);
+      keep_enc[k] = carve<uint8_t>(cur, NS * H);
+      drop_dec[k] = carve<char>(cur, NT * H * asz);
+      keep_dec[k] = carve<uint8_t>(cur, NT * H);
+    }
+    u_att = carve<char>(cur, NT * H * asz);
+    alpha = carve<float>(cur, (long long)B * T * S * 4);
+    cst_att = carve<char>(cur, NT * 2 * H * asz);
+    ho = carve<float>(cur, NT * H * 4);
+    hod = carve<char>(cur, NT * H * asz);
+    keep_o = carve<uint8_t>(cur, NT * H);
+    Y = carve<char>(cur, NT * (long long)V * asz);
+    losstok = carve<float>(cur, NT * 4);
+    dhpre = carve<char>(cur, NT * H * asz);
+    dcst = carve<float>(cur, NT * 2 * H * 4);
+    du_att = carve<char>(cur, NT * H * asz);
+    dXemb = carve<float>(cur, (NS + NT) * E * 4);
+    dtop = carve<float>(cur, NS * H * 4);
+    dhc = carve<float>(cur, (long long)B * H * 4);
+    dcc = carve<float>(cur, (long long)B * H * 4);
+    fin_dh.assign(L + 1, nullptr); fin_dc.assign(L + 1, nullptr);
+    for (int k = 1; k <= L; ++k) {
+      fin_dh[k] = carve<float>(cur, (long long)B * H * 4);
+      fin_dc[k] = carve<float>(cur, (long long)B * H * 4);
+    }
+    long long colmax = std::max<long long>(V, 4LL * H);
+    colpart = carve<float>(cur, 64 * colmax * 4);
+    for (int t = 0; t < 2; ++t) {
+      seg_off_d[t] = carve<int>(cur, (NS + NT + 1) * 4);
+      seg_pos_d[t] = carve<int>(cur, (NS + NT) * 4);
+      uniq_d[t] = carve<int>(cur, (NS + NT) * 4);
+      gcomp[t] = carve<float>(cur, (NS + NT) * E * 4);
+    }
+    normpart = carve<double>(cur, 3 * NORM_BLOCKS * 8);
+    scal_d = carve<StepScalars>(cur, sizeof(StepScalars));
+    out_d = carve<StepOut>(cur, sizeof(StepOut));
+    s32_d = carve<float>(cur, 4);
+    return (size_t)(cur - base);
+  }
+  void ensure_ws(int S_, int T_, int B_) {
+    S = S_; T = T_; B = B_;
+    size_t need = layout(nullptr);
+    if (need > ws_cap) {
+      CMT_CUDA(cudaStreamSynchronize(st));
+      if (ws) cudaFree(ws);
+      ws = nullptr;
+      CMT_CUDA(cudaMalloc(&ws, need));
+      ws_cap = need;
+    }
+    layout(ws);
+    status_d = &out_d->status;
+    losssum_d = &out_d->loss_sum;
+    normscal_d = out_d->scal;
+  }
+
+  // ---- batch staging: host validation (model.py:146-151, attention.py:153-154) + H2D ----
+  void stage(const long long* src, const float* smask, int S_, const long long* tgt, const float* tmask, int T_,
+             int B_) {
+    if (S_ < 1 || T_ < 1 || B_ < 1) throw Error(CMT_ERR_SHAPE, "batch dimensions must be positive");
+    auto bad_id = [&](const long long* ids, long long n, long long& bad) {
+      for (long long i = 0; i < n; ++i)
+        if (ids[i] < 0 || ids[i] >= V) { bad = ids[i]; return true; }
+      return false;
+    };
+    long long bad;
+    long long NS = (long long)S_ * B_, NT = (long long)T_ * B_;
+    if (bad_id(src, NS, bad) || bad_id(tgt, NT, bad))
+      throw Error(CMT_ERR_CONFIG, "token id " + std::to_string(bad) + " outside vocabulary of size " + std::to_string(V));
+    for (int b = 0; b < B_; ++b) {
+      bool any = false;
+      for (int s = 0; s < S_; ++s) any |= smask[(long long)s * B_ + b] > 0.f;
+      if (!any) throw Error(CMT_ERR_MASK, "a batch column has every source position masked");
+    }
+    float ntok = 0.f;  // numpy float32 sum of {0,1} masks is exact below 2^24
+    for (long long i = 0; i < NT; ++i) ntok += tmask[i];
+    ntok_local = ntok;
+    if (!(ntok > 0.f)) throw Error(CMT_ERR_CONFIG, "smoothed_loss needs at least one unmasked token");
+    ensure_ws(S_, T_, B_);
+    // pinned staging: ids (int32) + masks + segments
+    size_t nbytes = (size_t)(NS + 2 * NT) * 4 + (size_t)(NS + NT) * 4 + 2 * (size_t)(3 * (NS + NT) + 2) * 4;
+    char* p = (char*)pin_in.get(nbytes);
+    CMT_CUDA(cudaStreamSynchronize(st));  // previous step may still read the staging buffer
+    int* h_src = (int*)p;
+    int* h_tin = h_src + NS;
+    int* h_tout = h_tin + NT;
+    float* h_sm = (float*)(h_tout + NT);
+    float* h_tm = h_sm + NS;
+    for (long long i = 0; i < NS; ++i) h_src[i] = (int)src[i];
+    for (int b = 0; b < B_; ++b) h_tin[b] = 2;  // BOS (model.py:239-244)
+    for (long long i = B_; i < NT; ++i) h_tin[i] = (int)tgt[i - B_];
+    for (long long i = 0; i < NT; ++i) h_tout[i] = (int)tgt[i];
+    std::memcpy(h_sm, smask, NS * 4);
+    std::memcpy(h_tm, tmask, NT * 4);
+    CMT_CUDA(cudaMemcpyAsync(src_ids_d, h_src, NS * 4, cudaMemcpyHostToDevice, st));
+    CMT_CUDA(cudaMemcpyAsync(tgt_in_d, h_tin, NT * 4, cudaMemcpyHostToDevice, st));
+    CMT_CUDA(cudaMemcpyAsync(tgt_out_d, h_tout, NT * 4, cudaMemcpyHostToDevice, st));
+    CMT_CUDA(cudaMemcpyAsync(src_mask_d, h_sm, NS * 4, cudaMemcpyHostToDevice, st));
+    CMT_CUDA(cudaMemcpyAsync(tgt_mask_d, h_tm, NT * 4, cudaMemcpyHostToDevice, st));
+    // embedding segments: unique ids (ascending) with their positions in order
+    int* q = (int*)(h_tm + NT);
+    auto build = [&](int t, const std::vector<std::pair<int, int>>& idpos) {
+      std::vector<std::pair<int, int>> v = idpos;
+      std::stable_sort(v.begin(), v.end(), [](auto& a, auto& b) { return a.first < b.first; });
+      int n = (int)v.size();
+      int* off = q; int* pos = q + n + 1; int* uq = pos + n;
+      int nu = 0;
+      for (int i = 0; i < n; ++i) {
+        if (i == 0 || v[i].first != v[i - 1].first) { off[nu] = i; uq[nu] = v[i].first; ++nu; }
+        pos[i] = v[i].second;
+      }
+      off[nu] = n;
+      nuniq[t] = nu;
+      nseg_pos[t] = n;
+      uniq_h[t].assign(uq, uq + nu);
+      CMT_CUDA(cudaMemcpyAsync(seg_off_d[t], off, (nu + 1) * 4, cudaMemcpyHostToDevice, st));
+      CMT_CUDA(cudaMemcpyAsync(seg_pos_d[t], pos, n * 4, cudaMemcpyHostToDevice, st));
+      CMT_CUDA(cudaMemcpyAsync(uniq_d[t], uq, nu * 4, cudaMemcpyHostToDevice, st));
+      q = uq + nu;
+    };
+    std::vector<std::pair<int, int>> a, b;
+    for (long long i = 0; i < NS; ++i) a.push_back({h_src[i], (int)i});
+    for (long long i = 0; i < NT; ++i) b.push_back({h_tin[i], (int)(NS + i)});
+    if (cfg.shared_embeddings) {
+      a.insert(a.end(), b.begin(), b.end());
+      build(0, a);
+      nuniq[1] = 0;
+    } else {
+      build(0, a);
+      build(1, b);
+    }
+    staged = true;
+  }
+
+  // ---- launch helpers ----
+  template <class Epi>
+  void gemm(int M, int N, int K, Mat A, Mat Bm, const Epi& e, int bn = 0) {
+    if (M <= 0 || N <= 0) return;
+    if (!bf) {
+      dim3 grid(ceil_div(N, 64), ceil_div(M, 64));
+      gemm_simt_kernel<Epi><<<grid, 256, 0, st>>>((const float*)A.p, A.ld, A.mn, (const float*)Bm.p, Bm.ld, Bm.mn, M,
+                                                   N, K, e);
+      CMT_LAUNCHED();
+      CMT_CUDA(cudaGetLastError());
+      return;
+    }
+    dispatch_tc(M, N, K, A, Bm, e, bn);
+  }
+  void dispatch_tc(int M, int N, int K, Mat A, Mat Bm, const EpiStore& e, int bn) {
+    if (!bn) bn = pick_bn(M, N);
+    int key = A.mn * 2 + Bm.mn;
+#define CMT_TC(BN_, AMN, BMN) \
+  if (bn == BN_ && key == AMN * 2 + BMN) return launch_tc<BN_, AMN, BMN, EpiStore>(st, M, N, K, A, Bm, e);
+    CMT_TC(64, 0, 1) CMT_TC(128, 0, 1) CMT_TC(256, 0, 1)
+    CMT_TC(64, 0, 0) CMT_TC(128, 0, 0) CMT_TC(256, 0, 0)
+    CMT_TC(64, 1, 1) CMT_TC(128, 1, 1) CMT_TC(256, 1, 1)
+#undef CMT_TC
+    throw Error(CMT_ERR_INTERNAL, "no tcgen05 GEMM instantiation for this operand layout");
+  }
+  void dispatch_tc(int M, int N, int K, Mat A, Mat Bm, const EpiLstmFwd& e, int) {
+    if (A.mn || !Bm.mn) throw Error(CMT_ERR_INTERNAL, "lstm fwd layout");
+    launch_tc<64, 0, 1, EpiLstmFwd>(st, M, N, K, A, Bm, e);
+  }
+  void dispatch_tc(int M, int N, int K, Mat A, Mat Bm, const EpiLstmBwd& e, int) {
+    if (A.mn || Bm.mn) throw Error(CMT_ERR_INTERNAL, "lstm bwd layout");
+    launch_tc<32, 0, 0, EpiLstmBwd>(st, M, N, K, A, Bm, e);
+  }
+  void dispatch_tc(int M, int N, int K, Mat A, Mat Bm, const EpiInitGrad& e, int) {
+    launch_tc<32, 0, 0, EpiInitGrad>(st, M, N, K, A, Bm, e);
+  }
+
+  EpiStore store(void* C, long long ldc, bool c_act) const {
+    EpiStore e;
+    e.C = C; e.ldc = ldc; e.c_bf16 = (c_act && bf) ? 1 : 0;
+    return e;
+  }
+  int grid_for(long long n) const { return (int)std::min<long long>(8 * g_num_sms, std::max<long long>(1, ceil_div(n, 256))); }
+
+  template <typename T>
+  void launch_gather(const void* table, const int* ids, int N, void* out) {
+    gather_rows_kernel<T><<<N, 128, 0, st>>>((const T*)table, E, ids, N, (T*)out);
+    CMT_LAUNCHED();
+  }
+  void gather(int t, const int* ids, int N, void* out) {
+    if (bf) launch_gather<bf16>(table_v(t), ids, N, out);
+    else launch_gather<float>(table_v(t), ids, N, out);
+  }
+  template <typename TI, typename TO>
+  void launch_dropout(const void* x, void* y, uint8_t* keep, int N, unsigned long long base, const Pcg& pcg) {
+    dim3 blk(32, 8);
+    dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, 32), 8));
+    float scale = 1.0f / (float)(1.0 - cfg.dropout);
+    dropout_fwd_kernel2<TI, TO><<<grid, blk, 0, st>>>((const TI*)x, (TO*)y, keep, N, H, pcg, base, cfg.dropout, scale);
+    CMT_LAUNCHED();
+  }
+
+  // ---- LSTM scans ----
+  struct ScanViews {
+    void* ybase;        // y[0]
+    const void* hprev;  // h_{t-1} for t (row t*B+b)
+    float* cbase;
+    const float* cprev;
+  };
+  ScanViews views(int l, bool reverse) {
+    long long slot = (long long)B * H;
+    char* y = (char*)lw[l].yext;
+    float* c = lw[l].cext;
+    if (!reverse) return {y + slot * asz, y, c + slot, c};
+    return {y, y + slot * asz, c, c + slot};
+  }
+
+  void scan_fwd(int l, const void* X, int din, int steps, bool reverse, const float* mask) {
+    const Layer& ly = layers[l];
+    long long N = (long long)steps * B;
+    // hoisted input projection Ux = X W_x + b   (layers.py:354-357, K3)
+    EpiStore e = store(ux, 4LL * H, false);
+    e.bias = dw + ly.b_off;
+    gemm((int)N, 4 * H, din, Mat{X, din, 0}, Mat{wv(ly.w_off), 4LL * H, 1}, e);
+    ScanViews v = views(l, reverse);
+    const void* Wh = (const char*)wv(ly.w_off) + (size_t)din * 4 * H * asz;
+    for (int p = 0; p < steps; ++p) {
+      int t = reverse ? steps - 1 - p : p;
+      EpiLstmFwd f;
+      f.ux = ux; f.hprev = v.hprev; f.cprev = v.cprev; f.y = v.ybase; f.cst = v.cbase;
+      f.acts = lw[l].acts; f.tcache = lw[l].tc; f.mask = mask ? mask + (long long)t * B : nullptr;
+      f.row0 = (long long)t * B; f.H = H; f.act_bf16 = bf;
+      const void* hp = (const char*)v.hprev + (size_t)t * B * H * asz;
+      gemm(B, 4 * H, H, Mat{hp, H, 0}, Mat{Wh, 4LL * H, 1}, f);
+    }
+  }
+
+  // BPTT for layer l; writes dX (= or +=, optional dropout mask) and param grads.
+  void scan_bwd(int l, const void* X, int din, int steps, bool reverse, const float* mask, const float* dy,
+                const float* dh_final, const float* dc_final, float* dh0, float* dc0, float* dX, int dx_beta,
+                const uint8_t* dx_keep) {
+    const Layer& ly = layers[l];
+    long long N = (long long)steps * B;
+    long long BH = (long long)B * H;
+    ScanViews v = views(l, reverse);
+    if (dh_final) CMT_CUDA(cudaMemcpyAsync(dhc, dh_final, BH * 4, cudaMemcpyDeviceToDevice, st));
+    else CMT_CUDA(cudaMemsetAsync(dhc, 0, BH * 4, st));
+    if (dc_final) CMT_CUDA(cudaMemcpyAsync(dcc, dc_final, BH * 4, cudaMemcpyDeviceToDevice, st));
+    else CMT_CUDA(cudaMemsetAsync(dcc, 0, BH * 4, st));
+    const void* WhN = (const char*)wv(ly.w_off) + (size_t)din * 4 * H * asz;  // rows din.. of [din+H][4H]
+    auto time_of = [&](int p) { return reverse ? steps - 1 - p : p; };
+    for (int p = steps - 1; p >= 0; --p) {
+      int t = time_of(p);
+      EpiLstmBwd f;
+      f.dy = dy; f.dhc = dhc; f.dc = dcc; f.acts = lw[l].acts; f.tcache = lw[l].tc; f.cprev = v.cprev;
+      f.mask = mask ? mask + (long long)t * B : nullptr; f.dU = dU; f.row0 = (long long)t * B; f.H = H;
+      f.act_bf16 = bf;
+      if (p == steps - 1) {
+        gemm(B, H, 0, Mat{nullptr, 4LL * H, 0}, Mat{WhN, 4LL * H, 0}, f);
+      } else {
+        int tn = time_of(p + 1);
+        const void* a = (const char*)dU + (size_t)tn * B * 4 * H * asz;
+        gemm(B, H, 4 * H, Mat{a, 4LL * H, 0}, Mat{WhN, 4LL * H, 0}, f);
+      }
+    }
+    if (dh0) {
+      EpiInitGrad f{dh0, dc0, dhc, dcc, H};
+      const void* a = (const char*)dU + (size_t)time_of(0) * B * 4 * H * asz;
+      gemm(B, H, 4 * H, Mat{a, 4LL * H, 0}, Mat{WhN, 4LL * H, 0}, f);
+    }
+    // weight grads: dW[0:din] = X^T dU, dW[din:] = Hprev^T dU  (layers.py:389-391, batched; K6)
+    gemm(din, 4 * H, (int)N, Mat{X, din, 1}, Mat{dU, 4LL * H, 1}, store(dg + ly.w_off, 4LL * H, false));
+    gemm(H, 4 * H, (int)N, Mat{v.hprev, H, 1}, Mat{dU, 4LL * H, 1},
+         store(dg + ly.w_off + (size_t)din * 4 * H, 4LL * H, false));
+    colsum(dU, true, N, 4 * H, dg + ly.b_off);
+    // input grads dX = dU W_x^T (layers.py:392; K7), dropout backward fused (layers.py:292-296)
+    EpiStore e = store(dX, din, false);
+    e.beta = dx_beta;
+    if (dx_keep) { e.dmask = dx_keep; e.ld_dmask = din; e.dscale = 1.0f / (float)(1.0 - cfg.dropout); }
+    gemm((int)N, din, 4 * H, Mat{dU, 4LL * H, 0}, Mat{wv(ly.w_off), 4LL * H, 0}, e);
+  }
+
+  void colsum(const void* D, bool is_act, long long rows, int cols, float* out) {
+    int chunks = (int)std::min<long long>(64, std::max<long long>(1, rows / 64));
+    int rows_per = ceil_div(rows, chunks);
+    chunks = ceil_div(rows, rows_per);
+    dim3 grid(ceil_div(cols, 256), chunks);
+    if (is_act && bf) colsum_partial_kernel<bf16><<<grid, 256, 0, st>>>((const bf16*)D, cols, (int)rows, cols, rows_per, colpart);
+    else colsum_partial_kernel<float><<<grid, 256, 0, st>>>((const float*)D, cols, (int)rows, cols, rows_per, colpart);
+    CMT_LAUNCHED();
+    colsum_final_kernel<<<ceil_div(cols, 256), 256, 0, st>>>(colpart, chunks, cols, out);
+    CMT_LAUNCHED();
+  }
+
+  template <typename T>
+  void copy2d(const void* s, long long lds, void* d, long long ldd, int rows, int cols) {
+    copy2d_kernel<T, T><<<grid_for((long long)rows * cols), 256, 0, st>>>((const T*)s, lds, (T*)d, ldd, rows, cols);
+    CMT_LAUNCHED();
+  }
+  void copy_act(const void* s, long long lds, void* d, long long ldd, int rows, int cols) {
+    if (bf) copy2d<bf16>(s, lds, d, ldd, rows, cols);
+    else copy2d<float>(s, lds, d, ldd, rows, cols);
+  }
+
+  // ---- the step ----
+  void run(const cmt_step_args& a, cmt_step_result* res) {
+    if (!staged) throw Error(CMT_ERR_INTERNAL, "no batch staged");
+    const long long NS = (long long)S * B, NT = (long long)T * B, BH = (long long)B * H;
+    const bool drop = cfg.dropout > 0.0;
+    Pcg pcg{a.pcg_state_hi, a.pcg_state_lo, a.pcg_inc_hi, a.pcg_inc_lo};
+    double ntok = a.global_ntok > 0 ? a.global_ntok : ntok_local;
+    float inv_ntok = (float)(1.0 / (double)(float)ntok);
+    CMT_CUDA(cudaMemsetAsync(out_d, 0, sizeof(StepOut), st));
+
+    // ===== forward =====
+    gather(0, src_ids_d, (int)NS, Xs);
+    gather(tgt_table(), tgt_in_d, (int)NT, Xt);
+    for (int l : {0, 1}) {  // zero initial states of the encoder scans
+      ScanViews v = views(l, l == 1);
+      CMT_CUDA(cudaMemsetAsync((char*)v.hprev + (size_t)(l == 1 ? (S - 1) : 0) * BH * asz, 0, BH * asz, st));
+      CMT_CUDA(cudaMemsetAsync((float*)v.cprev + (size_t)(l == 1 ? (S - 1) : 0) * BH, 0, BH * 4, st));
+    }
+    scan_fwd(0, Xs, E, S, false, src_mask_d);
+    scan_fwd(1, Xs, E, S, true, src_mask_d);
+    {
+      ScanViews f = views(0, false), r = views(1, true);
+      if (bf) add2_kernel<bf16><<<grid_for(NS * H), 256, 0, st>>>((const bf16*)f.ybase, (const bf16*)r.ybase, (bf16*)top, NS * H);
+      else add2_kernel<float><<<grid_for(NS * H), 256, 0, st>>>((const float*)f.ybase, (const float*)r.ybase, (float*)top, NS * H);
+      CMT_LAUNCHED();
+    }
+    unsigned long long draw = 0;
+    const void* cur = top;
+    for (int k = 2; k <= L; ++k) {
+      const void* in = cur;
+      if (drop) {
+        if (bf) launch_dropout<bf16, bf16>(cur, drop_enc[k], keep_enc[k], (int)NS, draw, pcg);
+        else launch_dropout<float, float>(cur, drop_enc[k], keep_enc[k], (int)NS, draw, pcg);
+        draw += (unsigned long long)NS * H;
+        in = drop_enc[k];
+      } else {
+        drop_enc[k] = const_cast<void*>(cur);
+      }
+      CMT_CUDA(cudaMemsetAsync(lw[k].yext, 0, BH * asz, st));
+      CMT_CUDA(cudaMemsetAsync(lw[k].cext, 0, BH * 4, st));
+      scan_fwd(k, in, H, S, false, src_mask_d);
+      cur = views(k, false).ybase;
+    }
+    const void* Hs = (L == 1) ? top : views(L, false).ybase;
+    // decoder: layer k starts from encoder layer k's final state (model.py:292-305)
+    const void* x = Xt;
+    for (int k = 1; k <= L; ++k) {
+      int l = L + k;
+      if (k > 1) {
+        const void* prev = views(l - 1, false).ybase;
+        if (drop) {
+          if (bf) launch_dropout<bf16, bf16>(prev, drop_dec[k], keep_dec[k], (int)NT, draw, pcg);
+          else launch_dropout<float, float>(prev, drop_dec[k], keep_dec[k], (int)NT, draw, pcg);
+          draw += (unsigned long long)NT * H;
+          x = drop_dec[k];
+        } else {
+          drop_dec[k] = const_cast<void*>(prev);
+          x = prev;
+        }
+      }
+      // encoder final: l1.bwd final sits in slot 0; deep layers in slot S
+      int el = (k == 1) ? 1 : k;
+      size_t fslot = (k == 1) ? 0 : (size_t)S;
+      copy_act((char*)lw[el].yext + fslot * BH * asz, H, lw[l].yext, H, B, H);
+      CMT_CUDA(cudaMemcpyAsync(lw[l].cext, lw[el].cext + fslot * BH, BH * 4, cudaMemcpyDeviceToDevice, st));
+      scan_fwd(l, x, k == 1 ? E : H, T, false, nullptr);
+    }
+    const void* Ht = views(2 * L, false).ybase;
+    // attention (attention.py:146-173)
+    copy_act(Ht, H, (char*)cst_att + (size_t)H * asz, 2LL * H, (int)NT, H);
+    gemm((int)NT, H, H, Mat{Ht, H, 0}, Mat{wv(off_wa), H, 1}, store(u_att, H, true));
+    {
+      size_t smem = attn_fwd_smem(S, T);
+      if (bf) {
+        cudaFuncSetAttribute(attn_fwd_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attn_fwd_kernel<bf16><<<B, ATT_THREADS, smem, st>>>((const bf16*)Hs, (const bf16*)u_att, src_mask_d, S, T, B, H,
+                                                              alpha, (bf16*)cst_att, 2LL * H, status_d);
+      } else {
+        cudaFuncSetAttribute(attn_fwd_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attn_fwd_kernel<float><<<B, ATT_THREADS, smem, st>>>((const float*)Hs, (const float*)u_att, src_mask_d, S, T, B,
+                                                               H, alpha, (float*)cst_att, 2LL * H, status_d);
+      }
+      CMT_LAUNCHED();
+      CMT_CUDA(cudaGetLastError());
+    }
+    {
+      EpiStore e = store(ho, H, false);
+      e.act = 1;
+      gemm((int)NT, H, 2 * H, Mat{cst_att, 2LL * H, 0}, Mat{wv(off_wc), H, 1}, e);
+    }
+    const void* hin = ho;
+    if (drop) {
+      if (bf) launch_dropout<float, bf16>(ho, hod, keep_o, (int)NT, draw, pcg);
+      else launch_dropout<float, float>(ho, hod, keep_o, (int)NT, draw, pcg);
+      draw += (unsigned long long)NT * H;
+      hin = hod;
+    } else {
+      if (bf) {
+        copy2d_kernel<float, bf16><<<grid_for(NT * H), 256, 0, st>>>(ho, H, (bf16*)hod, H, (int)NT, H);
+        CMT_LAUNCHED();
+      } else {
+        CMT_CUDA(cudaMemcpyAsync(hod, ho, NT * H * 4, cudaMemcpyDeviceToDevice, st));
+      }
+      hin = hod;
+    }
+    {
+      EpiStore e = store(Y, V, true);
+      e.bias = dw + off_bo;
+      e.act = cfg.output_tanh ? 1 : 0;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (time_dominant) {
+        CMT_CUDA(cudaEventCreate(&e0));
+        CMT_CUDA(cudaEventCreate(&e1));
+        CMT_CUDA(cudaEventRecord(e0, st));
+      }
+      gemm((int)NT, V, H, Mat{hin, H, 0}, Mat{wv(off_wo), V, 1}, e);
+      if (time_dominant) {
+        CMT_CUDA(cudaEventRecord(e1, st));
+        dom_events.push_back({e0, e1});
+      }
+    }
+    // fused log-softmax + smoothed CE + grad (training.py:96-120, tensor.py:146-151)
+    if (bf) ce_kernel<bf16><<<(int)NT, CE_THREADS, 0, st>>>((bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon, inv_ntok,
+                                                           cfg.output_tanh, losstok, status_d);
+    else ce_kernel<float><<<(int)NT, CE_THREADS, 0, st>>>((float*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon, inv_ntok,
+                                                         cfg.output_tanh, losstok, status_d);
+    CMT_LAUNCHED();
+    sum_to_double_kernel<<<1, 1024, 0, st>>>(losstok, (int)NT, losssum_d);
+    CMT_LAUNCHED();
+
+    // ===== backward =====
+    // output projection (layers.py:64-73): dW_o, db_o, dH_o (+ dropout bwd + tanh' of H_o)
+    gemm(H, V, (int)NT, Mat{hin, H, 1}, Mat{Y, V, 1}, store(dg + off_wo, V, false));
+    colsum(Y, true, NT, V, dg + off_bo);
+    {
+      EpiStore e = store(dhpre, H, true);
+      if (drop) { e.dmask = keep_o; e.ld_dmask = H; e.dscale = 1.0f / (float)(1.0 - cfg.dropout); }
+      e.tgrad_y = ho; e.ld_tgrad = H;
+      gemm((int)NT, H, V, Mat{Y, V, 0}, Mat{wv(off_wo), V, 0}, e);
+    }
+    // W_c (attention.py:171)
+    gemm(2 * H, H, (int)NT, Mat{cst_att, 2LL * H, 1}, Mat{dhpre, H, 1}, store(dg + off_wc, H, false));
+    gemm((int)NT, 2 * H, H, Mat{dhpre, H, 0}, Mat{wv(off_wc), H, 0}, store(dcst, 2LL * H, false));
+    // attention core backward
+    float* dHs = (L == 1) ? dtop : lw[L].dy;
+    CMT_CUDA(cudaMemsetAsync(dHs, 0, NS * H * 4, st));
+    {
+      size_t smem = attn_bwd_smem(S, T);
+      if (bf) {
+        cudaFuncSetAttribute(attn_bwd_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attn_bwd_kernel<bf16><<<B, ATT_THREADS, smem, st>>>((const bf16*)Hs, (const bf16*)u_att, alpha, dcst, 2LL * H, S, T,
+                                                              B, H, dHs, (bf16*)du_att);
+      } else {
+        cudaFuncSetAttribute(attn_bwd_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attn_bwd_kernel<float><<<B, ATT_THREADS, smem, st>>>((const float*)Hs, (const float*)u_att, alpha, dcst, 2LL * H, S,
+                                                               T, B, H, dHs, (float*)du_att);
+      }
+      CMT_LAUNCHED();
+      CMT_CUDA(cudaGetLastError());
+    }
+    // W_a (attention.py:166): dW_a and dH_t = du W_a^T + dC_st[:, H:]
+    gemm(H, H, (int)NT, Mat{Ht, H, 1}, Mat{du_att, H, 1}, store(dg + off_wa, H, false));
+    {
+      EpiStore e = store(lw[2 * L].dy, H, false);
+      e.add = dcst + H; e.ld_add = 2LL * H;
+      gemm((int)NT, H, H, Mat{du_att, H, 0}, Mat{wv(off_wa), H, 0}, e);
+    }
+    // decoder BPTT, top layer first (graph.py:112-115); init-state grads -> encoder finals
+    for (int k = L; k >= 1; --k) {
+      int l = L + k;
+      const void* X = (k == 1) ? Xt : drop_dec[k];
+      int din = (k == 1) ? E : H;
+      float* dX = (k == 1) ? dXemb + NS * E : lw[l - 1].dy;
+      const uint8_t* kp = (k > 1 && drop) ? keep_dec[k] : nullptr;
+      scan_bwd(l, X, din, T, false, nullptr, lw[l].dy, nullptr, nullptr, fin_dh[k], fin_dc[k], dX, 0, kp);
+    }
+    // encoder deep layers, top first
+    for (int k = L; k >= 2; --k) {
+      float* dX = (k == 2) ? dtop : lw[k - 1].dy;
+      const uint8_t* kp = drop ? keep_enc[k] : nullptr;
+      scan_bwd(k, drop_enc[k], H, S, false, src_mask_d, lw[k].dy, fin_dh[k], fin_dc[k], nullptr, nullptr, dX, 0, kp);
+    }
+    // layer 1: top = y_f + y_b so both directions receive dtop (layers.py:176-180)
+    scan_bwd(1, Xs, E, S, true, src_mask_d, dtop, fin_dh[1], fin_dc[1], nullptr, nullptr, dXemb, 0, nullptr);
+    scan_bwd(0, Xs, E, S, false, src_mask_d, dtop, nullptr, nullptr, nullptr, nullptr, dXemb, 1, nullptr);
+    // embedding grads: deterministic segmented scatter (tensor.py:208-216)
+    for (int t = 0; t < n_tables; ++t) {
+      if (nuniq[t] == 0) continue;
+      scatter_compact_kernel<<<nuniq[t], 128, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t], gcomp[t]);
+      CMT_LAUNCHED();
+    }
+
+    // ===== global-norm clip + SGD (training.py:123-142) =====
+    int nparts = 0;
+    sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(dg, (long long)dense_n, normpart);
+    CMT_LAUNCHED();
+    nparts += NORM_BLOCKS;
+    for (int t = 0; t < n_tables; ++t) {
+      if (nuniq[t] == 0) continue;
+      sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(gcomp[t], (long long)nuniq[t] * E, normpart + nparts);
+      CMT_LAUNCHED();
+      nparts += NORM_BLOCKS;
+    }
+    clip_scale_kernel<<<1, 32, 0, st>>>(normpart, nparts, a.lr, a.clip_norm, normscal_d, s32_d, status_d);
+    CMT_LAUNCHED();
+    if (!(a.flags & CMT_FLAG_NO_UPDATE)) {
+      sgd_dense_kernel<<<grid_for((long long)dense_n), 256, 0, st>>>(dw, dg, bf ? dsh : nullptr, (long long)dense_n, s32_d,
+                                                                     status_d);
+      CMT_LAUNCHED();
+      for (int t = 0; t < n_tables; ++t) {
+        if (nuniq[t] == 0) continue;
+        sgd_rows_kernel<<<nuniq[t], 128, 0, st>>>(emb_w[t], bf ? emb_sh[t] : nullptr, E, uniq_d[t], nuniq[t], gcomp[t],
+                                                   s32_d, status_d);
+        CMT_LAUNCHED();
+      }
+    }
+    CMT_CUDA(cudaGetLastError());
+    CMT_CUDA(cudaMemcpyAsync(out_h, out_d, sizeof(StepOut), cudaMemcpyDeviceToHost, st));
+    last_draws = draw;
+    last_ntok = ntok;
+    if (res) {
+      res->draws = draw;
+      res->status = CMT_OK;
+      if (!(a.flags & CMT_FLAG_ASYNC)) wait(res);
+    }
+  }
+  unsigned long long last_draws = 0;
+  double last_ntok = 1;
+  int time_dominant = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> dom_events;
+  // mean duration (ms) of the timed dominant-kernel launches since the last call
+  double dominant_ms(double* count) {
+    CMT_CUDA(cudaStreamSynchronize(st));
+    double tot = 0;
+    for (auto& p : dom_events) {
+      float ms = 0;
+      CMT_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
+      tot += ms;
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
+    *count = (double)dom_events.size();
+    double r = dom_events.empty() ? 0.0 : tot / dom_events.size();
+    dom_events.clear();
+    return r;
+  }
+
+  void wait(cmt_step_result* res) {
+    CMT_CUDA(cudaStreamSynchronize(st));
+    res->draws = last_draws;
+    res->loss = (double)((float)out_h->loss_sum / (float)last_ntok);
+    res->grad_norm = out_h->scal[1];
+    int s = out_h->status;
+    res->status = (s & ST_SCORES) ? CMT_ERR_NUM_SCORES
+                : (s & ST_LOGITS) ? CMT_ERR_NUM_LOGITS
+                : (s & ST_LOSS)   ? CMT_ERR_NUM_LOSS
+                : (s & ST_NORM)   ? CMT_ERR_NUM_NORM
+                                  : CMT_OK;
+  }
+};
+
+}  // namespace cmt
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using cmt::Engine;
+using cmt::Error;
+
+struct cmt_engine {
+  Engine* eng;
+  std::string err;
+};
+static thread_local std::string g_err;
+
+template <class F>
+static int guard(cmt_engine* e, F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& x) {
+    (e ? e->err : g_err) = x.what();
+    return x.code;
+  } catch (const std::exception& x) {
+    (e ? e->err : g_err) = x.what();
+    return cmt::CMT_ERR_INTERNAL;
+  }
+}
+
+extern "C" {
+
+int cmt_create(const cmt_config* cfg, int device, cmt_engine** out) {
+  return guard(nullptr, [&] {
+    auto* h = new cmt_engine;
+    try {
+      h->eng = new Engine(*cfg, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+void cmt_destroy(cmt_engine* e) {
+  if (!e) return;
+  delete e->eng;
+  delete e;
+}
+const char* cmt_last_error(cmt_engine* e) { return e ? e->err.c_str() : g_err.c_str(); }
+int cmt_num_blocks(cmt_engine* e) { return (int)e->eng->blocks.size(); }
+int cmt_block_info(cmt_engine* e, int idx, char* name, int cap, long long* rows, long long* cols) {
+  return guard(e, [&] {
+    if (idx < 0 || idx >= (int)e->eng->blocks.size()) throw Error(cmt::CMT_ERR_SHAPE, "block index out of range");
+    auto& b = e->eng->blocks[idx];
+    std::snprintf(name, cap, "%s", b.name.c_str());
+    *rows = b.rows;
+    *cols = b.cols;
+  });
+}
+int cmt_upload_param(cmt_engine* e, int idx, const float* h, long long rows, long long cols) {
+  return guard(e, [&] { e->eng->upload(idx, h, rows, cols); });
+}
+int cmt_download_param(cmt_engine* e, int idx, float* h, long long rows, long long cols) {
+  return guard(e, [&] { e->eng->download(idx, h, rows, cols, false); });
+}
+int cmt_download_grad(cmt_engine* e, int idx, float* h, long long rows, long long cols) {
+  return guard(e, [&] { e->eng->download(idx, h, rows, cols, true); });
+}
+int cmt_stage_batch(cmt_engine* e, const long long* src, const float* sm, int S, const long long* tgt, const float* tm,
+                    int T, int B) {
+  return guard(e, [&] { e->eng->stage(src, sm, S, tgt, tm, T, B); });
+}
+int cmt_run_step(cmt_engine* e, const cmt_step_args* a, cmt_step_result* r) {
+  int rc = guard(e, [&] { e->eng->run(*a, r); });
+  if (rc == 0 && r && !(a->flags & CMT_FLAG_ASYNC) && r->status != 0) {
+    e->err = "numeric error in train step";
+    return r->status;
+  }
+  return rc;
+}
+int cmt_train_step(cmt_engine* e, const long long* src, const float* sm, int S, const long long* tgt, const float* tm,
+                   int T, int B, const cmt_step_args* a, cmt_step_result* r) {
+  int rc = cmt_stage_batch(e, src, sm, S, tgt, tm, T, B);
+  if (rc) return rc;
+  return cmt_run_step(e, a, r);
+}
+int cmt_wait(cmt_engine* e, cmt_step_result* r) {
+  int rc = guard(e, [&] { e->eng->wait(r); });
+  return rc ? rc : r->status;
+}
+int cmt_set_comm(cmt_engine* e, const void*, int rank, int world) {
+  return guard(e, [&] {
+    if (world != 1 || rank != 0) throw Error(cmt::CMT_ERR_INTERNAL, "NCCL data parallel not built in this version");
+  });
+}
+int cmt_event_record(cmt_engine* e, int slot) {
+  return guard(e, [&] { CMT_CUDA(cudaEventRecord(e->eng->ev[slot & 15], e->eng->st)); });
+}
+int cmt_event_elapsed(cmt_engine* e, int a, int b, float* ms) {
+  return guard(e, [&] {
+    CMT_CUDA(cudaEventSynchronize(e->eng->ev[b & 15]));
+    CMT_CUDA(cudaEventElapsedTime(ms, e->eng->ev[a & 15], e->eng->ev[b & 15]));
+  });
+}
+unsigned long long cmt_launch_count(void) { return cmt::g_launches; }
+
+// ---- test hooks (not part of the reference interface): single kernels on device pointers ----
+int cmt_test_gemm(int mode, int M, int N, int K, const void* A, long long lda, int a_mn, const void* B, long long ldb,
+                  int b_mn, float* C, long long ldc, int bn, int beta) {
+  return guard(nullptr, [&] {
+    cmt::EpiStore e;
+    e.C = C; e.ldc = ldc; e.beta = beta;
+    cmt::Mat a{A, lda, a_mn}, b{B, ldb, b_mn};
+    cudaStream_t st = 0;
+    if (mode == CMT_MODE_FP32) {
+      dim3 grid(cmt::ceil_div(N, 64), cmt::ceil_div(M, 64));
+      cmt::gemm_simt_kernel<cmt::EpiStore><<<grid, 256, 0, st>>>((const float*)A, lda, a_mn, (const float*)B, ldb, b_mn,
+                                                                   M, N, K, e);
+    } else {
+      int key = a_mn * 2 + b_mn;
+#define T_(BN_, AMN, BMN) else if (bn == BN_ && key == AMN * 2 + BMN) cmt::launch_tc<BN_, AMN, BMN, cmt::EpiStore>(st, M, N, K, a, b, e);
+      if (0) {}
+      T_(64, 0, 1) T_(128, 0, 1) T_(256, 0, 1) T_(64, 0, 0) T_(128, 0, 0) T_(256, 0, 0) T_(64, 1, 1) T_(128, 1, 1)
+      T_(256, 1, 1)
+      else throw Error(cmt::CMT_ERR_INTERNAL, "no such GEMM instantiation");
+#undef T_
+    }
+    CMT_CUDA(cudaGetLastError());
+    CMT_CUDA(cudaDeviceSynchronize());
+  });
+}
+int cmt_test_dropout(unsigned long long sh, unsigned long long sl, unsigned long long ih, unsigned long long il,
+                     unsigned long long base, int N, int H, double p, const float* x, float* y, unsigned char* keep) {
+  return guard(nullptr, [&] {
+    cmt::Pcg pcg{sh, sl, ih, il};
+    dim3 blk(32, 8), grid(cmt::ceil_div(H, 32), cmt::ceil_div(cmt::ceil_div(N, 32), 8));
+    cmt::dropout_fwd_kernel2<float, float><<<grid, blk>>>(x, y, keep, N, H, pcg, base, p, 1.0f / (float)(1.0 - p));
+    CMT_CUDA(cudaGetLastError());
+    CMT_CUDA(cudaDeviceSynchronize());
+  });
+}
+int cmt_set_option(cmt_engine* e, const char* key, long long value) {
+  return guard(e, [&] {
+    std::string k(key);
+    if (k == "time_dominant") e->eng->time_dominant = (int)value;
+    else throw Error(cmt::CMT_ERR_CONFIG, "unknown option " + k);
+  });
+}
+int cmt_get_stat(cmt_engine* e, const char* key, double* value, double* count) {
+  return guard(e, [&] {
+    std::string k(key);
+    if (k == "dominant_ms") *value = e->eng->dominant_ms(count);
+    else throw Error(cmt::CMT_ERR_CONFIG, "unknown stat " + k);
+  });
+}
+
+}  // extern "C"

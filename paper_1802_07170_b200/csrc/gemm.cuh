@@ -1,0 +1,438 @@
+// GEMM family for the train step.
+//
+// Logical contract: C[m][n] = epilogue( sum_k A(m,k) * B(n,k) ).
+//   A(m,k) lives at A + m*lda + k (K-major) or A + k*lda + m (MN-major),
+//   B(n,k) likewise.  Every GEMM of the step maps onto
+//   one of (A K-major, B MN-major) [forward: X @ W], (K, K) [dgrad: dY @ W^T]
+//   or (MN, MN) [wgrad: X^T @ dY] with weights kept in the reference's natural
+//   (dim_in, dim_out) layout — no transposed weight copies.
+//
+// Production (bf16): persistent warp-specialised tcgen05 kernel.  TMA loads
+// 128B-swizzled tiles into a multi-stage smem ring, one elected thread issues
+// tcgen05.mma (M=128, N=BN, K=16) into a double-buffered TMEM accumulator,
+// four epilogue warps drain TMEM with tcgen05.ld and run a fused epilogue
+// functor (bias/tanh/dropout-mask/accumulate, or the LSTM cell forward /
+// backward) while the next tile's MMAs proceed.
+//
+// Validation (fp32): a tiled SIMT kernel with the *same* epilogue functors, so
+// the fp32 validation mode exercises identical orchestration and cell math.
+#pragma once
+#include "ptx.cuh"
+
+namespace cmt {
+
+// ---------------------------------------------------------------------------
+// Epilogues.  apply(m, n0, v, M, N): v holds the 32 accumulator values of row
+// m, columns n0..n0+31 (columns >= N must be ignored).
+// ---------------------------------------------------------------------------
+
+struct EpiStore {
+  void* C = nullptr;
+  long long ldc = 0;
+  int c_bf16 = 0;
+  int beta = 0;                  // C += result (fp32 C only)
+  const float* add = nullptr;    // result += add[m*ld_add + n]
+  long long ld_add = 0;
+  const float* bias = nullptr;   // per column
+  int act = 0;                   // 1: tanh
+  const uint8_t* dmask = nullptr;  // dropout keep-mask (applied after act)
+  long long ld_dmask = 0;
+  float dscale = 1.f;
+  const float* tgrad_y = nullptr;  // multiply by (1 - y^2): tanh' from its output
+  long long ld_tgrad = 0;
+  float alpha = 1.f;
+
+  CMT_D void apply(int m, int n0, const float* v, int M, int N) const {
+    float x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      int n = n0 + j;
+      float t = alpha * v[j];
+      if (n < N) {
+        if (bias) t += bias[n];
+        if (act == 1) t = tanhf(t);
+        if (dmask) t = dmask[(long long)m * ld_dmask + n] ? t * dscale : 0.f * t;
+        if (tgrad_y) {
+          float yy = tgrad_y[(long long)m * ld_tgrad + n];
+          t *= (1.f - yy * yy);
+        }
+        if (add) t += add[(long long)m * ld_add + n];
+      }
+      x[j] = t;
+    }
+    long long base = (long long)m * ldc + n0;
+    bool full = (n0 + 32 <= N);
+    if (c_bf16) {
+      bf16* c = (bf16*)C + base;
+      if (full && ((((uintptr_t)c) & 15) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          __align__(16) bf16 tmp[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) tmp[j] = __float2bfloat16_rn(x[q * 8 + j]);
+          *(uint4*)(c + q * 8) = *(uint4*)tmp;
+        }
+      } else {
+        for (int j = 0; j < 32 && n0 + j < N; ++j) c[j] = __float2bfloat16_rn(x[j]);
+      }
+    } else {
+      float* c = (float*)C + base;
+      if (full && ((((uintptr_t)c) & 15) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 o = make_float4(x[q * 4], x[q * 4 + 1], x[q * 4 + 2], x[q * 4 + 3]);
+          if (beta) {
+            float4 old = *(float4*)(c + q * 4);
+            o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+          }
+          *(float4*)(c + q * 4) = o;
+        }
+      } else {
+        for (int j = 0; j < 32 && n0 + j < N; ++j) c[j] = beta ? c[j] + x[j] : x[j];
+      }
+    }
+  }
+};
+
+// LSTM forward cell fused into the recurrent GEMM of step t
+// (reference layers.py:344-363 cell, layers.py:453-464 mask gating).
+// Gate columns are interleaved: column 4*j+q is gate q (i,f,g,o) of unit j.
+struct EpiLstmFwd {
+  const float* ux;      // [rows][4H]  hoisted W_x x_t + b (row = row0 + m)
+  const void* hprev;    // act [rows][H] (h_{t-1}, row = row0 + m)
+  const float* cprev;   // [rows][H]
+  void* y;              // act [rows][H]  h_t (masked carry)
+  float* cst;           // [rows][H]      c_t (masked carry)
+  float* acts;          // [rows][4H]     i,f,g,o
+  float* tcache;        // [rows][H]      tanh(c_new)
+  const float* mask;    // [B] for this step, or null (decoder: unmasked)
+  long long row0;
+  int H;
+  int act_bf16;
+
+  CMT_D void apply(int m, int n0, const float* v, int M, int N) const {
+    long long row = row0 + m;
+    const float* uxr = ux + row * 4LL * H;
+    float mk = mask ? mask[m] : 1.f;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      int gc = n0 + 4 * jj;
+      if (gc >= N) break;
+      int j = gc >> 2;
+      float4 u4 = *(const float4*)(uxr + gc);
+      float gi = sigmoidf_(v[4 * jj + 0] + u4.x);
+      float gf = sigmoidf_(v[4 * jj + 1] + u4.y);
+      float gg = tanhf(v[4 * jj + 2] + u4.z);
+      float go = sigmoidf_(v[4 * jj + 3] + u4.w);
+      float cp = cprev[row * H + j];
+      float hp = act_bf16 ? __bfloat162float(((const bf16*)hprev)[row * H + j]) : ((const float*)hprev)[row * H + j];
+      float cn = __fadd_rn(__fmul_rn(gf, cp), __fmul_rn(gi, gg));
+      float tcn = tanhf(cn);
+      float hn = __fmul_rn(go, tcn);
+      float h = hn, c = cn;
+      if (mask) {
+        h = mk * hn + (1.f - mk) * hp;
+        c = mk * cn + (1.f - mk) * cp;
+      }
+      *(float4*)(acts + row * 4LL * H + gc) = make_float4(gi, gf, gg, go);
+      tcache[row * H + j] = tcn;
+      cst[row * H + j] = c;
+      if (act_bf16) ((bf16*)y)[row * H + j] = __float2bfloat16_rn(h);
+      else ((float*)y)[row * H + j] = h;
+    }
+  }
+};
+
+// LSTM cell backward at time t fused into the dh GEMM (acc = W_h dU_{t_next}).
+// reference layers.py:366-395 (cell) and layers.py:477-490 (mask split).
+struct EpiLstmBwd {
+  const float* dy;      // [rows][H] grad of this layer's output (row = row0 + m)
+  float* dhc;           // [B][H] carry (1-m) dh from the later step, in/out
+  float* dc;            // [B][H] cell grad carry, in/out
+  const float* acts;    // [rows][4H]
+  const float* tcache;  // [rows][H]
+  const float* cprev;   // [rows][H]
+  const float* mask;    // [B] or null
+  void* dU;             // act [rows][4H]
+  long long row0;
+  int H;
+  int act_bf16;
+
+  CMT_D void apply(int m, int n0, const float* v, int M, int N) const {
+    long long row = row0 + m;
+    float mk = mask ? mask[m] : 1.f;
+    for (int jj = 0; jj < 32; ++jj) {
+      int j = n0 + jj;
+      if (j >= N) break;
+      long long bi = (long long)m * H + j;
+      float dh = v[jj] + dhc[bi] + dy[row * H + j];
+      float dcin = dc[bi];
+      float dhn = dh, dcn = dcin, dhcar = 0.f, dccar = 0.f;
+      if (mask) {
+        dhn = mk * dh; dcn = mk * dcin;
+        dhcar = (1.f - mk) * dh; dccar = (1.f - mk) * dcin;
+      }
+      float4 a = *(const float4*)(acts + row * 4LL * H + 4 * j);  // i f g o
+      float tc = tcache[row * H + j];
+      float cp = cprev[row * H + j];
+      float dct = dhn * a.w * (1.f - tc * tc) + dcn;
+      float di = dct * a.z * (a.x * (1.f - a.x));
+      float df = dct * cp * (a.y * (1.f - a.y));
+      float dg = dct * a.x * (1.f - a.z * a.z);
+      float dO = dhn * tc * (a.w * (1.f - a.w));
+      long long o = row * 4LL * H + 4 * j;
+      if (act_bf16) {
+        __align__(8) bf16 t4[4] = {__float2bfloat16_rn(di), __float2bfloat16_rn(df), __float2bfloat16_rn(dg),
+                                   __float2bfloat16_rn(dO)};
+        *(uint2*)((bf16*)dU + o) = *(uint2*)t4;
+      } else {
+        *(float4*)((float*)dU + o) = make_float4(di, df, dg, dO);
+      }
+      dc[bi] = dct * a.y + dccar;
+      dhc[bi] = dhcar;
+    }
+  }
+};
+
+// After the last BPTT step: grads of the initial state (layers.py:491-493).
+struct EpiInitGrad {
+  float* dh0;           // [B][H]
+  float* dc0;           // [B][H]
+  const float* dhc;
+  const float* dc;
+  int H;
+  CMT_D void apply(int m, int n0, const float* v, int M, int N) const {
+    for (int jj = 0; jj < 32; ++jj) {
+      int j = n0 + jj;
+      if (j >= N) break;
+      long long bi = (long long)m * H + j;
+      dh0[bi] = v[jj] + dhc[bi];
+      dc0[bi] = dc[bi];
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// tcgen05 persistent GEMM (bf16 -> fp32)
+// ---------------------------------------------------------------------------
+namespace tc {
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int NUM_THREADS = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 epilogue
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+};
+}  // namespace tc
+
+template <int BN, int A_MN, int B_MN, class Epi>
+__global__ void __launch_bounds__(tc::NUM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, Epi epi) {
+  using C = tc::Cfg<BN>;
+  constexpr int S = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * C::A_BYTES;
+  uint64_t* full = (uint64_t*)(smem + S * C::STAGE_BYTES);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int tiles_m = (M + tc::BM - 1) / tc::BM;
+  const int tiles_n = (N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = (K + tc::BK - 1) / tc::BK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    for (int i = 0; i < S; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 4);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && num_kb > 0) {
+      // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile % tiles_m) * tc::BM;
+        const int n0 = (tile / tiles_m) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* a = sA + stage * C::A_BYTES;
+          uint8_t* b = sB + stage * C::B_BYTES;
+          const int k0 = kb * tc::BK;
+          if (A_MN) {
+            ptx::tma_load_2d(&tmA, &full[stage], a, m0, k0);
+            ptx::tma_load_2d(&tmA, &full[stage], a + 64 * tc::BK * 2, m0 + 64, k0);
+          } else {
+            ptx::tma_load_2d(&tmA, &full[stage], a, k0, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int q = 0; q < BN / 64; ++q) ptx::tma_load_2d(&tmB, &full[stage], b + q * 64 * tc::BK * 2, n0 + q * 64, k0);
+          } else {
+            ptx::tma_load_2d(&tmB, &full[stage], b, k0, n0);
+          }
+          ptx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && num_kb > 0) {
+      // ===== MMA issuer =====
+      const uint32_t idesc = ptx::idesc_bf16(tc::BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int iter = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+        const int buf = iter & 1;
+        const uint32_t aphase = (iter >> 1) & 1;
+        ptx::mbar_wait(&tempty[buf], aphase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t dtm = tmem_base + buf * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = ptx::smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < tc::BK / 16; ++kk) {
+            uint64_t ad = A_MN ? ptx::smem_desc_sw128(a_addr + kk * 2048, 64 * tc::BK * 2, 1024)
+                               : ptx::smem_desc_sw128(a_addr + kk * 32, 16, 1024);
+            uint64_t bd = B_MN ? ptx::smem_desc_sw128(b_addr + kk * 2048, 64 * tc::BK * 2, 1024)
+                               : ptx::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
+            ptx::umma_bf16(dtm, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+          }
+          ptx::umma_commit(&empty[stage]);
+          if (kb == num_kb - 1) ptx::umma_commit(&tfull[buf]);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue =====
+    const int q = warp & 3;  // TMEM lane quarter accessible by this warp
+    int iter = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+      const int m0 = (tile % tiles_m) * tc::BM;
+      const int n0 = (tile / tiles_m) * BN;
+      const int buf = iter & 1;
+      const uint32_t aphase = (iter >> 1) & 1;
+      const int m = m0 + q * 32 + lane;
+      if (num_kb > 0) {
+        ptx::mbar_wait(&tfull[buf], aphase);
+        ptx::tc_fence_after();
+      }
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        if (num_kb > 0) {
+          ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN + c * 32, v);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        }
+        if (m < M && n0 + c * 32 < N) epi.apply(m, n0 + c * 32, v, M, N);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0 && num_kb > 0) ptx::mbar_arrive(&tempty[buf]);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp32 SIMT GEMM (validation mode), same epilogues.
+// ---------------------------------------------------------------------------
+template <class Epi>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict__ A, long long lda, int a_mn,
+                                                        const float* __restrict__ B, long long ldb, int b_mn, int M,
+                                                        int N, int K, Epi epi) {
+  __shared__ float As[16][65];
+  __shared__ float Bs[16][65];
+  __shared__ float Cs[64][65];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = tid; i < 16 * 64; i += 256) {
+      int kk, r;
+      if (a_mn) { kk = i / 64; r = i % 64; } else { r = i / 16; kk = i % 16; }
+      int m = m0 + r, k = k0 + kk;
+      float va = 0.f;
+      if (m < M && k < K) va = a_mn ? A[(long long)k * lda + m] : A[(long long)m * lda + k];
+      As[kk][r] = va;
+      if (b_mn) { kk = i / 64; r = i % 64; } else { r = i / 16; kk = i % 16; }
+      int n = n0 + r;
+      k = k0 + kk;
+      float vb = 0.f;
+      if (n < N && k < K) vb = b_mn ? B[(long long)k * ldb + n] : B[(long long)n * ldb + k];
+      Bs[kk][r] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Cs[ty + 16 * i][tx + 16 * j] = acc[i][j];
+  __syncthreads();
+  if (tid < 128) {
+    int r = tid >> 1, ch = tid & 1;
+    int m = m0 + r, n = n0 + ch * 32;
+    if (m < M && n < N) {
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = Cs[r][ch * 32 + j];
+      epi.apply(m, n, v, M, N);
+    }
+  }
+}
+
+}  // namespace cmt

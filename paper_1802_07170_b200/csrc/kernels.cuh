@@ -1,0 +1,503 @@
+// Memory-bound and small fused kernels of the train step: embedding gather /
+// deterministic scatter, PCG64-exact dropout, bidirectional sum, Luong
+// attention forward/backward, fused log-softmax + label-smoothed CE + grad,
+// column sums (bias grads), global-norm reduction and the clipped SGD update.
+#pragma once
+#include "common.cuh"
+
+namespace cmt {
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+template <typename T>
+CMT_D float ldf(const T* p, long long i) { return to_f<T>(p[i]); }
+
+CMT_D float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+CMT_D float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+CMT_D double warp_sumd(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Embedding (reference tensor.py:191-216, layers.py:79-113)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void gather_rows_kernel(const T* __restrict__ table, int E, const int* __restrict__ ids, int N,
+                                   T* __restrict__ out) {
+  int n = blockIdx.x;
+  if (n >= N) return;
+  const T* src = table + (long long)ids[n] * E;
+  T* dst = out + (long long)n * E;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) dst[e] = src[e];
+}
+
+// gout[u][:] = sum over positions p of segment u (in position order) of dX[pos[p]][:]
+// — the deterministic equivalent of np.add.at(table_grad, ids, dX.T).
+__global__ void scatter_compact_kernel(const float* __restrict__ dX, int E, const int* __restrict__ seg_off,
+                                       const int* __restrict__ seg_pos, int nseg, float* __restrict__ gout) {
+  int u = blockIdx.x;
+  if (u >= nseg) return;
+  int b = seg_off[u], e_ = seg_off[u + 1];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    float acc = 0.f;
+    for (int p = b; p < e_; ++p) acc += dX[(long long)seg_pos[p] * E + e];
+    gout[(long long)u * E + e] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// elementwise
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void add2_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ o, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    o[i] = from_f<T>(to_f<T>(a[i]) + to_f<T>(b[i]));
+}
+
+template <typename TS, typename TD>
+__global__ void copy2d_kernel(const TS* __restrict__ s, long long lds, TD* __restrict__ d, long long ldd, int rows,
+                              int cols) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)rows * cols;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long r = i / cols, c = i % cols;
+    d[r * ldd + c] = from_f<TD>(to_f<TS>(s[r * lds + c]));
+  }
+}
+
+__global__ void fill_kernel(float* p, long long n, float v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void to_bf16_kernel(const float* __restrict__ s, bf16* __restrict__ d, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    d[i] = __float2bfloat16_rn(s[i]);
+}
+
+// ---------------------------------------------------------------------------
+// PCG64 (numpy's default bit generator: 128-bit LCG + XSL-RR output) with
+// O(log n) jump-ahead, so every dropout element regenerates the exact double
+// numpy's Generator.random() draws for it (reference layers.py:283).
+// ---------------------------------------------------------------------------
+typedef unsigned __int128 u128;
+struct Pcg {
+  unsigned long long state_hi, state_lo, inc_hi, inc_lo;
+};
+CMT_D u128 pcg_mult() {
+  return ((u128)0x2360ed051fc65da4ULL << 64) | (u128)0x4385df649fccf645ULL;
+}
+CMT_D u128 pcg_advance(u128 state, u128 inc, unsigned long long delta) {
+  u128 cur_mult = pcg_mult(), cur_plus = inc, acc_mult = 1, acc_plus = 0;
+  while (delta) {
+    if (delta & 1) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * state + acc_plus;
+}
+CMT_D unsigned long long pcg_out(u128 s) {
+  unsigned long long hi = (unsigned long long)(s >> 64), lo = (unsigned long long)s;
+  unsigned rot = (unsigned)(s >> 122);
+  unsigned long long x = hi ^ lo;
+  return (x >> rot) | (x << ((64 - rot) & 63));
+}
+
+// y = x * keep/(1-p) for one dropout site of shape (H, N) in the reference's
+// C order: element (h, n) is draw (base + h*N + n).  Activations here are
+// token-major [n][h]; a warp covers 32 consecutive h, each thread 32
+// consecutive n of its h, so mask writes stay 32-byte coalesced.
+template <typename TI, typename TO>
+__global__ void dropout_fwd_kernel2(const TI* __restrict__ x, TO* __restrict__ y, uint8_t* __restrict__ keep, int N,
+                                   int H, Pcg pcg, unsigned long long base, double p, float scale) {
+  int h = blockIdx.x * 32 + threadIdx.x;
+  int n0 = (blockIdx.y * blockDim.y + threadIdx.y) * 32;
+  if (h >= H || n0 >= N) return;
+  u128 st = ((u128)pcg.state_hi << 64) | pcg.state_lo;
+  u128 inc = ((u128)pcg.inc_hi << 64) | pcg.inc_lo;
+  u128 s = pcg_advance(st, inc, base + (unsigned long long)h * N + n0);
+  const u128 mult = pcg_mult();
+  int nend = min(N, n0 + 32);
+  for (int n = n0; n < nend; ++n) {
+    s = s * mult + inc;
+    unsigned long long r = pcg_out(s);
+    double u = (double)(r >> 11) * (1.0 / 9007199254740992.0);
+    bool k = u >= p;
+    long long i = (long long)n * H + h;
+    keep[i] = k;
+    float xv = to_f<TI>(x[i]);
+    y[i] = from_f<TO>(k ? xv * scale : xv * 0.f);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Luong "general" attention, one CTA per sentence b (attention.py:46-84,
+// layers.py:183-215).  Hs rows n = s*B+b, queries n = t*B+b.
+// ---------------------------------------------------------------------------
+constexpr int ATT_THREADS = 256;
+constexpr int ATT_MAXP = 64;  // register tile: S*T <= 64*256
+constexpr int ATT_HC = 32;
+
+inline size_t attn_fwd_smem(int S, int T) { return sizeof(float) * ((size_t)T * (S + 1) + (size_t)(S + T) * (ATT_HC + 1)); }
+inline size_t attn_bwd_smem(int S, int T) {
+  return sizeof(float) * (2 * (size_t)T * (S + 1) + (size_t)(S + 2 * T) * (ATT_HC + 1));
+}
+
+// sc[t][s] = sum_h P[t][h] * Q[s][h] over all H (P rows t*B+b, Q rows s*B+b)
+template <typename TP, typename TQ>
+CMT_D void att_scores(const TP* P, long long ldp, const TQ* Q, long long ldq, int S, int T, int B, int H, int b,
+                      float* sc, float* tP, float* tQ) {
+  const int tid = threadIdx.x;
+  float acc[ATT_MAXP];
+#pragma unroll
+  for (int r = 0; r < ATT_MAXP; ++r) acc[r] = 0.f;
+  const int np = S * T;
+  for (int h0 = 0; h0 < H; h0 += ATT_HC) {
+    for (int i = tid; i < T * ATT_HC; i += ATT_THREADS) {
+      int t = i / ATT_HC, hh = i % ATT_HC;
+      tP[t * (ATT_HC + 1) + hh] = (h0 + hh < H) ? to_f<TP>(P[(long long)(t * B + b) * ldp + h0 + hh]) : 0.f;
+    }
+    for (int i = tid; i < S * ATT_HC; i += ATT_THREADS) {
+      int s = i / ATT_HC, hh = i % ATT_HC;
+      tQ[s * (ATT_HC + 1) + hh] = (h0 + hh < H) ? to_f<TQ>(Q[(long long)(s * B + b) * ldq + h0 + hh]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < ATT_MAXP; ++r) {
+      int q = tid + r * ATT_THREADS;
+      if (q < np) {
+        int t = q / S, s = q % S;
+        const float* pp = tP + t * (ATT_HC + 1);
+        const float* qq = tQ + s * (ATT_HC + 1);
+        float a = acc[r];
+#pragma unroll
+        for (int hh = 0; hh < ATT_HC; ++hh) a = fmaf(pp[hh], qq[hh], a);
+        acc[r] = a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < ATT_MAXP; ++r) {
+    int q = tid + r * ATT_THREADS;
+    if (q < np) sc[(q / S) * (S + 1) + (q % S)] = acc[r];
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(ATT_THREADS) attn_fwd_kernel(const T* __restrict__ Hs, const T* __restrict__ U,
+                                                               const float* __restrict__ src_mask, int S, int Tq,
+                                                               int B, int H, float* __restrict__ alpha,
+                                                               T* __restrict__ ctx, long long ldctx,
+                                                               int* __restrict__ status) {
+  extern __shared__ float sm[];
+  const int b = blockIdx.x;
+  float* sc = sm;                                // [T][S+1]
+  float* tP = sc + Tq * (S + 1);                 // [T][HC+1]
+  float* tQ = tP + Tq * (ATT_HC + 1);            // [S][HC+1]
+  att_scores(U, H, Hs, H, S, Tq, B, H, b, sc, tP, tQ);
+  // masked column softmax over s (additive -1e9 as in layers.py:190/202)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = warp; t < Tq; t += ATT_THREADS / 32) {
+    float* row = sc + t * (S + 1);
+    float mx = -INFINITY;
+    bool bad = false;
+    for (int s = lane; s < S; s += 32) {
+      float v = row[s] + (1.f - src_mask[s * B + b]) * -1e9f;
+      bad |= !isfinite(v);
+      row[s] = v;
+      mx = fmaxf(mx, v);
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int s = lane; s < S; s += 32) {
+      float e = expf(row[s] - mx);
+      row[s] = e;
+      sum += e;
+    }
+    sum = warp_sum(sum);
+    float inv = 1.f / sum;
+    for (int s = lane; s < S; s += 32) {
+      float a = row[s] / sum;
+      row[s] = a;
+      alpha[((long long)b * Tq + t) * S + s] = a;
+    }
+    (void)inv;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_SCORES);
+  }
+  __syncthreads();
+  // context: ctx[t][h] = sum_s alpha[t][s] Hs[s][h]
+  for (int h0 = 0; h0 < H; h0 += ATT_HC) {
+    for (int i = threadIdx.x; i < S * ATT_HC; i += ATT_THREADS) {
+      int s = i / ATT_HC, hh = i % ATT_HC;
+      tQ[s * (ATT_HC + 1) + hh] = (h0 + hh < H) ? to_f<T>(Hs[(long long)(s * B + b) * H + h0 + hh]) : 0.f;
+    }
+    __syncthreads();
+    const int hh = threadIdx.x & 31;
+    for (int t = threadIdx.x >> 5; t < Tq; t += ATT_THREADS / 32) {
+      const float* row = sc + t * (S + 1);
+      float a = 0.f;
+      for (int s = 0; s < S; ++s) a = fmaf(row[s], tQ[s * (ATT_HC + 1) + hh], a);
+      if (h0 + hh < H) ctx[(long long)(t * B + b) * ldctx + h0 + hh] = from_f<T>(a);
+    }
+    __syncthreads();
+  }
+}
+
+// backward: given dC (= dCst[:, :H], fp32), produce dHs (+=) and du (act).
+template <typename T>
+__global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(const T* __restrict__ Hs, const T* __restrict__ U,
+                                                               const float* __restrict__ alpha,
+                                                               const float* __restrict__ dC, long long lddc, int S,
+                                                               int Tq, int B, int H, float* __restrict__ dHs,
+                                                               T* __restrict__ dU) {
+  extern __shared__ float sm[];
+  const int b = blockIdx.x;
+  float* da = sm;                         // [T][S+1]  d alpha -> d scores
+  float* al = da + Tq * (S + 1);          // [T][S+1]  alpha
+  float* tP = al + Tq * (S + 1);          // [T][HC+1]
+  float* tQ = tP + Tq * (ATT_HC + 1);     // [S][HC+1]
+  float* tR = tQ + S * (ATT_HC + 1);      // [T][HC+1]
+  // d alpha[t][s] = sum_h dC[t][h] Hs[s][h]
+  att_scores(dC, lddc, Hs, H, S, Tq, B, H, b, da, tP, tQ);
+  for (int i = threadIdx.x; i < Tq * S; i += ATT_THREADS) {
+    int t = i / S, s = i % S;
+    al[t * (S + 1) + s] = alpha[((long long)b * Tq + t) * S + s];
+  }
+  __syncthreads();
+  // d scores = p * (g - sum_s p g)   (layers.py:210-215)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = warp; t < Tq; t += ATT_THREADS / 32) {
+    float* g = da + t * (S + 1);
+    const float* p = al + t * (S + 1);
+    float dot = 0.f;
+    for (int s = lane; s < S; s += 32) dot += p[s] * g[s];
+    dot = warp_sum(dot);
+    for (int s = lane; s < S; s += 32) g[s] = p[s] * (g[s] - dot);
+  }
+  __syncthreads();
+  const int hh = threadIdx.x & 31;
+  for (int h0 = 0; h0 < H; h0 += ATT_HC) {
+    for (int i = threadIdx.x; i < Tq * ATT_HC; i += ATT_THREADS) {
+      int t = i / ATT_HC, c = i % ATT_HC;
+      bool ok = h0 + c < H;
+      tP[t * (ATT_HC + 1) + c] = ok ? dC[(long long)(t * B + b) * lddc + h0 + c] : 0.f;
+      tR[t * (ATT_HC + 1) + c] = ok ? to_f<T>(U[(long long)(t * B + b) * H + h0 + c]) : 0.f;
+    }
+    for (int i = threadIdx.x; i < S * ATT_HC; i += ATT_THREADS) {
+      int s = i / ATT_HC, c = i % ATT_HC;
+      tQ[s * (ATT_HC + 1) + c] = (h0 + c < H) ? to_f<T>(Hs[(long long)(s * B + b) * H + h0 + c]) : 0.f;
+    }
+    __syncthreads();
+    // dHs[s][h] += sum_t alpha[t][s] dC[t][h] + dscores[t][s] U[t][h]
+    for (int s = threadIdx.x >> 5; s < S; s += ATT_THREADS / 32) {
+      float a = 0.f;
+      for (int t = 0; t < Tq; ++t)
+        a = fmaf(al[t * (S + 1) + s], tP[t * (ATT_HC + 1) + hh], fmaf(da[t * (S + 1) + s], tR[t * (ATT_HC + 1) + hh], a));
+      if (h0 + hh < H) dHs[(long long)(s * B + b) * H + h0 + hh] += a;
+    }
+    // du[t][h] = sum_s dscores[t][s] Hs[s][h]
+    for (int t = threadIdx.x >> 5; t < Tq; t += ATT_THREADS / 32) {
+      const float* g = da + t * (S + 1);
+      float a = 0.f;
+      for (int s = 0; s < S; ++s) a = fmaf(g[s], tQ[s * (ATT_HC + 1) + hh], a);
+      if (h0 + hh < H) dU[(long long)(t * B + b) * H + h0 + hh] = from_f<T>(a);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused log-softmax + label-smoothed CE + gradient (+ tanh'), one CTA per
+// token row of the [N_T][V] logits; the gradient overwrites the logits.
+// loss_n = lse - (1-eps) y_gold - (eps/V) sum_v y_v            (training.py:111-113)
+// d_v    = (e^{y_v-lse} - eps/V - (1-eps)[v=gold]) m_n / ntok  (training.py:116-119)
+// dpre_v = d_v (1 - y_v^2) when the output tanh is on           (layers.py:136-138)
+// ---------------------------------------------------------------------------
+constexpr int CE_THREADS = 512;
+template <typename T>
+__global__ void __launch_bounds__(CE_THREADS) ce_kernel(T* __restrict__ Y, int V, const int* __restrict__ tgt,
+                                                        const float* __restrict__ tmask, float eps, float inv_ntok,
+                                                        int tanh_on, float* __restrict__ losstok,
+                                                        int* __restrict__ status) {
+  __shared__ float red_m[CE_THREADS / 32], red_s[CE_THREADS / 32], red_y[CE_THREADS / 32];
+  __shared__ float bc[2];
+  const long long n = blockIdx.x;
+  T* row = Y + n * V;
+  float mx = -INFINITY, se = 0.f, sy = 0.f;
+  bool bad = false;
+  for (int v = threadIdx.x; v < V; v += CE_THREADS) {
+    float y = to_f<T>(row[v]);
+    bad |= !isfinite(y);
+    sy += y;
+    if (y > mx) {
+      se = se * expf(mx - y) + 1.f;
+      mx = y;
+    } else {
+      se += expf(y - mx);
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float wm = warp_max(mx);
+  se = (mx == -INFINITY) ? 0.f : se * expf(mx - wm);
+  se = warp_sum(se);
+  sy = warp_sum(sy);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_LOGITS);
+  if (lane == 0) { red_m[warp] = wm; red_s[warp] = se; red_y[warp] = sy; }
+  __syncthreads();
+  if (warp == 0) {
+    float m2 = lane < CE_THREADS / 32 ? red_m[lane] : -INFINITY;
+    float s2 = lane < CE_THREADS / 32 ? red_s[lane] : 0.f;
+    float y2 = lane < CE_THREADS / 32 ? red_y[lane] : 0.f;
+    float gm = warp_max(m2);
+    s2 = (m2 == -INFINITY) ? 0.f : s2 * expf(m2 - gm);
+    s2 = warp_sum(s2);
+    y2 = warp_sum(y2);
+    if (lane == 0) {
+      float lse = gm + logf(s2);
+      int g = tgt[n];
+      float gold = to_f<T>(row[g]);
+      float per = lse - (1.f - eps) * gold - (eps / (float)V) * y2;
+      // reference per_token = -((1-eps) lp_gold + (eps/V) sum lp)  with lp = y - lse
+      float m = tmask[n];
+      losstok[n] = per * m;
+      if (!isfinite(per)) atomicOr(status, ST_LOSS);
+      bc[0] = lse;
+      bc[1] = m * inv_ntok;
+    }
+  }
+  __syncthreads();
+  const float lse = bc[0], w = bc[1];
+  const int g = tgt[n];
+  const float eV = eps / (float)V;
+  for (int v = threadIdx.x; v < V; v += CE_THREADS) {
+    float y = to_f<T>(row[v]);
+    float d = expf(y - lse) - eV - (v == g ? (1.f - eps) : 0.f);
+    d *= w;
+    if (tanh_on) d *= (1.f - y * y);
+    row[v] = from_f<T>(d);
+  }
+}
+
+// deterministic sum of a float vector into a double (single CTA)
+__global__ void sum_to_double_kernel(const float* __restrict__ x, int n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a += (double)x[i];
+  a = warp_sumd(a);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sumd(v);
+    if (threadIdx.x == 0) *out = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Column sums (bias grads: layers.py:72-73, 391): partial over row chunks,
+// then a fixed-order combine -> deterministic.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void colsum_partial_kernel(const T* __restrict__ D, long long ld, int rows, int cols, int rows_per,
+                                      float* __restrict__ part) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  int r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
+  float a = 0.f;
+  for (int r = r0; r < r1; ++r) a += to_f<T>(D[(long long)r * ld + c]);
+  part[(long long)blockIdx.y * cols + c] = a;
+}
+__global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, int cols, float* __restrict__ out) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float a = 0.f;
+  for (int k = 0; k < chunks; ++k) a += part[(long long)k * cols + c];
+  out[c] = a;
+}
+
+// ---------------------------------------------------------------------------
+// Global-norm clip + SGD (training.py:123-142)
+// ---------------------------------------------------------------------------
+constexpr int NORM_BLOCKS = 592;  // 4 x 148 SMs
+__global__ void sumsq_partial_kernel(const float* __restrict__ g, long long n, double* __restrict__ part) {
+  __shared__ double red[32];
+  float a = 0.f;
+  double ad = 0.0;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int cnt = 0;
+  for (; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float v = g[i];
+    a = fmaf(v, v, a);
+    if (++cnt == 256) { ad += a; a = 0.f; cnt = 0; }
+  }
+  ad += a;
+  ad = warp_sumd(ad);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ad;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sumd(v);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+  }
+}
+
+// scal[0] = sum of squares, scal[1] = norm; s32 = fp32(lr * scale)
+__global__ void clip_scale_kernel(const double* __restrict__ part, int nparts, double lr, double clip,
+                                  double* __restrict__ scal, float* __restrict__ s32, int* __restrict__ status) {
+  if (threadIdx.x != 0) return;
+  double sq = 0.0;
+  for (int i = 0; i < nparts; ++i) sq += part[i];
+  double norm = sqrt(sq);
+  scal[0] = sq;
+  scal[1] = norm;
+  if (!isfinite(norm)) atomicOr(status, ST_NORM);
+  double scale = 1.0;
+  if (clip > 0.0 && norm > clip) scale = clip / norm;
+  *s32 = (float)(lr * scale);
+}
+
+constexpr int ST_ABORT = ST_SCORES | ST_LOGITS | ST_LOSS | ST_NORM;
+
+__global__ void sgd_dense_kernel(float* __restrict__ w, const float* __restrict__ g, bf16* __restrict__ shadow,
+                                 long long n, const float* __restrict__ s32, const int* __restrict__ status) {
+  if (*status & ST_ABORT) return;
+  const float s = *s32;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float nw = __fsub_rn(w[i], __fmul_rn(s, g[i]));
+    w[i] = nw;
+    if (shadow) shadow[i] = __float2bfloat16_rn(nw);
+  }
+}
+
+__global__ void sgd_rows_kernel(float* __restrict__ table, bf16* __restrict__ shadow, int E,
+                                const int* __restrict__ ids, int nrows, const float* __restrict__ gc,
+                                const float* __restrict__ s32, const int* __restrict__ status) {
+  if (*status & ST_ABORT) return;
+  int u = blockIdx.x;
+  if (u >= nrows) return;
+  const float s = *s32;
+  long long r = (long long)ids[u] * E;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    float nw = __fsub_rn(table[r + e], __fmul_rn(s, gc[(long long)u * E + e]));
+    table[r + e] = nw;
+    if (shadow) shadow[r + e] = __float2bfloat16_rn(nw);
+  }
+}
+
+}  // namespace cmt

@@ -1,0 +1,212 @@
+"""Python handle on one device engine (one model, one GPU).
+
+Wraps the C ABI (include/cytonmt_b200.h) with numpy marshalling: parameter
+upload/download by reference block name, batch staging, the step call, and
+the PCG64 bookkeeping that keeps the caller's ``Rng`` in lock-step with the
+reference (the device regenerates numpy's dropout draws bit-exactly; the
+caller's generator is then advanced by the number of draws consumed).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, MaskError, NumericError, ShapeError, ToolkitError
+
+_ERRORS = {
+    _lib.CMT_ERR_CONFIG: ConfigError,
+    _lib.CMT_ERR_MASK: MaskError,
+    _lib.CMT_ERR_SHAPE: ShapeError,
+    _lib.CMT_ERR_NUM_SCORES: NumericError,
+    _lib.CMT_ERR_NUM_LOGITS: NumericError,
+    _lib.CMT_ERR_NUM_LOSS: NumericError,
+    _lib.CMT_ERR_NUM_NORM: NumericError,
+}
+_NUMERIC_MSG = {
+    _lib.CMT_ERR_NUM_SCORES: "softmax_columns received non-finite input",
+    _lib.CMT_ERR_NUM_LOGITS: "log_softmax_columns received non-finite input",
+    _lib.CMT_ERR_NUM_LOSS: "training loss is not finite",
+    _lib.CMT_ERR_NUM_NORM: "gradient norm is not finite; step aborted",
+}
+
+
+def _fptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def _llptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong))
+
+
+def pcg_state(rng):
+    """(state_hi, state_lo, inc_hi, inc_lo) of a reference Rng / numpy Generator."""
+    gen = getattr(rng, "gen", rng)
+    st = gen.bit_generator.state
+    if st.get("bit_generator") != "PCG64":
+        raise ConfigError(f"dropout parity needs a PCG64 generator, got {st.get('bit_generator')}")
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    m = (1 << 64) - 1
+    return s >> 64, s & m, inc >> 64, inc & m
+
+
+def dropout_draws(cfg, S, T, B):
+    """Doubles the reference forward draws (SURVEY §3.1 order)."""
+    if cfg.dropout <= 0.0:
+        return 0
+    L, H = cfg.depth, cfg.hidden_size
+    return H * B * ((L - 1) * S + (L - 1) * T + T)
+
+
+class Engine:
+    def __init__(self, config, mode="bf16", device=0):
+        self.lib = _lib.load()
+        self.config = config
+        self.mode = mode
+        c = _lib.Config(int(config.vocab_size), int(config.embedding_size), int(config.hidden_size),
+                        int(config.depth), int(bool(config.output_tanh)), int(bool(config.shared_embeddings)),
+                        float(config.dropout), _lib.MODE_BF16 if mode == "bf16" else _lib.MODE_FP32)
+        h = ctypes.c_void_p()
+        rc = self.lib.cmt_create(ctypes.byref(c), int(device), ctypes.byref(h))
+        if rc:
+            raise self._exc(rc, self.lib.cmt_last_error(None))
+        self.h = h
+        self.blocks = []
+        name = ctypes.create_string_buffer(256)
+        r, cc = ctypes.c_longlong(), ctypes.c_longlong()
+        for i in range(self.lib.cmt_num_blocks(h)):
+            self._check(self.lib.cmt_block_info(h, i, name, 256, ctypes.byref(r), ctypes.byref(cc)))
+            self.blocks.append((name.value.decode(), (r.value, cc.value)))
+        self.index = {n: i for i, (n, _) in enumerate(self.blocks)}
+        self.last_draws = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.cmt_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- errors ----
+    @staticmethod
+    def _exc(rc, msg):
+        msg = msg.decode() if isinstance(msg, bytes) else str(msg)
+        cls = _ERRORS.get(rc, RuntimeError if rc in (_lib.CMT_ERR_CUDA, _lib.CMT_ERR_INTERNAL) else ToolkitError)
+        if rc in _NUMERIC_MSG:
+            msg = _NUMERIC_MSG[rc]
+        return cls(msg)
+
+    def _check(self, rc):
+        if rc:
+            raise self._exc(rc, self.lib.cmt_last_error(self.h))
+
+    # ---- parameters ----
+    def upload(self, params):
+        """params: reference ModelParams (blocks()) or {name: array}."""
+        items = params.items() if isinstance(params, dict) else ((b.name, b.var.data) for b in params.blocks())
+        seen = set()
+        for n, arr in items:
+            i = self.index[n]
+            a = np.ascontiguousarray(arr, dtype=np.float32)
+            if a.shape != self.blocks[i][1]:
+                raise ShapeError(f"{n}: shape {a.shape} != {self.blocks[i][1]}")
+            self._check(self.lib.cmt_upload_param(self.h, i, _fptr(a), a.shape[0], a.shape[1]))
+            seen.add(n)
+        missing = set(self.index) - seen
+        if missing:
+            raise ConfigError(f"upload is missing parameters {sorted(missing)}")
+
+    def _download(self, fn, name):
+        i = self.index[name]
+        out = np.empty(self.blocks[i][1], dtype=np.float32)
+        self._check(fn(self.h, i, _fptr(out), out.shape[0], out.shape[1]))
+        return out
+
+    def params(self):
+        return {n: self._download(self.lib.cmt_download_param, n) for n, _ in self.blocks}
+
+    def grads(self):
+        return {n: self._download(self.lib.cmt_download_grad, n) for n, _ in self.blocks}
+
+    def download_into(self, params):
+        for b in params.blocks():
+            np.copyto(b.var.data, self._download(self.lib.cmt_download_param, b.name).astype(b.var.data.dtype))
+
+    # ---- steps ----
+    def stage(self, src_ids, src_mask, tgt_ids, tgt_mask):
+        src = np.ascontiguousarray(src_ids, dtype=np.int64)
+        tgt = np.ascontiguousarray(tgt_ids, dtype=np.int64)
+        sm = np.ascontiguousarray(src_mask, dtype=np.float32)
+        tm = np.ascontiguousarray(tgt_mask, dtype=np.float32)
+        if src.ndim != 2 or tgt.ndim != 2 or src.shape[1] != tgt.shape[1] or sm.shape != src.shape \
+                or tm.shape != tgt.shape:
+            raise ShapeError(f"batch shapes disagree: src {src.shape} mask {sm.shape} tgt {tgt.shape} mask {tm.shape}")
+        S, B = src.shape
+        T = tgt.shape[0]
+        self._staged = (src, sm, tgt, tm)  # keep host buffers alive for the call
+        self._check(self.lib.cmt_stage_batch(self.h, _llptr(src), _fptr(sm), S, _llptr(tgt), _fptr(tm), T, B))
+        self.shape = (S, T, B)
+
+    def run(self, lr, clip, eps, rng=None, update=True, global_ntok=0.0, asynchronous=False):
+        """One step on the staged batch.  Advances ``rng`` by the draws used."""
+        st = pcg_state(rng) if rng is not None else (0, 0, 0, 1)
+        a = _lib.StepArgs(float(lr), float(clip) if clip is not None else -1.0, float(eps),
+                          st[0], st[1], st[2], st[3], float(global_ntok),
+                          (0 if update else _lib.FLAG_NO_UPDATE) | (_lib.FLAG_ASYNC if asynchronous else 0))
+        r = _lib.StepResult()
+        rc = self.lib.cmt_run_step(self.h, ctypes.byref(a), ctypes.byref(r))
+        self.last_draws = r.draws
+        if rng is not None and r.draws and rc in (0, _lib.CMT_ERR_NUM_SCORES, _lib.CMT_ERR_NUM_LOGITS,
+                                                    _lib.CMT_ERR_NUM_LOSS, _lib.CMT_ERR_NUM_NORM):
+            getattr(rng, "gen", rng).bit_generator.advance(int(r.draws))
+        self._check(rc)
+        return r
+
+    def wait(self):
+        r = _lib.StepResult()
+        self._check(self.lib.cmt_wait(self.h, ctypes.byref(r)))
+        return r
+
+    def step(self, batch, lr, clip, eps, rng=None, update=True):
+        """Stage + run: returns (loss, grad_norm)."""
+        src, tgt = batch.src_ids, batch.tgt_ids
+        try:
+            self.stage(src, batch.src_mask, tgt, batch.tgt_mask)
+        except ConfigError as e:
+            # the reference raises the empty-target ConfigError after its forward
+            # pass, so the dropout draws are consumed (training.py:149-153)
+            if "unmasked token" in str(e) and rng is not None:
+                S, B = np.shape(src)
+                n = dropout_draws(self.config, S, np.shape(tgt)[0], B)
+                if n:
+                    getattr(rng, "gen", rng).bit_generator.advance(n)
+            raise
+        r = self.run(lr, clip, eps, rng, update)
+        return r.loss, r.grad_norm
+
+    # ---- timing ----
+    def set_option(self, key, value):
+        self._check(self.lib.cmt_set_option(self.h, key.encode(), int(value)))
+
+    def stat(self, key):
+        v, c = ctypes.c_double(), ctypes.c_double()
+        self._check(self.lib.cmt_get_stat(self.h, key.encode(), ctypes.byref(v), ctypes.byref(c)))
+        return v.value, c.value
+
+    def record(self, slot):
+        self._check(self.lib.cmt_event_record(self.h, slot))
+
+    def elapsed_ms(self, a, b):
+        ms = ctypes.c_float()
+        self._check(self.lib.cmt_event_elapsed(self.h, a, b, ctypes.byref(ms)))
+        return ms.value
+
+
+def launch_count():
+    return _lib.load().cmt_launch_count()

@@ -1,0 +1,193 @@
+"""Whole-step GPU parity through the C ABI.
+
+* fp32 validation mode vs the REFERENCE's own outputs (golden fixtures from
+  tests/golden/make_golden.py): loss, every per-block gradient, the updated
+  weights, the gradient norm and the dropout RNG state, at 1e-4 norm-relative
+  (the north-star fp32 tolerance; metric of pkg/tests/helpers.py:80-81).
+* bf16 production mode vs the oracle at 2e-2 norm-relative.
+* error semantics: ConfigError / MaskError / NumericError with weights unchanged.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from oracle import minmt_oracle as O  # noqa: E402
+from tests.gpu_helpers import engine_step, oracle_step, scaled_params  # noqa: E402
+
+GOLDEN = ["toy", "toy_dropout", "ragged_clip", "notanh_shared", "deep_noclip"]
+FP32_TOL = 1e-4
+BF16_TOL = 2e-2
+
+
+def dims_of(g):
+    return O.Dims(int(g["V"]), int(g["E"]), int(g["H"]), int(g["L"]), float(g["dropout"]), bool(g["tanh"]),
+                  bool(g["shared"]))
+
+
+def golden_args(g):
+    clip = None if float(g["clip"]) < 0 else float(g["clip"])
+    batch = (g["src"], g["src_mask"], g["tgt"], g["tgt_mask"])
+    return batch, float(g["eps"]), float(g["lr"]), clip, int(g["seed"]) + 5
+
+
+@pytest.mark.parametrize("case", GOLDEN)
+def test_fp32_step_matches_reference_golden(golden, case):
+    g = golden(case)
+    d = dims_of(g)
+    names = [str(n) for n in g["names"]]
+    params = {n: g[f"init:{n}"] for n in names}
+    batch, eps, lr, clip, seed = golden_args(g)
+    # grads (no update)
+    loss, _, grads, _, _ = engine_step(d, params, batch, eps, lr, clip, seed, "fp32", update=False)
+    assert abs(loss - float(g["loss"])) <= FP32_TOL * abs(float(g["loss"]))
+    for n in names:
+        assert O.norm_rel_err(grads[n], g[f"grad:{n}"]) < FP32_TOL, n
+    # full step: norm, updated weights, RNG state
+    loss, norm, _, newp, gen = engine_step(d, params, batch, eps, lr, clip, seed, "fp32", update=True)
+    assert abs(norm - float(g["norm"])) <= FP32_TOL * float(g["norm"])
+    for n in names:
+        assert O.norm_rel_err(newp[n] - g[f"init:{n}"], g[f"new:{n}"] - g[f"init:{n}"]) < FP32_TOL, n
+    st = gen.bit_generator.state["state"]
+    ref = [int(x) for x in g["rng_state"]]
+    assert (st["state"] >> 64, st["state"] & ((1 << 64) - 1)) == (ref[0], ref[1])
+
+
+def test_fp32_tiny_config_checksums(golden):
+    """BASELINE configs[0] (V=1k, H=128, B=16, len 20) against reference checksums."""
+    from paper_1802_07170_b200.model import Model, ModelConfig, Rng
+    g = golden("tiny")
+    d = dims_of(g)
+    m = Model.new(ModelConfig(d.vocab, d.emb, d.hidden, d.depth, d.dropout), Rng(int(g["seed"])))
+    params = {b.name: b.var.data for b in m.params.blocks()}
+    batch, eps, lr, clip, seed = golden_args(g)
+    loss, _, grads, _, _ = engine_step(d, params, batch, eps, lr, clip, seed, "fp32", update=False)
+    assert abs(loss - float(g["loss"])) <= FP32_TOL * float(g["loss"])
+    for n, gr in grads.items():
+        ck = g[f"grad:{n}"]
+        gg = gr.astype(np.float64).ravel()
+        idx = np.linspace(0, gg.size - 1, num=min(16, gg.size)).astype(np.int64)
+        scale = max(np.abs(gg).max(), 1e-30)
+        assert abs(np.sqrt((gg * gg).sum()) - np.sqrt(ck[1])) <= FP32_TOL * np.sqrt(ck[1]) + 1e-12, n
+        assert np.abs(gg[idx] - ck[4:4 + idx.size]).max() <= FP32_TOL * scale, n
+
+
+BF16_CASES = {
+    # (V, E, H, L, B, S, T, dropout, tanh, shared, ragged, eps, clip)
+    "small_ragged": (64, 32, 32, 2, 8, 7, 6, 0.2, True, False, True, 0.1, 5.0),
+    "deep_shared_clip": (96, 16, 24, 3, 6, 5, 9, 0.1, True, True, True, 0.1, 0.02),
+    "notanh_b1": (40, 16, 16, 2, 1, 4, 3, 0.0, False, False, False, 0.0, None),
+    "tiny_cfg": (1000, 128, 128, 1, 16, 20, 20, 0.2, True, False, True, 0.1, 5.0),
+}
+
+
+@pytest.mark.parametrize("case", list(BF16_CASES))
+def test_bf16_step_matches_oracle(case):
+    V, E, H, L, B, S, T, p, tanh_, shared, ragged, eps, clip = BF16_CASES[case]
+    d = O.Dims(V, E, H, L, p, tanh_, shared)
+    params = scaled_params(d, 3, 0.1)
+    batch = O.synthetic_batch(V, S, T, B, seed=4, ragged=ragged)
+    lr, seed = 1.0, 21
+    ol, _, og, _, ogen = oracle_step(d, params, batch, eps, lr, clip, seed, update=False)
+    loss, _, grads, _, gen = engine_step(d, params, batch, eps, lr, clip, seed, "bf16", update=False)
+    assert abs(loss - ol) <= BF16_TOL * abs(ol)
+    for n in grads:
+        assert O.norm_rel_err(grads[n], og[n]) < BF16_TOL, (n, O.norm_rel_err(grads[n], og[n]))
+    assert gen.bit_generator.state == ogen.bit_generator.state
+    # updated weights (delta) vs the oracle's update
+    ol, onorm, _, op, _ = oracle_step(d, params, batch, eps, lr, clip, seed, update=True)
+    loss, norm, _, newp, _ = engine_step(d, params, batch, eps, lr, clip, seed, "bf16", update=True)
+    assert abs(norm - onorm) <= BF16_TOL * onorm
+    for n in newp:
+        assert O.norm_rel_err(newp[n] - params[n], op[n] - params[n]) < BF16_TOL, n
+
+
+@pytest.mark.slow
+def test_bf16_c2_config_matches_oracle():
+    """BASELINE configs[1]: 2-layer bi-enc 512, V=30k, B=64, len 50 (oracle ~6 s)."""
+    d = O.Dims(30000, 512, 512, 2, 0.2)
+    params = scaled_params(d, 5, 0.1)
+    batch = O.synthetic_batch(30000, 50, 50, 64, seed=0, ragged=True)
+    ol, _, og, _, _ = oracle_step(d, params, batch, 0.1, 1.0, 5.0, 5, update=False)
+    loss, _, grads, _, _ = engine_step(d, params, batch, 0.1, 1.0, 5.0, 5, "bf16", update=False)
+    assert abs(loss - ol) <= BF16_TOL * ol
+    worst = max(O.norm_rel_err(grads[n], og[n]) for n in grads)
+    assert worst < BF16_TOL, worst
+
+
+def test_fp32_c2_shape_matches_oracle_small_vocab():
+    d = O.Dims(512, 64, 64, 2, 0.2)
+    params = scaled_params(d, 8, 0.1)
+    batch = O.synthetic_batch(512, 30, 25, 32, seed=2, ragged=True)
+    ol, _, og, _, _ = oracle_step(d, params, batch, 0.1, 1.0, 5.0, 9, update=False)
+    loss, _, grads, _, _ = engine_step(d, params, batch, 0.1, 1.0, 5.0, 9, "fp32", update=False)
+    assert abs(loss - ol) <= FP32_TOL * ol
+    for n in grads:
+        assert O.norm_rel_err(grads[n], og[n]) < FP32_TOL, n
+
+
+# ---- error semantics ----
+
+def _small():
+    d = O.Dims(64, 16, 16, 2, 0.2)
+    return d, scaled_params(d, 1, 0.1), O.synthetic_batch(64, 5, 4, 4, seed=1)
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+def test_bad_token_id_raises_config_error(mode):
+    from paper_1802_07170_b200.errors import ConfigError
+    d, params, (src, sm, tgt, tm) = _small()
+    src = src.copy()
+    src[2, 1] = 64
+    with pytest.raises(ConfigError, match="token id 64 outside vocabulary of size 64"):
+        engine_step(d, params, (src, sm, tgt, tm), 0.1, 1.0, 5.0, 1, mode)
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+def test_fully_masked_column_raises_mask_error(mode):
+    from paper_1802_07170_b200.errors import MaskError
+    d, params, (src, sm, tgt, tm) = _small()
+    sm = sm.copy()
+    sm[:, 2] = 0
+    with pytest.raises(MaskError):
+        engine_step(d, params, (src, sm, tgt, tm), 0.1, 1.0, 5.0, 1, mode)
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+def test_nonfinite_aborts_without_update(mode):
+    from paper_1802_07170_b200.engine import Engine
+    from paper_1802_07170_b200.errors import NumericError
+    from paper_1802_07170_b200.model import Batch
+    from tests.gpu_helpers import cfg_of
+    d, params, (src, sm, tgt, tm) = _small()
+    params = {k: v.copy() for k, v in params.items()}
+    params["out.b"][3, 0] = np.inf     # logits non-finite -> NumericError, nothing moves
+    eng = Engine(cfg_of(d), mode=mode)
+    eng.upload(params)
+    with pytest.raises(NumericError):
+        eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, np.random.default_rng(0))
+    after = eng.params()
+    for n in params:
+        assert np.array_equal(after[n], params[n]), n
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+def test_drop_in_train_step_and_determinism(mode):
+    """training.train_step on the host mirror: reference semantics (loss float,
+    params updated, grads zero, rng advanced); two identical runs are bit-identical."""
+    from paper_1802_07170_b200 import training
+    from paper_1802_07170_b200.model import Batch, Model, ModelConfig, Rng, TrainConfig
+    outs = []
+    for _ in range(2):
+        m = Model.new(ModelConfig(80, 32, 32, 2, 0.2), Rng(3))
+        src, sm, tgt, tm = O.synthetic_batch(80, 6, 5, 8, seed=3, ragged=True)
+        rng = Rng(7)
+        losses = [training.train_step(m, Batch(src, tgt, sm, tm), TrainConfig(), 1.0, rng, mode=mode)
+                  for _ in range(3)]
+        assert all(isinstance(x, float) for x in losses) and losses[2] < losses[0]
+        assert all(not b.var.grad.any() for b in m.params.blocks())
+        outs.append((losses, {b.name: b.var.data.copy() for b in m.params.blocks()}, rng.gen.random()))
+    assert outs[0][0] == outs[1][0] and outs[0][2] == outs[1][2]
+    for n in outs[0][1]:
+        assert np.array_equal(outs[0][1][n], outs[1][1][n]), n
