@@ -106,9 +106,12 @@ unsigned long long cmt_launch_count(void);                   /* kernels launched
 int cmt_set_option(cmt_engine* e, const char* key, long long value); /* "time_dominant": CUDA-event the logits GEMM */
 int cmt_get_stat(cmt_engine* e, const char* key, double* value, double* count); /* "dominant_ms": mean launch ms */
 
+/* debug: copy an internal buffer (e.g. "Y", "yext:3", "dy:0") as fp32; *n = element count */
+int cmt_debug_buffer(cmt_engine* e, const char* name, float* out, long long cap, long long* n);
 /* test hooks (parity tests only; device pointers): one GEMM C = A B^T (fp32 out), one dropout site */
+/* flags: 1 = accumulate into C, 2 = bf16 C, 4 = tanh; bias may be NULL */
 int cmt_test_gemm(int mode, int M, int N, int K, const void* A, long long lda, int a_mn, const void* B, long long ldb,
-                  int b_mn, float* C, long long ldc, int bn, int beta);
+                  int b_mn, void* C, long long ldc, int bn, int flags, const float* bias);
 int cmt_test_dropout(unsigned long long state_hi, unsigned long long state_lo, unsigned long long inc_hi,
                      unsigned long long inc_lo, unsigned long long base, int N, int H, double p, const float* x,
                      float* y, unsigned char* keep);

@@ -244,6 +244,14 @@ class Engine {
 
   static size_t al(size_t x) { return (x + 63) & ~(size_t)63; }
 
+  // Host<->device copies are ordered on the engine stream: a plain cudaMemcpy
+  // from pageable memory may return before its DMA lands, racing kernels that
+  // run on this non-blocking stream (e.g. the bf16 shadow refresh).
+  void copy_sync(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    CMT_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, st));
+    CMT_CUDA(cudaStreamSynchronize(st));
+  }
+
   void build_registry() {
     n_tables = cfg.shared_embeddings ? 1 : 2;
     blocks.push_back({"src_embed", V, E, BK_EMB, 0, -1, -1, 0});
@@ -309,12 +317,12 @@ class Engine {
     const BlockInfo& b = blocks[idx];
     CMT_CUDA(cudaStreamSynchronize(st));
     if (b.kind == BK_EMB) {
-      CMT_CUDA(cudaMemcpy(emb_w[b.table], h, (size_t)rows * cols * 4, cudaMemcpyHostToDevice));
+      copy_sync(emb_w[b.table], h, (size_t)rows * cols * 4, cudaMemcpyHostToDevice);
       if (bf) refresh_shadow(emb_w[b.table], emb_sh[b.table], (size_t)rows * cols);
       return;
     }
     if (b.kind == BK_DENSE) {
-      CMT_CUDA(cudaMemcpy(dw + b.off, h, (size_t)rows * cols * 4, cudaMemcpyHostToDevice));
+      copy_sync(dw + b.off, h, (size_t)rows * cols * 4, cudaMemcpyHostToDevice);
       if (bf) refresh_shadow(dw + b.off, dsh + b.off, (size_t)rows * cols);
       return;
     }
@@ -324,16 +332,16 @@ class Engine {
       // gather the current interleaved matrix, patch gate q, write back
       size_t rowsW = ly.din + H;
       std::vector<float> tmp(rowsW * n4);
-      CMT_CUDA(cudaMemcpy(tmp.data(), dw + ly.w_off, tmp.size() * 4, cudaMemcpyDeviceToHost));
+      copy_sync(tmp.data(), dw + ly.w_off, tmp.size() * 4, cudaMemcpyDeviceToHost);
       for (size_t r = 0; r < rowsW; ++r)
         for (int j = 0; j < H; ++j) tmp[r * n4 + 4 * j + b.gate] = h[r * H + j];
-      CMT_CUDA(cudaMemcpy(dw + ly.w_off, tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice));
+      copy_sync(dw + ly.w_off, tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice);
       if (bf) refresh_shadow(dw + ly.w_off, dsh + ly.w_off, tmp.size());
     } else {
       std::vector<float> tmp(n4);
-      CMT_CUDA(cudaMemcpy(tmp.data(), dw + ly.b_off, n4 * 4, cudaMemcpyDeviceToHost));
+      copy_sync(tmp.data(), dw + ly.b_off, n4 * 4, cudaMemcpyDeviceToHost);
       for (int j = 0; j < H; ++j) tmp[4 * j + b.gate] = h[j];
-      CMT_CUDA(cudaMemcpy(dw + ly.b_off, tmp.data(), n4 * 4, cudaMemcpyHostToDevice));
+      copy_sync(dw + ly.b_off, tmp.data(), n4 * 4, cudaMemcpyHostToDevice);
       if (bf) refresh_shadow(dw + ly.b_off, dsh + ly.b_off, n4);
     }
   }
@@ -349,21 +357,21 @@ class Engine {
     const float* base = grad ? dg : dw;
     if (b.kind == BK_EMB) {
       if (!grad) {
-        CMT_CUDA(cudaMemcpy(h, emb_w[b.table], (size_t)rows * cols * 4, cudaMemcpyDeviceToHost));
+        copy_sync(h, emb_w[b.table], (size_t)rows * cols * 4, cudaMemcpyDeviceToHost);
       } else {
         std::memset(h, 0, (size_t)rows * cols * 4);
         int t = b.table;
         int n = nuniq[t];
         if (n > 0) {
           std::vector<float> gc((size_t)n * E);
-          CMT_CUDA(cudaMemcpy(gc.data(), gcomp[t], gc.size() * 4, cudaMemcpyDeviceToHost));
+          copy_sync(gc.data(), gcomp[t], gc.size() * 4, cudaMemcpyDeviceToHost);
           for (int u = 0; u < n; ++u) std::memcpy(h + (size_t)uniq_h[t][u] * E, &gc[(size_t)u * E], E * 4);
         }
       }
       return;
     }
     if (b.kind == BK_DENSE) {
-      CMT_CUDA(cudaMemcpy(h, base + b.off, (size_t)rows * cols * 4, cudaMemcpyDeviceToHost));
+      copy_sync(h, base + b.off, (size_t)rows * cols * 4, cudaMemcpyDeviceToHost);
       return;
     }
     const Layer& ly = layers[b.layer];
@@ -371,12 +379,12 @@ class Engine {
     if (b.kind == BK_LSTM_W) {
       size_t rowsW = ly.din + H;
       std::vector<float> tmp(rowsW * n4);
-      CMT_CUDA(cudaMemcpy(tmp.data(), base + ly.w_off, tmp.size() * 4, cudaMemcpyDeviceToHost));
+      copy_sync(tmp.data(), base + ly.w_off, tmp.size() * 4, cudaMemcpyDeviceToHost);
       for (size_t r = 0; r < rowsW; ++r)
         for (int j = 0; j < H; ++j) h[r * H + j] = tmp[r * n4 + 4 * j + b.gate];
     } else {
       std::vector<float> tmp(n4);
-      CMT_CUDA(cudaMemcpy(tmp.data(), base + ly.b_off, n4 * 4, cudaMemcpyDeviceToHost));
+      copy_sync(tmp.data(), base + ly.b_off, n4 * 4, cudaMemcpyDeviceToHost);
       for (int j = 0; j < H; ++j) h[j] = tmp[4 * j + b.gate];
     }
   }
@@ -557,6 +565,16 @@ class Engine {
       dim3 grid(ceil_div(N, 64), ceil_div(M, 64));
       gemm_simt_kernel<Epi><<<grid, 256, 0, st>>>((const float*)A.p, A.ld, A.mn, (const float*)Bm.p, Bm.ld, Bm.mn, M,
                                                    N, K, e);
+      CMT_LAUNCHED();
+      CMT_CUDA(cudaGetLastError());
+      return;
+    }
+    if (K < tc::BK) {
+      // tiny contraction (toy dims / K=0 BPTT start): TMA boxes would exceed the
+      // tensor extent, run the bf16 SIMT kernel with the same epilogue instead
+      dim3 grid(ceil_div(N, 64), ceil_div(M, 64));
+      gemm_simt_kernel<Epi, bf16><<<grid, 256, 0, st>>>((const bf16*)A.p, A.ld, A.mn, (const bf16*)Bm.p, Bm.ld, Bm.mn,
+                                                          M, N, K, e);
       CMT_LAUNCHED();
       CMT_CUDA(cudaGetLastError());
       return;
@@ -834,6 +852,7 @@ class Engine {
         dom_events.push_back({e0, e1});
       }
     }
+    if (stop_after == 1) { CMT_CUDA(cudaStreamSynchronize(st)); return; }
     // fused log-softmax + smoothed CE + grad (training.py:96-120, tensor.py:146-151)
     if (bf) ce_kernel<bf16><<<(int)NT, CE_THREADS, 0, st>>>((bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon, inv_ntok,
                                                            cfg.output_tanh, losstok, status_d);
@@ -843,6 +862,7 @@ class Engine {
     sum_to_double_kernel<<<1, 1024, 0, st>>>(losstok, (int)NT, losssum_d);
     CMT_LAUNCHED();
 
+    if (stop_after == 2) { CMT_CUDA(cudaStreamSynchronize(st)); return; }
     // ===== backward =====
     // output projection (layers.py:64-73): dW_o, db_o, dH_o (+ dropout bwd + tanh' of H_o)
     gemm(H, V, (int)NT, Mat{hin, H, 1}, Mat{Y, V, 1}, store(dg + off_wo, V, false));
@@ -939,9 +959,47 @@ class Engine {
       if (!(a.flags & CMT_FLAG_ASYNC)) wait(res);
     }
   }
+  // debug: copy an internal buffer (converted to fp32) to the host
+  long long debug_buffer(const std::string& name, float* out, long long cap) {
+    CMT_CUDA(cudaStreamSynchronize(st));
+    long long NS = (long long)S * B, NT = (long long)T * B;
+    const void* p = nullptr;
+    long long n = 0;
+    bool act = false;
+    auto lidx = [&](const std::string& s) { return std::stoi(s.substr(s.find(':') + 1)); };
+    if (name == "Xs") { p = Xs; n = NS * E; act = true; }
+    else if (name == "Xt") { p = Xt; n = NT * E; act = true; }
+    else if (name == "top") { p = top; n = NS * H; act = true; }
+    else if (name == "u_att") { p = u_att; n = NT * H; act = true; }
+    else if (name == "cst_att") { p = cst_att; n = NT * 2 * H; act = true; }
+    else if (name == "hod") { p = hod; n = NT * H; act = true; }
+    else if (name == "Y") { p = Y; n = NT * V; act = true; }
+    else if (name == "dhpre") { p = dhpre; n = NT * H; act = true; }
+    else if (name == "du_att") { p = du_att; n = NT * H; act = true; }
+    else if (name == "alpha") { p = alpha; n = (long long)B * T * S; }
+    else if (name == "ho") { p = ho; n = NT * H; }
+    else if (name == "dcst") { p = dcst; n = NT * 2 * H; }
+    else if (name == "dXemb") { p = dXemb; n = (NS + NT) * E; }
+    else if (name == "dtop") { p = dtop; n = NS * H; }
+    else if (name.rfind("yext:", 0) == 0) { int l = lidx(name); p = lw[l].yext; n = ((l <= L ? S : T) + 1LL) * B * H; act = true; }
+    else if (name.rfind("cext:", 0) == 0) { int l = lidx(name); p = lw[l].cext; n = ((l <= L ? S : T) + 1LL) * B * H; }
+    else if (name.rfind("acts:", 0) == 0) { int l = lidx(name); p = lw[l].acts; n = (l <= L ? S : T) * (long long)B * 4 * H; }
+    else if (name.rfind("dy:", 0) == 0) { int l = lidx(name); p = lw[l].dy; n = (l <= L ? S : T) * (long long)B * H; }
+    else throw Error(CMT_ERR_CONFIG, "unknown debug buffer " + name);
+    if (n > cap) throw Error(CMT_ERR_SHAPE, "debug buffer too small");
+    if (act && bf) {
+      std::vector<bf16> tmp(n);
+      copy_sync(tmp.data(), p, n * 2, cudaMemcpyDeviceToHost);
+      for (long long i = 0; i < n; ++i) out[i] = __bfloat162float(tmp[i]);
+    } else {
+      copy_sync(out, p, n * 4, cudaMemcpyDeviceToHost);
+    }
+    return n;
+  }
   unsigned long long last_draws = 0;
   double last_ntok = 1;
   int time_dominant = 0;
+  int stop_after = 0;  // debug: 1 = after the logits GEMM, 2 = after the CE
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> dom_events;
   // mean duration (ms) of the timed dominant-kernel launches since the last call
   double dominant_ms(double* count) {
@@ -1081,10 +1139,10 @@ unsigned long long cmt_launch_count(void) { return cmt::g_launches; }
 
 // ---- test hooks (not part of the reference interface): single kernels on device pointers ----
 int cmt_test_gemm(int mode, int M, int N, int K, const void* A, long long lda, int a_mn, const void* B, long long ldb,
-                  int b_mn, float* C, long long ldc, int bn, int beta) {
+                  int b_mn, void* C, long long ldc, int bn, int flags, const float* bias) {
   return guard(nullptr, [&] {
     cmt::EpiStore e;
-    e.C = C; e.ldc = ldc; e.beta = beta;
+    e.C = C; e.ldc = ldc; e.beta = flags & 1; e.c_bf16 = (flags >> 1) & 1; e.act = (flags >> 2) & 1; e.bias = bias;
     cmt::Mat a{A, lda, a_mn}, b{B, ldb, b_mn};
     cudaStream_t st = 0;
     if (mode == CMT_MODE_FP32) {
@@ -1118,8 +1176,12 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
   return guard(e, [&] {
     std::string k(key);
     if (k == "time_dominant") e->eng->time_dominant = (int)value;
+    else if (k == "stop_after") e->eng->stop_after = (int)value;
     else throw Error(cmt::CMT_ERR_CONFIG, "unknown option " + k);
   });
+}
+int cmt_debug_buffer(cmt_engine* e, const char* name, float* out, long long cap, long long* n) {
+  return guard(e, [&] { *n = e->eng->debug_buffer(name, out, cap); });
 }
 int cmt_get_stat(cmt_engine* e, const char* key, double* value, double* count) {
   return guard(e, [&] {

@@ -377,9 +377,9 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
 // ---------------------------------------------------------------------------
 // fp32 SIMT GEMM (validation mode), same epilogues.
 // ---------------------------------------------------------------------------
-template <class Epi>
-__global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict__ A, long long lda, int a_mn,
-                                                        const float* __restrict__ B, long long ldb, int b_mn, int M,
+template <class Epi, typename TI = float>
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const TI* __restrict__ A, long long lda, int a_mn,
+                                                        const TI* __restrict__ B, long long ldb, int b_mn, int M,
                                                         int N, int K, Epi epi) {
   __shared__ float As[16][65];
   __shared__ float Bs[16][65];
@@ -394,13 +394,13 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
       if (a_mn) { kk = i / 64; r = i % 64; } else { r = i / 16; kk = i % 16; }
       int m = m0 + r, k = k0 + kk;
       float va = 0.f;
-      if (m < M && k < K) va = a_mn ? A[(long long)k * lda + m] : A[(long long)m * lda + k];
+      if (m < M && k < K) va = to_f<TI>(a_mn ? A[(long long)k * lda + m] : A[(long long)m * lda + k]);
       As[kk][r] = va;
       if (b_mn) { kk = i / 64; r = i % 64; } else { r = i / 16; kk = i % 16; }
       int n = n0 + r;
       k = k0 + kk;
       float vb = 0.f;
-      if (n < N && k < K) vb = b_mn ? B[(long long)k * ldb + n] : B[(long long)n * ldb + k];
+      if (n < N && k < K) vb = to_f<TI>(b_mn ? B[(long long)k * ldb + n] : B[(long long)n * ldb + k]);
       Bs[kk][r] = vb;
     }
     __syncthreads();

@@ -190,6 +190,12 @@ class Engine:
         r = self.run(lr, clip, eps, rng, update)
         return r.loss, r.grad_norm
 
+    def debug_buffer(self, name, cap=1 << 28):
+        out = np.empty(cap, dtype=np.float32)
+        n = ctypes.c_longlong()
+        self._check(self.lib.cmt_debug_buffer(self.h, name.encode(), _fptr(out), cap, ctypes.byref(n)))
+        return out[:n.value].copy()
+
     # ---- timing ----
     def set_option(self, key, value):
         self._check(self.lib.cmt_set_option(self.h, key.encode(), int(value)))

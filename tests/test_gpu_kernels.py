@@ -24,7 +24,7 @@ def _gemm(mode, M, N, K, a_mn, b_mn, bn, beta=0, seed=0):
     lda = M if a_mn else K
     ldb = N if b_mn else K
     lib = _lib.load()
-    rc = lib.cmt_test_gemm(mode, M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, C.data_ptr(), N, bn, beta)
+    rc = lib.cmt_test_gemm(mode, M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, C.data_ptr(), N, bn, beta, None)
     assert rc == 0, lib.cmt_last_error(None)
     ref = Al.float() @ Bl.float().t() + (C0 if beta else 0)
     return C.cpu(), ref
