@@ -1145,7 +1145,11 @@ int cmt_test_gemm(int mode, int M, int N, int K, const void* A, long long lda, i
     e.C = C; e.ldc = ldc; e.beta = flags & 1; e.c_bf16 = (flags >> 1) & 1; e.act = (flags >> 2) & 1; e.bias = bias;
     cmt::Mat a{A, lda, a_mn}, b{B, ldb, b_mn};
     cudaStream_t st = 0;
-    if (mode == CMT_MODE_FP32) {
+    if (mode == CMT_MODE_BF16 && K < cmt::tc::BK) {  // same routing as the engine
+      dim3 grid(cmt::ceil_div(N, 64), cmt::ceil_div(M, 64));
+      cmt::gemm_simt_kernel<cmt::EpiStore, cmt::bf16><<<grid, 256, 0, st>>>((const cmt::bf16*)A, lda, a_mn,
+                                                                             (const cmt::bf16*)B, ldb, b_mn, M, N, K, e);
+    } else if (mode == CMT_MODE_FP32) {
       dim3 grid(cmt::ceil_div(N, 64), cmt::ceil_div(M, 64));
       cmt::gemm_simt_kernel<cmt::EpiStore><<<grid, 256, 0, st>>>((const float*)A, lda, a_mn, (const float*)B, ldb, b_mn,
                                                                    M, N, K, e);
