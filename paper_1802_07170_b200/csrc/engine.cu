@@ -26,6 +26,7 @@
 #include "../../include/cytonmt_b200.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "lstm_persistent.cuh"
 
 namespace cmt {
 unsigned long long g_launches = 0;
@@ -201,6 +202,8 @@ class Engine {
   int nuniq[2] = {0, 0};
   int nseg_pos[2] = {0, 0};
   double* normpart;
+  unsigned* flags;
+  int persistent = 1;  // option: persistent recurrent kernels in bf16 mode
   StepScalars* scal_d;
   StepOut* out_d;
   float* s32_d;
@@ -458,6 +461,7 @@ class Engine {
       gcomp[t] = carve<float>(cur, (NS + NT) * E * 4);
     }
     normpart = carve<double>(cur, 3 * NORM_BLOCKS * 8);
+    flags = carve<unsigned>(cur, 64 * 4);
     scal_d = carve<StepScalars>(cur, sizeof(StepScalars));
     out_d = carve<StepOut>(cur, sizeof(StepOut));
     s32_d = carve<float>(cur, 4);
@@ -629,6 +633,30 @@ class Engine {
     CMT_LAUNCHED();
   }
 
+  // ---- persistent recurrent kernels (bf16) ----
+  bool use_persistent() const {
+    return bf && persistent && (H % 64 == 0) && B <= 128 && (H / 16) <= g_num_sms &&
+           pr::smem_bytes(H) <= 227 * 1024;
+  }
+  template <typename P>
+  void launch_coop(void (*k)(const CUtensorMap, const CUtensorMap, P), int grid, const CUtensorMap& a,
+                   const CUtensorMap& b, const P& prm) {
+    size_t smem = pr::smem_bytes(H);
+    CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3(grid);
+    c.blockDim = dim3(pr::THREADS);
+    c.dynamicSmemBytes = smem;
+    c.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    c.attrs = at;
+    c.numAttrs = 1;
+    CMT_CUDA(cudaLaunchKernelEx(&c, k, a, b, prm));
+    CMT_LAUNCHED();
+  }
+
   // ---- LSTM scans ----
   struct ScanViews {
     void* ybase;        // y[0]
@@ -652,6 +680,19 @@ class Engine {
     e.bias = dw + ly.b_off;
     gemm((int)N, 4 * H, din, Mat{X, din, 0}, Mat{wv(ly.w_off), 4LL * H, 1}, e);
     ScanViews v = views(l, reverse);
+    if (use_persistent()) {
+      CUtensorMap tmH, tmW;
+      make_map(&tmH, lw[l].yext, H, (long long)(steps + 1) * B, H, 64, 128);
+      make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 64);
+      LstmFwdP prm;
+      prm.ux = ux; prm.y = (bf16*)v.ybase; prm.hprev = (const bf16*)v.hprev; prm.cst = v.cbase; prm.cprev = v.cprev;
+      prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.mask = mask; prm.flag = flags + (l & 31);
+      prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
+      prm.hrow0 = reverse ? B : 0;
+      CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
+      launch_coop(lstm_fwd_persistent, 4 * H / pr::FWD_NG, tmH, tmW, prm);
+      return;
+    }
     const void* Wh = (const char*)wv(ly.w_off) + (size_t)din * 4 * H * asz;
     for (int p = 0; p < steps; ++p) {
       int t = reverse ? steps - 1 - p : p;
@@ -678,6 +719,18 @@ class Engine {
     else CMT_CUDA(cudaMemsetAsync(dcc, 0, BH * 4, st));
     const void* WhN = (const char*)wv(ly.w_off) + (size_t)din * 4 * H * asz;  // rows din.. of [din+H][4H]
     auto time_of = [&](int p) { return reverse ? steps - 1 - p : p; };
+    if (use_persistent()) {
+      CUtensorMap tmA, tmW;
+      make_map(&tmA, dU, 4LL * H, N, 4LL * H, 64, 128);
+      make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 16);
+      LstmBwdP prm;
+      prm.dy = dy; prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.cprev = v.cprev; prm.mask = mask;
+      prm.dU = (bf16*)dU; prm.dh_final = dh_final; prm.dc_final = dc_final; prm.dh0 = dh0; prm.dc0 = dc0;
+      prm.flag = flags + 32 + (l & 31);
+      prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
+      CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
+      launch_coop(lstm_bwd_persistent, H / pr::BWD_NU, tmA, tmW, prm);
+    } else
     for (int p = steps - 1; p >= 0; --p) {
       int t = time_of(p);
       EpiLstmBwd f;
@@ -692,7 +745,7 @@ class Engine {
         gemm(B, H, 4 * H, Mat{a, 4LL * H, 0}, Mat{WhN, 4LL * H, 0}, f);
       }
     }
-    if (dh0) {
+    if (dh0 && !use_persistent()) {
       EpiInitGrad f{dh0, dc0, dhc, dcc, H};
       const void* a = (const char*)dU + (size_t)time_of(0) * B * 4 * H * asz;
       gemm(B, H, 4 * H, Mat{a, 4LL * H, 0}, Mat{WhN, 4LL * H, 0}, f);
@@ -1180,6 +1233,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
   return guard(e, [&] {
     std::string k(key);
     if (k == "time_dominant") e->eng->time_dominant = (int)value;
+    else if (k == "persistent") e->eng->persistent = (int)value;
     else if (k == "stop_after") e->eng->stop_after = (int)value;
     else throw Error(cmt::CMT_ERR_CONFIG, "unknown option " + k);
   });

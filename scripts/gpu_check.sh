@@ -3,7 +3,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 nvidia-smi -L > gpurun_out/gpu.txt 2>&1
-timeout -s KILL ${T_TESTS:-900} python -m pytest tests -m gpu -q --maxfail=15 -p no:cacheprovider ${PYTEST_ARGS} > gpurun_out/tests.txt 2>&1
+timeout -s KILL ${T_TESTS:-900} python -m pytest tests -m "${PYTEST_MARK:-gpu}" -q --maxfail=15 -p no:cacheprovider ${PYTEST_ARGS} > gpurun_out/tests.txt 2>&1
 echo "tests rc=$?" >> gpurun_out/tests.txt
 timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
 echo "smoke rc=$?" >> gpurun_out/smoke.txt

@@ -204,3 +204,29 @@ def test_drop_in_train_step_and_determinism(mode):
     assert outs[0][0] == outs[1][0] and outs[0][2] == outs[1][2]
     for n in outs[0][1]:
         assert np.array_equal(outs[0][1][n], outs[1][1][n]), n
+
+
+@pytest.mark.parametrize("case", [(256, 128, 128, 2, 32, 11, 9, True), (512, 64, 128, 3, 128, 7, 12, True),
+                                  (300, 64, 64, 1, 5, 13, 4, False)])
+def test_persistent_recurrence_matches_per_step_and_oracle(case):
+    """The persistent recurrent kernels (default in bf16) against the per-step
+    tcgen05 path and the oracle, masked + unmasked, forward + reverse scans."""
+    from paper_1802_07170_b200.engine import Engine
+    from paper_1802_07170_b200.model import Batch
+    from tests.gpu_helpers import cfg_of
+    V, E, H, L, B, S, T, ragged = case
+    d = O.Dims(V, E, H, L, 0.2)
+    params = scaled_params(d, 11, 0.1)
+    src, sm, tgt, tm = O.synthetic_batch(V, S, T, B, seed=6, ragged=ragged)
+    _, _, og, _, _ = oracle_step(d, params, (src, sm, tgt, tm), 0.1, 1.0, 5.0, 3, update=False)
+    out = {}
+    for pers in (0, 1):
+        eng = Engine(cfg_of(d), mode="bf16")
+        eng.set_option("persistent", pers)
+        eng.upload(params)
+        eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, np.random.Generator(np.random.PCG64(3)), update=False)
+        out[pers] = eng.grads()
+        eng.close()
+    for n in og:
+        assert O.norm_rel_err(out[1][n], out[0][n]) < BF16_TOL, n
+        assert O.norm_rel_err(out[1][n], og[n]) < BF16_TOL, n
