@@ -204,6 +204,8 @@ class Engine {
   double* normpart;
   unsigned* flags;
   int persistent = 1;  // option: persistent recurrent kernels in bf16 mode
+  int trace_layer = -1;  // debug: record per-step phase timestamps of this layer's forward scan
+  unsigned long long* trace_d = nullptr;
   StepScalars* scal_d;
   StepOut* out_d;
   float* s32_d;
@@ -635,8 +637,7 @@ class Engine {
 
   // ---- persistent recurrent kernels (bf16) ----
   bool use_persistent() const {
-    return bf && persistent && (H % 64 == 0) && B <= 128 && (H / 16) <= g_num_sms &&
-           pr::smem_bytes(H) <= 227 * 1024;
+    return bf && persistent && (H % 64 == 0) && B <= 128 && (H / 16) <= g_num_sms && pr::stages_for(H) >= 2;
   }
   template <typename P>
   void launch_coop(void (*k)(const CUtensorMap, const CUtensorMap, P), int grid, const CUtensorMap& a,
@@ -689,6 +690,8 @@ class Engine {
       prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.mask = mask; prm.flag = flags + (l & 31);
       prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
       prm.hrow0 = reverse ? B : 0;
+      prm.trace = (trace_layer == l) ? trace_d : nullptr;
+      prm.stages = pr::stages_for(H);
       CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
       launch_coop(lstm_fwd_persistent, 4 * H / pr::FWD_NG, tmH, tmW, prm);
       return;
@@ -728,6 +731,8 @@ class Engine {
       prm.dU = (bf16*)dU; prm.dh_final = dh_final; prm.dc_final = dc_final; prm.dh0 = dh0; prm.dc0 = dc0;
       prm.flag = flags + 32 + (l & 31);
       prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
+      prm.trace = nullptr;
+      prm.stages = pr::stages_for(H);
       CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
       launch_coop(lstm_bwd_persistent, H / pr::BWD_NU, tmA, tmW, prm);
     } else
@@ -1234,6 +1239,11 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     std::string k(key);
     if (k == "time_dominant") e->eng->time_dominant = (int)value;
     else if (k == "persistent") e->eng->persistent = (int)value;
+    else if (k == "trace_layer") {
+      e->eng->trace_layer = (int)value;
+      if (!e->eng->trace_d) CMT_CUDA(cudaMalloc(&e->eng->trace_d, 4096 * 8));
+      CMT_CUDA(cudaMemset(e->eng->trace_d, 0, 4096 * 8));
+    }
     else if (k == "stop_after") e->eng->stop_after = (int)value;
     else throw Error(cmt::CMT_ERR_CONFIG, "unknown option " + k);
   });
@@ -1245,6 +1255,13 @@ int cmt_get_stat(cmt_engine* e, const char* key, double* value, double* count) {
   return guard(e, [&] {
     std::string k(key);
     if (k == "dominant_ms") *value = e->eng->dominant_ms(count);
+    else if (k.rfind("trace:", 0) == 0) {
+      int i = std::stoi(k.substr(6));
+      unsigned long long v = 0;
+      CMT_CUDA(cudaStreamSynchronize(e->eng->st));
+      CMT_CUDA(cudaMemcpy(&v, e->eng->trace_d + i, 8, cudaMemcpyDeviceToHost));
+      *value = (double)v;
+    }
     else throw Error(cmt::CMT_ERR_CONFIG, "unknown stat " + k);
   });
 }

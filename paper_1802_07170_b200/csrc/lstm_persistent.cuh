@@ -20,11 +20,18 @@
 namespace cmt {
 namespace pr {
 constexpr int THREADS = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 cell epilogue
-constexpr int STAGES = 4;
+constexpr int MAX_STAGES = 8;
 constexpr int A_BYTES = 128 * 64 * 2;  // one [128 rows][64] bf16 k-block
 constexpr int FWD_NG = 64;             // gate columns per CTA
 constexpr int BWD_NU = 16;             // units per CTA
-inline size_t smem_bytes(int H) { return 1024 + (size_t)H * 128 + STAGES * A_BYTES + 256; }
+constexpr size_t SMEM_LIMIT = 227 * 1024;
+// as many TMA stages as fit beside the resident W_h slice (H*128 bytes)
+inline int stages_for(int H) {
+  long long room = (long long)SMEM_LIMIT - 1024 - 256 - (long long)H * 128;
+  long long s = room / A_BYTES;
+  return (int)(s > MAX_STAGES ? MAX_STAGES : s);
+}
+inline size_t smem_bytes(int H) { return 1024 + (size_t)H * 128 + (size_t)stages_for(H) * A_BYTES + 256; }
 }  // namespace pr
 
 struct LstmFwdP {
@@ -39,7 +46,14 @@ struct LstmFwdP {
   unsigned* flag;       // zeroed before launch
   int steps, B, H, din, reverse;
   int hrow0;            // row of h_{-1}(t=0) in the Yext tensor map
+  int stages;
+  unsigned long long* trace;  // debug: per-step phase timestamps of CTA 0 (or null)
 };
+CMT_D unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __global__ void __launch_bounds__(pr::THREADS, 1)
     lstm_fwd_persistent(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW, LstmFwdP p) {
@@ -48,9 +62,9 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
   const int KB = p.H / 64;
   uint8_t* sW = smem;                     // KB x [64 K rows][64 N] (MN-major atoms)
   uint8_t* sA = smem + (size_t)KB * 8192;  // STAGES x [128][64] (K-major)
-  uint64_t* full = (uint64_t*)(sA + pr::STAGES * pr::A_BYTES);
-  uint64_t* empty = full + pr::STAGES;
-  uint64_t* wfull = empty + pr::STAGES;
+  uint64_t* full = (uint64_t*)(sA + p.stages * pr::A_BYTES);
+  uint64_t* empty = full + pr::MAX_STAGES;
+  uint64_t* wfull = empty + pr::MAX_STAGES;
   uint64_t* tfull = wfull + 1;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
@@ -62,7 +76,7 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
   if (threadIdx.x == 0) {
     ptx::prefetch_tmap(&tmH);
     ptx::prefetch_tmap(&tmW);
-    for (int i = 0; i < pr::STAGES; ++i) {
+    for (int i = 0; i < p.stages; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1);
     }
@@ -90,12 +104,13 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
           while (ptx::ld_acquire(p.flag) < target) __nanosleep(20);
           ptx::fence_proxy_async_global();
         }
+        if (p.trace && blockIdx.x == 0) p.trace[s * 4 + 0] = gtimer();
         const int hrow = p.hrow0 + t * p.B;
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::tma_load_2d(&tmH, &full[stage], sA + stage * pr::A_BYTES, kb * 64, hrow);
           ptx::mbar_expect_tx(&full[stage], pr::A_BYTES);
-          if (++stage == pr::STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -120,7 +135,7 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
             ptx::umma_bf16(tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
           }
           ptx::umma_commit(&empty[stage]);
-          if (++stage == pr::STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
         ptx::umma_commit(tfull);
       }
@@ -142,28 +157,34 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
     }
     for (int s = 0; s < p.steps; ++s) {
       const int t = p.reverse ? p.steps - 1 - s : s;
+      const long long row = (long long)t * p.B + b;
+      // prefetch this step's inputs before waiting for the accumulator
+      float4 x[16];
+      float mk = 1.f;
+      if (valid) {
+        const float4* uxr = (const float4*)(p.ux + row * 4 * H + n0);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) x[u] = __ldg(uxr + u);
+        if (p.mask) mk = __ldg(p.mask + row);
+      }
       ptx::mbar_wait(tfull, s & 1);
       ptx::tc_fence_after();
+      if (p.trace && blockIdx.x == 0 && threadIdx.x == 128) p.trace[s * 4 + 1] = gtimer();
       float v[64];
       ptx::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16), v);
       ptx::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 32, v + 32);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(tempty);
+      float tcv[16];
       if (valid) {
-        const long long row = (long long)t * p.B + b;
-        const float4* uxr = (const float4*)(p.ux + row * 4 * H + n0);
-        float4* ar = (float4*)(p.acts + row * 4 * H + n0);
-        const float mk = p.mask ? p.mask[row] : 1.f;
-        float tcv[16];
         __align__(16) bf16 hb[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
-          const float4 x = uxr[u];
-          const float gi = ptx::sigmoid_fast(v[4 * u + 0] + x.x);
-          const float gf = ptx::sigmoid_fast(v[4 * u + 1] + x.y);
-          const float gg = ptx::tanh_fast(v[4 * u + 2] + x.z);
-          const float go = ptx::sigmoid_fast(v[4 * u + 3] + x.w);
+          const float gi = ptx::sigmoid_fast(v[4 * u + 0] + x[u].x);
+          const float gf = ptx::sigmoid_fast(v[4 * u + 1] + x[u].y);
+          const float gg = ptx::tanh_fast(v[4 * u + 2] + x[u].z);
+          const float go = ptx::sigmoid_fast(v[4 * u + 3] + x[u].w);
           const float cn = gf * c[u] + gi * gg;
           const float tcn = ptx::tanh_fast(cn);
           const float hn = go * tcn;
@@ -174,10 +195,26 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
             h[u] = hn;
             c[u] = cn;
           }
-          ar[u] = make_float4(gi, gf, gg, go);
+          x[u] = make_float4(gi, gf, gg, go);  // reuse: activations for the cache
           tcv[u] = tcn;
           hb[u] = __float2bfloat16_rn(h[u]);
         }
+        uint4* yr = (uint4*)(p.y + row * H + u0);
+        yr[0] = ((uint4*)hb)[0];
+        yr[1] = ((uint4*)hb)[1];
+      }
+      if (p.trace && blockIdx.x == 0 && threadIdx.x == 128) p.trace[s * 4 + 2] = gtimer();
+      // publish h_t (the only value other CTAs need), then write the BPTT caches
+      ptx::named_bar_sync(1, 128);
+      if (threadIdx.x == 128) {
+        __threadfence();
+        ptx::red_release_add(p.flag, 1u);
+        if (p.trace && blockIdx.x == 0) p.trace[s * 4 + 3] = gtimer();
+      }
+      if (valid) {
+        float4* ar = (float4*)(p.acts + row * 4 * H + n0);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) ar[u] = x[u];
         float4* tcr = (float4*)(p.tcache + row * H + u0);
         float4* csr = (float4*)(p.cst + row * H + u0);
 #pragma unroll
@@ -185,14 +222,6 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
           tcr[k] = make_float4(tcv[4 * k], tcv[4 * k + 1], tcv[4 * k + 2], tcv[4 * k + 3]);
           csr[k] = make_float4(c[4 * k], c[4 * k + 1], c[4 * k + 2], c[4 * k + 3]);
         }
-        uint4* yr = (uint4*)(p.y + row * H + u0);
-        yr[0] = ((uint4*)hb)[0];
-        yr[1] = ((uint4*)hb)[1];
-      }
-      ptx::named_bar_sync(1, 128);
-      if (threadIdx.x == 128) {
-        __threadfence();
-        ptx::red_release_add(p.flag, 1u);
       }
     }
   }
@@ -217,6 +246,8 @@ struct LstmBwdP {
   float* dc0;
   unsigned* flag;
   int steps, B, H, din, reverse;
+  int stages;
+  unsigned long long* trace;
 };
 
 __global__ void __launch_bounds__(pr::THREADS, 1)
@@ -226,9 +257,9 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
   const int KB = p.H / 16;                 // 4H / 64 k-blocks
   uint8_t* sW = smem;                      // KB x [16 rows][64 K] (K-major), 2 KB each
   uint8_t* sA = smem + (size_t)KB * 2048;  // STAGES x [128][64]
-  uint64_t* full = (uint64_t*)(sA + pr::STAGES * pr::A_BYTES);
-  uint64_t* empty = full + pr::STAGES;
-  uint64_t* wfull = empty + pr::STAGES;
+  uint64_t* full = (uint64_t*)(sA + p.stages * pr::A_BYTES);
+  uint64_t* empty = full + pr::MAX_STAGES;
+  uint64_t* wfull = empty + pr::MAX_STAGES;
   uint64_t* tfull = wfull + 1;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
@@ -241,7 +272,7 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
   if (threadIdx.x == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmW);
-    for (int i = 0; i < pr::STAGES; ++i) {
+    for (int i = 0; i < p.stages; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1);
     }
@@ -272,7 +303,7 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::tma_load_2d(&tmA, &full[stage], sA + stage * pr::A_BYTES, kb * 64, arow);
           ptx::mbar_expect_tx(&full[stage], pr::A_BYTES);
-          if (++stage == pr::STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -297,7 +328,7 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
             ptx::umma_bf16(tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
           }
           ptx::umma_commit(&empty[stage]);
-          if (++stage == pr::STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
         ptx::umma_commit(tfull);
       }
@@ -314,6 +345,27 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
       dc[u] = (valid && p.dc_final) ? p.dc_final[(long long)b * H + u0 + u] : 0.f;
     }
     for (int i = 0; i < rounds; ++i) {
+      const bool cell = i < p.steps;
+      const int t = cell ? time_of(p.steps - 1 - i) : 0;
+      const long long row = (long long)t * p.B + b;
+      // prefetch the cell inputs of this round before waiting for the accumulator
+      float4 dy4[4], tc4[4], cp4[4], a4[16];
+      float mk = 1.f;
+      if (valid && cell) {
+        const float4* dyr = (const float4*)(p.dy + row * H + u0);
+        const float4* tcr = (const float4*)(p.tcache + row * H + u0);
+        const float4* cpr = (const float4*)(p.cprev + row * H + u0);
+        const float4* ar = (const float4*)(p.acts + row * 4 * H + 4 * u0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          dy4[k] = __ldg(dyr + k);
+          tc4[k] = __ldg(tcr + k);
+          cp4[k] = __ldg(cpr + k);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) a4[u] = __ldg(ar + u);
+        if (p.mask) mk = __ldg(p.mask + row);
+      }
       float acc[16];
       if (i > 0) {
         ptx::mbar_wait(tfull, (i - 1) & 1);
@@ -327,21 +379,13 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
         for (int u = 0; u < 16; ++u) acc[u] = 0.f;
       }
       if (valid) {
-        if (i < p.steps) {
-          const int t = time_of(p.steps - 1 - i);
-          const long long row = (long long)t * p.B + b;
-          const float mk = p.mask ? p.mask[row] : 1.f;
-          const float4* dyr = (const float4*)(p.dy + row * H + u0);
-          const float4* tcr = (const float4*)(p.tcache + row * H + u0);
-          const float4* cpr = (const float4*)(p.cprev + row * H + u0);
-          const float4* ar = (const float4*)(p.acts + row * 4 * H + 4 * u0);
+        if (cell) {
           __align__(16) bf16 du[64];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const float4 dy4 = dyr[k], tc4 = tcr[k], cp4 = cpr[k];
-            const float dyv[4] = {dy4.x, dy4.y, dy4.z, dy4.w};
-            const float tcv[4] = {tc4.x, tc4.y, tc4.z, tc4.w};
-            const float cpv[4] = {cp4.x, cp4.y, cp4.z, cp4.w};
+            const float dyv[4] = {dy4[k].x, dy4[k].y, dy4[k].z, dy4[k].w};
+            const float tcv[4] = {tc4[k].x, tc4[k].y, tc4[k].z, tc4[k].w};
+            const float cpv[4] = {cp4[k].x, cp4[k].y, cp4[k].z, cp4[k].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int u = 4 * k + e;
@@ -351,7 +395,7 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
                 dhn = mk * dh; dcn = mk * dc[u];
                 dhcar = (1.f - mk) * dh; dccar = (1.f - mk) * dc[u];
               }
-              const float4 a = ar[u];  // i f g o
+              const float4 a = a4[u];  // i f g o
               const float tc = tcv[e];
               const float dct = dhn * a.w * (1.f - tc * tc) + dcn;
               du[4 * u + 0] = __float2bfloat16_rn(dct * a.z * (a.x * (1.f - a.x)));
