@@ -637,7 +637,8 @@ class Engine {
 
   // ---- persistent recurrent kernels (bf16) ----
   bool use_persistent() const {
-    return bf && persistent && (H % 64 == 0) && B <= 128 && (H / 16) <= g_num_sms && pr::stages_for(H) >= 2;
+    return bf && persistent && (H % 64 == 0) && B <= 128 && (H / 16) * ceil_div(B, pr::ROWS) <= g_num_sms &&
+           pr::stages_for(H) >= 2;
   }
   template <typename P>
   void launch_coop(void (*k)(const CUtensorMap, const CUtensorMap, P), int grid, const CUtensorMap& a,
@@ -683,7 +684,7 @@ class Engine {
     ScanViews v = views(l, reverse);
     if (use_persistent()) {
       CUtensorMap tmH, tmW;
-      make_map(&tmH, lw[l].yext, H, (long long)(steps + 1) * B, H, 64, 128);
+      make_map(&tmH, lw[l].yext, H, (long long)(steps + 1) * B, H, 64, pr::ROWS);
       make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 64);
       LstmFwdP prm;
       prm.ux = ux; prm.y = (bf16*)v.ybase; prm.hprev = (const bf16*)v.hprev; prm.cst = v.cbase; prm.cprev = v.cprev;
@@ -693,7 +694,7 @@ class Engine {
       prm.trace = (trace_layer == l) ? trace_d : nullptr;
       prm.stages = pr::stages_for(H);
       CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
-      launch_coop(lstm_fwd_persistent, 4 * H / pr::FWD_NG, tmH, tmW, prm);
+      launch_coop(lstm_fwd_persistent, 4 * H / pr::FWD_NG * ceil_div(B, pr::ROWS), tmH, tmW, prm);
       return;
     }
     const void* Wh = (const char*)wv(ly.w_off) + (size_t)din * 4 * H * asz;
@@ -724,7 +725,7 @@ class Engine {
     auto time_of = [&](int p) { return reverse ? steps - 1 - p : p; };
     if (use_persistent()) {
       CUtensorMap tmA, tmW;
-      make_map(&tmA, dU, 4LL * H, N, 4LL * H, 64, 128);
+      make_map(&tmA, dU, 4LL * H, N, 4LL * H, 64, pr::ROWS);
       make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 16);
       LstmBwdP prm;
       prm.dy = dy; prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.cprev = v.cprev; prm.mask = mask;
@@ -734,7 +735,7 @@ class Engine {
       prm.trace = nullptr;
       prm.stages = pr::stages_for(H);
       CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
-      launch_coop(lstm_bwd_persistent, H / pr::BWD_NU, tmA, tmW, prm);
+      launch_coop(lstm_bwd_persistent, H / pr::BWD_NU * ceil_div(B, pr::ROWS), tmA, tmW, prm);
     } else
     for (int p = steps - 1; p >= 0; --p) {
       int t = time_of(p);

@@ -21,7 +21,9 @@ namespace cmt {
 namespace pr {
 constexpr int THREADS = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 cell epilogue
 constexpr int MAX_STAGES = 8;
-constexpr int A_BYTES = 128 * 64 * 2;  // one [128 rows][64] bf16 k-block
+constexpr int A_BYTES = 128 * 64 * 2;  // smem stage: [128 rows][64] bf16 (UMMA M=128 reads all rows)
+constexpr int ROWS = 64;               // batch rows per CTA; rows 64..127 of a stage are never loaded
+constexpr int LOAD_BYTES = ROWS * 64 * 2;
 constexpr int FWD_NG = 64;             // gate columns per CTA
 constexpr int BWD_NU = 16;             // units per CTA
 constexpr size_t SMEM_LIMIT = 227 * 1024;
@@ -71,8 +73,11 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
-  const int n0 = blockIdx.x * pr::FWD_NG;
+  const int nh = (p.B + pr::ROWS - 1) / pr::ROWS;
+  const int half = blockIdx.x % nh;
+  const int n0 = (blockIdx.x / nh) * pr::FWD_NG;
   const int u0 = n0 >> 2;
+  const int r0 = half * pr::ROWS;
   if (threadIdx.x == 0) {
     ptx::prefetch_tmap(&tmH);
     ptx::prefetch_tmap(&tmW);
@@ -82,7 +87,7 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
     }
     ptx::mbar_init(wfull, 1);
     ptx::mbar_init(tfull, 1);
-    ptx::mbar_init(tempty, 4);
+    ptx::mbar_init(tempty, 2);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 64);
@@ -101,15 +106,15 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
         const int t = p.reverse ? p.steps - 1 - s : s;
         if (s > 0) {
           const unsigned target = (unsigned)(G * s);
-          while (ptx::ld_acquire(p.flag) < target) __nanosleep(20);
+          while (ptx::ld_acquire(p.flag) < target) {}
           ptx::fence_proxy_async_global();
         }
         if (p.trace && blockIdx.x == 0) p.trace[s * 4 + 0] = gtimer();
-        const int hrow = p.hrow0 + t * p.B;
+        const int hrow = p.hrow0 + t * p.B + r0;
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::tma_load_2d(&tmH, &full[stage], sA + stage * pr::A_BYTES, kb * 64, hrow);
-          ptx::mbar_expect_tx(&full[stage], pr::A_BYTES);
+          ptx::mbar_expect_tx(&full[stage], pr::LOAD_BYTES);
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -140,10 +145,10 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
         ptx::umma_commit(tfull);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 6) {
     const int q = warp & 3;
-    const int b = q * 32 + lane;
-    const bool valid = b < p.B;
+    const int b = r0 + q * 32 + lane;
+    const bool valid = b < p.B && b < r0 + pr::ROWS;
     const long long H = p.H;
     float c[16], h[16];
     {
@@ -205,9 +210,8 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
       }
       if (p.trace && blockIdx.x == 0 && threadIdx.x == 128) p.trace[s * 4 + 2] = gtimer();
       // publish h_t (the only value other CTAs need), then write the BPTT caches
-      ptx::named_bar_sync(1, 128);
+      ptx::named_bar_sync(1, 64);
       if (threadIdx.x == 128) {
-        __threadfence();
         ptx::red_release_add(p.flag, 1u);
         if (p.trace && blockIdx.x == 0) p.trace[s * 4 + 3] = gtimer();
       }
@@ -266,7 +270,10 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
-  const int u0 = blockIdx.x * pr::BWD_NU;
+  const int nh = (p.B + pr::ROWS - 1) / pr::ROWS;
+  const int half = blockIdx.x % nh;
+  const int u0 = (blockIdx.x / nh) * pr::BWD_NU;
+  const int r0 = half * pr::ROWS;
   const int rounds = p.steps + (p.dh0 ? 1 : 0);
   auto time_of = [&](int pos) { return p.reverse ? p.steps - 1 - pos : pos; };
   if (threadIdx.x == 0) {
@@ -278,7 +285,7 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
     }
     ptx::mbar_init(wfull, 1);
     ptx::mbar_init(tfull, 1);
-    ptx::mbar_init(tempty, 4);
+    ptx::mbar_init(tempty, 2);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 32);
@@ -296,13 +303,13 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
       for (int i = 1; i < rounds; ++i) {
         // round i consumes dU of the position finished in round i-1
         const unsigned target = (unsigned)(G * i);
-        while (ptx::ld_acquire(p.flag) < target) __nanosleep(20);
+        while (ptx::ld_acquire(p.flag) < target) {}
         ptx::fence_proxy_async_global();
-        const int arow = time_of(p.steps - i) * p.B;
+        const int arow = time_of(p.steps - i) * p.B + r0;
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::tma_load_2d(&tmA, &full[stage], sA + stage * pr::A_BYTES, kb * 64, arow);
-          ptx::mbar_expect_tx(&full[stage], pr::A_BYTES);
+          ptx::mbar_expect_tx(&full[stage], pr::LOAD_BYTES);
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -333,10 +340,10 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
         ptx::umma_commit(tfull);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 6) {
     const int q = warp & 3;
-    const int b = q * 32 + lane;
-    const bool valid = b < p.B;
+    const int b = r0 + q * 32 + lane;
+    const bool valid = b < p.B && b < r0 + pr::ROWS;
     const long long H = p.H;
     float dhc[16], dc[16];
 #pragma unroll
@@ -417,11 +424,8 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
           }
         }
       }
-      ptx::named_bar_sync(1, 128);
-      if (threadIdx.x == 128) {
-        __threadfence();
-        ptx::red_release_add(p.flag, 1u);
-      }
+      ptx::named_bar_sync(1, 64);
+      if (threadIdx.x == 128) ptx::red_release_add(p.flag, 1u);
     }
   }
   ptx::tc_fence_before();
