@@ -50,7 +50,7 @@ struct EpiStore {
       float t = alpha * v[j];
       if (n < N) {
         if (bias) t += bias[n];
-        if (act == 1) t = tanhf(t);
+        if (act == 1) t = c_bf16 ? ptx::tanh_fast(t) : tanhf(t);
         if (dmask) t = dmask[(long long)m * ld_dmask + n] ? t * dscale : 0.f * t;
         if (tgrad_y) {
           float yy = tgrad_y[(long long)m * ld_tgrad + n];
@@ -73,7 +73,9 @@ struct EpiStore {
           *(uint4*)(c + q * 8) = *(uint4*)tmp;
         }
       } else {
-        for (int j = 0; j < 32 && n0 + j < N; ++j) c[j] = __float2bfloat16_rn(x[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (n0 + j < N) c[j] = __float2bfloat16_rn(x[j]);
       }
     } else {
       float* c = (float*)C + base;
@@ -88,7 +90,9 @@ struct EpiStore {
           *(float4*)(c + q * 4) = o;
         }
       } else {
-        for (int j = 0; j < 32 && n0 + j < N; ++j) c[j] = beta ? c[j] + x[j] : x[j];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (n0 + j < N) c[j] = beta ? c[j] + x[j] : x[j];
       }
     }
   }
@@ -218,7 +222,8 @@ struct EpiInitGrad {
 namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int NUM_THREADS = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 epilogue
+constexpr int NUM_THREADS = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 epilogue (2 per SMSP)
+constexpr int EPI_WARPS = 8;
 
 template <int BN>
 struct Cfg {
@@ -264,7 +269,7 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 4);
+      ptx::mbar_init(&tempty[i], tc::EPI_WARPS);
     }
     ptx::fence_barrier_init();
   }
@@ -286,7 +291,9 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * C::A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
-          const int k0 = kb * tc::BK;
+          // stagger the K order per tile so concurrent CTAs sharing an operand
+          // tile do not request the same L2 lines at the same moment
+          const int k0 = ((kb + tile) % num_kb) * tc::BK;
           if (A_MN) {
             ptx::tma_load_2d(&tmA, &full[stage], a, m0, k0);
             ptx::tma_load_2d(&tmA, &full[stage], a + 64 * tc::BK * 2, m0 + 64, k0);
@@ -337,8 +344,11 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===== epilogue =====
+    // ===== epilogue: warps 4-7 drain the first half of the columns, 8-11 the second =====
     const int q = warp & 3;  // TMEM lane quarter accessible by this warp
+    constexpr int NCH = BN / 32;
+    const int c_lo = (warp < 8) ? 0 : (NCH + 1) / 2;
+    const int c_hi = (warp < 8) ? (NCH + 1) / 2 : NCH;
     int iter = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
       const int m0 = (tile % tiles_m) * tc::BM;
@@ -351,7 +361,7 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
         ptx::tc_fence_after();
       }
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = c_lo; c < c_hi; ++c) {
         float v[32];
         if (num_kb > 0) {
           ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN + c * 32, v);

@@ -106,14 +106,16 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
         const int t = p.reverse ? p.steps - 1 - s : s;
         if (s > 0) {
           const unsigned target = (unsigned)(G * s);
-          while (ptx::ld_acquire(p.flag) < target) {}
+          while (ptx::ld_relaxed(p.flag) < target) {}
+          ptx::fence_acquire_gpu();
           ptx::fence_proxy_async_global();
         }
-        if (p.trace && blockIdx.x == 0) p.trace[s * 4 + 0] = gtimer();
+        if (p.trace && blockIdx.x == 0) p.trace[s * 8 + 0] = gtimer();
         const int hrow = p.hrow0 + t * p.B + r0;
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::tma_load_2d(&tmH, &full[stage], sA + stage * pr::A_BYTES, kb * 64, hrow);
+          const int kbe = (kb + blockIdx.x) % KB;  // stagger: CTAs start on different k-blocks
+          ptx::tma_load_2d(&tmH, &full[stage], sA + stage * pr::A_BYTES, kbe * 64, hrow);
           ptx::mbar_expect_tx(&full[stage], pr::LOAD_BYTES);
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
@@ -132,11 +134,13 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (p.trace && blockIdx.x == 0 && (kb == 0 || kb == 5 || kb == 6 || kb == KB - 1))
+            p.trace[s * 8 + 4 + (kb == 0 ? 0 : kb == 5 ? 1 : kb == 6 ? 2 : 3)] = gtimer();
           const uint32_t a = ptx::smem_u32(sA + stage * pr::A_BYTES);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             uint64_t ad = ptx::smem_desc_sw128(a + kk * 32, 16, 1024);
-            uint64_t bd = ptx::smem_desc_sw128(wbase + kb * 8192 + kk * 2048, 8192, 1024);
+            uint64_t bd = ptx::smem_desc_sw128(wbase + ((kb + blockIdx.x) % KB) * 8192 + kk * 2048, 8192, 1024);
             ptx::umma_bf16(tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
           }
           ptx::umma_commit(&empty[stage]);
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
       }
       ptx::mbar_wait(tfull, s & 1);
       ptx::tc_fence_after();
-      if (p.trace && blockIdx.x == 0 && threadIdx.x == 128) p.trace[s * 4 + 1] = gtimer();
+      if (p.trace && blockIdx.x == 0 && threadIdx.x == 128) p.trace[s * 8 + 1] = gtimer();
       float v[64];
       ptx::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16), v);
       ptx::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 32, v + 32);
@@ -208,12 +212,12 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
         yr[0] = ((uint4*)hb)[0];
         yr[1] = ((uint4*)hb)[1];
       }
-      if (p.trace && blockIdx.x == 0 && threadIdx.x == 128) p.trace[s * 4 + 2] = gtimer();
+      if (p.trace && blockIdx.x == 0 && threadIdx.x == 128) p.trace[s * 8 + 2] = gtimer();
       // publish h_t (the only value other CTAs need), then write the BPTT caches
       ptx::named_bar_sync(1, 64);
       if (threadIdx.x == 128) {
         ptx::red_release_add(p.flag, 1u);
-        if (p.trace && blockIdx.x == 0) p.trace[s * 4 + 3] = gtimer();
+        if (p.trace && blockIdx.x == 0) p.trace[s * 8 + 3] = gtimer();
       }
       if (valid) {
         float4* ar = (float4*)(p.acts + row * 4 * H + n0);
@@ -303,12 +307,14 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
       for (int i = 1; i < rounds; ++i) {
         // round i consumes dU of the position finished in round i-1
         const unsigned target = (unsigned)(G * i);
-        while (ptx::ld_acquire(p.flag) < target) {}
+        while (ptx::ld_relaxed(p.flag) < target) {}
+          ptx::fence_acquire_gpu();
         ptx::fence_proxy_async_global();
         const int arow = time_of(p.steps - i) * p.B + r0;
         for (int kb = 0; kb < KB; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::tma_load_2d(&tmA, &full[stage], sA + stage * pr::A_BYTES, kb * 64, arow);
+          const int kbe = (kb + blockIdx.x) % KB;
+          ptx::tma_load_2d(&tmA, &full[stage], sA + stage * pr::A_BYTES, kbe * 64, arow);
           ptx::mbar_expect_tx(&full[stage], pr::LOAD_BYTES);
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             uint64_t ad = ptx::smem_desc_sw128(a + kk * 32, 16, 1024);
-            uint64_t bd = ptx::smem_desc_sw128(wbase + kb * 2048 + kk * 32, 16, 1024);
+            uint64_t bd = ptx::smem_desc_sw128(wbase + ((kb + blockIdx.x) % KB) * 2048 + kk * 32, 16, 1024);
             ptx::umma_bf16(tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
           }
           ptx::umma_commit(&empty[stage]);
