@@ -60,6 +60,23 @@ static void make_map(CUtensorMap* m, const void* ptr, long long d0, long long d1
   if (r != CUDA_SUCCESS) throw Error(CMT_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
+// bf16 3-D map over a row-major [rows][cols] matrix viewed as {64, rows, cols/64}
+// (strides {ld*2, 128 B}): one TMA fetches `box2` consecutive 64-column blocks
+// of `box1` rows into smem as box2 stacked [box1][64] 128B-swizzled tiles.
+static void make_map_kblocks(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int box1,
+                             int box2) {
+  if (((uintptr_t)ptr & 15) || ((ld * 2) & 15) || (cols % 64))
+    throw Error(CMT_ERR_SHAPE, "k-block TMA map needs 16-byte aligned rows and cols % 64 == 0");
+  cuuint64_t gdim[3] = {64, (cuuint64_t)rows, (cuuint64_t)(cols / 64)};
+  cuuint64_t gstr[2] = {(cuuint64_t)(ld * 2), 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)box1, (cuuint32_t)box2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = get_encode()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), gdim, gstr, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(CMT_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string((int)r));
+}
+
 struct Mat {
   const void* p;
   long long ld;
@@ -637,7 +654,7 @@ class Engine {
 
   // ---- persistent recurrent kernels (bf16) ----
   bool use_persistent() const {
-    return bf && persistent && (H % 64 == 0) && B <= 128 && (H / 16) * ceil_div(B, pr::ROWS) <= g_num_sms &&
+    return bf && persistent && (H % (64 * pr::KBOX) == 0) && B <= 128 && (H / 16) * ceil_div(B, pr::ROWS) <= g_num_sms &&
            pr::stages_for(H) >= 2;
   }
   template <typename P>
@@ -684,7 +701,7 @@ class Engine {
     ScanViews v = views(l, reverse);
     if (use_persistent()) {
       CUtensorMap tmH, tmW;
-      make_map(&tmH, lw[l].yext, H, (long long)(steps + 1) * B, H, 64, pr::ROWS);
+      make_map_kblocks(&tmH, lw[l].yext, (long long)(steps + 1) * B, H, H, pr::ROWS, pr::KBOX);
       make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 64);
       LstmFwdP prm;
       prm.ux = ux; prm.y = (bf16*)v.ybase; prm.hprev = (const bf16*)v.hprev; prm.cst = v.cbase; prm.cprev = v.cprev;
@@ -725,7 +742,7 @@ class Engine {
     auto time_of = [&](int p) { return reverse ? steps - 1 - p : p; };
     if (use_persistent()) {
       CUtensorMap tmA, tmW;
-      make_map(&tmA, dU, 4LL * H, N, 4LL * H, 64, pr::ROWS);
+      make_map_kblocks(&tmA, dU, N, 4LL * H, 4LL * H, pr::ROWS, pr::KBOX);
       make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 16);
       LstmBwdP prm;
       prm.dy = dy; prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.cprev = v.cprev; prm.mask = mask;

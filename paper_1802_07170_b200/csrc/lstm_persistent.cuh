@@ -21,19 +21,23 @@ namespace cmt {
 namespace pr {
 constexpr int THREADS = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 cell epilogue
 constexpr int MAX_STAGES = 8;
-constexpr int A_BYTES = 128 * 64 * 2;  // smem stage: [128 rows][64] bf16 (UMMA M=128 reads all rows)
-constexpr int ROWS = 64;               // batch rows per CTA; rows 64..127 of a stage are never loaded
-constexpr int LOAD_BYTES = ROWS * 64 * 2;
+constexpr int ROWS = 64;               // batch rows per CTA (the other 64 accumulator rows are don't-care)
+constexpr int KBLK = ROWS * 128;       // one k-block tile in smem: [64 rows][64 cols] bf16 = 8 KB
+constexpr int KBOX = 4;                // k-blocks fetched per (3-D) TMA instruction = one pipeline stage
+constexpr int STAGE_BYTES = KBOX * KBLK;
+constexpr int PAD = KBLK;              // UMMA M=128 reads 128 rows: the last tile spills 8 KB past its stage
 constexpr int FWD_NG = 64;             // gate columns per CTA
 constexpr int BWD_NU = 16;             // units per CTA
 constexpr size_t SMEM_LIMIT = 227 * 1024;
 // as many TMA stages as fit beside the resident W_h slice (H*128 bytes)
 inline int stages_for(int H) {
-  long long room = (long long)SMEM_LIMIT - 1024 - 256 - (long long)H * 128;
-  long long s = room / A_BYTES;
+  long long room = (long long)SMEM_LIMIT - 1024 - 256 - PAD - (long long)H * 128;
+  long long s = room / STAGE_BYTES;
   return (int)(s > MAX_STAGES ? MAX_STAGES : s);
 }
-inline size_t smem_bytes(int H) { return 1024 + (size_t)H * 128 + (size_t)stages_for(H) * A_BYTES + 256; }
+inline size_t smem_bytes(int H) {
+  return 1024 + (size_t)H * 128 + (size_t)stages_for(H) * STAGE_BYTES + PAD + 256;
+}
 }  // namespace pr
 
 struct LstmFwdP {
@@ -63,8 +67,8 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int KB = p.H / 64;
   uint8_t* sW = smem;                     // KB x [64 K rows][64 N] (MN-major atoms)
-  uint8_t* sA = smem + (size_t)KB * 8192;  // STAGES x [128][64] (K-major)
-  uint64_t* full = (uint64_t*)(sA + p.stages * pr::A_BYTES);
+  uint8_t* sA = smem + (size_t)KB * 8192;  // stages x KBOX x [64 rows][64] (K-major) + pad
+  uint64_t* full = (uint64_t*)(sA + p.stages * pr::STAGE_BYTES + pr::PAD);
   uint64_t* empty = full + pr::MAX_STAGES;
   uint64_t* wfull = empty + pr::MAX_STAGES;
   uint64_t* tfull = wfull + 1;
@@ -112,11 +116,10 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
         }
         if (p.trace && blockIdx.x == 0) p.trace[s * 8 + 0] = gtimer();
         const int hrow = p.hrow0 + t * p.B + r0;
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = 0; kb < KB; kb += pr::KBOX) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          const int kbe = (kb + blockIdx.x) % KB;  // stagger: CTAs start on different k-blocks
-          ptx::tma_load_2d(&tmH, &full[stage], sA + stage * pr::A_BYTES, kbe * 64, hrow);
-          ptx::mbar_expect_tx(&full[stage], pr::LOAD_BYTES);
+          ptx::tma_load_3d(&tmH, &full[stage], sA + stage * pr::STAGE_BYTES, 0, hrow, kb);
+          ptx::mbar_expect_tx(&full[stage], pr::STAGE_BYTES);
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -131,17 +134,20 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
       for (int s = 0; s < p.steps; ++s) {
         ptx::mbar_wait(tempty, (s & 1) ^ 1);
         ptx::tc_fence_after();
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb0 = 0; kb0 < KB; kb0 += pr::KBOX) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          if (p.trace && blockIdx.x == 0 && (kb == 0 || kb == 5 || kb == 6 || kb == KB - 1))
-            p.trace[s * 8 + 4 + (kb == 0 ? 0 : kb == 5 ? 1 : kb == 6 ? 2 : 3)] = gtimer();
-          const uint32_t a = ptx::smem_u32(sA + stage * pr::A_BYTES);
+          if (p.trace && blockIdx.x == 0 && (kb0 == 0 || kb0 == KB - pr::KBOX))
+            p.trace[s * 8 + 4 + (kb0 == 0 ? 0 : 3)] = gtimer();
+          const uint32_t a0 = ptx::smem_u32(sA + stage * pr::STAGE_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            uint64_t ad = ptx::smem_desc_sw128(a + kk * 32, 16, 1024);
-            uint64_t bd = ptx::smem_desc_sw128(wbase + ((kb + blockIdx.x) % KB) * 8192 + kk * 2048, 8192, 1024);
-            ptx::umma_bf16(tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+          for (int j = 0; j < pr::KBOX; ++j) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              uint64_t ad = ptx::smem_desc_sw128(a0 + j * pr::KBLK + kk * 32, 16, 1024);
+              uint64_t bd = ptx::smem_desc_sw128(wbase + (kb0 + j) * 8192 + kk * 2048, 8192, 1024);
+              ptx::umma_bf16(tmem, ad, bd, idesc, (kb0 | j | kk) ? 1u : 0u);
+            }
           }
           ptx::umma_commit(&empty[stage]);
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
@@ -264,8 +270,8 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int KB = p.H / 16;                 // 4H / 64 k-blocks
   uint8_t* sW = smem;                      // KB x [16 rows][64 K] (K-major), 2 KB each
-  uint8_t* sA = smem + (size_t)KB * 2048;  // STAGES x [128][64]
-  uint64_t* full = (uint64_t*)(sA + p.stages * pr::A_BYTES);
+  uint8_t* sA = smem + (size_t)KB * 2048;  // stages x KBOX x [64 rows][64] + pad
+  uint64_t* full = (uint64_t*)(sA + p.stages * pr::STAGE_BYTES + pr::PAD);
   uint64_t* empty = full + pr::MAX_STAGES;
   uint64_t* wfull = empty + pr::MAX_STAGES;
   uint64_t* tfull = wfull + 1;
@@ -311,11 +317,10 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
           ptx::fence_acquire_gpu();
         ptx::fence_proxy_async_global();
         const int arow = time_of(p.steps - i) * p.B + r0;
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = 0; kb < KB; kb += pr::KBOX) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          const int kbe = (kb + blockIdx.x) % KB;
-          ptx::tma_load_2d(&tmA, &full[stage], sA + stage * pr::A_BYTES, kbe * 64, arow);
-          ptx::mbar_expect_tx(&full[stage], pr::LOAD_BYTES);
+          ptx::tma_load_3d(&tmA, &full[stage], sA + stage * pr::STAGE_BYTES, 0, arow, kb);
+          ptx::mbar_expect_tx(&full[stage], pr::STAGE_BYTES);
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -330,15 +335,18 @@ __global__ void __launch_bounds__(pr::THREADS, 1)
       for (int i = 1; i < rounds; ++i) {
         ptx::mbar_wait(tempty, ((i - 1) & 1) ^ 1);
         ptx::tc_fence_after();
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb0 = 0; kb0 < KB; kb0 += pr::KBOX) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a = ptx::smem_u32(sA + stage * pr::A_BYTES);
+          const uint32_t a0 = ptx::smem_u32(sA + stage * pr::STAGE_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            uint64_t ad = ptx::smem_desc_sw128(a + kk * 32, 16, 1024);
-            uint64_t bd = ptx::smem_desc_sw128(wbase + ((kb + blockIdx.x) % KB) * 2048 + kk * 32, 16, 1024);
-            ptx::umma_bf16(tmem, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+          for (int j = 0; j < pr::KBOX; ++j) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              uint64_t ad = ptx::smem_desc_sw128(a0 + j * pr::KBLK + kk * 32, 16, 1024);
+              uint64_t bd = ptx::smem_desc_sw128(wbase + (kb0 + j) * 2048 + kk * 32, 16, 1024);
+              ptx::umma_bf16(tmem, ad, bd, idesc, (kb0 | j | kk) ? 1u : 0u);
+            }
           }
           ptx::umma_commit(&empty[stage]);
           if (++stage == p.stages) { stage = 0; phase ^= 1; }

@@ -46,6 +46,16 @@ CMT_D void tma_load_2d(const void* tmap, uint64_t* bar, void* smem, int c0, int 
       : "memory");
 }
 
+// 3-D TMA tile load (used to fetch several 64-column k-blocks of a row-major
+// matrix in one instruction: dims {64, rows, K/64}, strides {ld*2, 128 B}).
+CMT_D void tma_load_3d(const void* tmap, uint64_t* bar, void* smem, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(smem)),
+      "l"((uint64_t)tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // ---- tcgen05 ----
 CMT_D void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),

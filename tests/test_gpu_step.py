@@ -206,8 +206,8 @@ def test_drop_in_train_step_and_determinism(mode):
         assert np.array_equal(outs[0][1][n], outs[1][1][n]), n
 
 
-@pytest.mark.parametrize("case", [(256, 128, 128, 2, 32, 11, 9, True), (512, 64, 128, 3, 128, 7, 12, True),
-                                  (304, 64, 64, 1, 5, 13, 4, False)])
+@pytest.mark.parametrize("case", [(256, 128, 256, 2, 32, 11, 9, True), (512, 64, 256, 3, 128, 7, 12, True),
+                                  (304, 64, 512, 1, 5, 13, 4, False), (256, 256, 256, 2, 96, 6, 5, True)])
 def test_persistent_recurrence_matches_per_step_and_oracle(case):
     """The persistent recurrent kernels (default in bf16) against the per-step
     tcgen05 path and the oracle, masked + unmasked, forward + reverse scans."""
