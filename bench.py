@@ -184,8 +184,9 @@ def main():
     src, sm, tgt, tm = synthetic_batch(V, S, T, B, seed=rank)
     batch = Batch(src, tgt, sm, tm)
     rng = Rng(5 + rank)
+    from paper_1802_07170_b200 import dp as dpmod
     ntok_local = float(tm.sum())
-    ntok_global = ntok_local * world
+    ntok_global = dpmod.global_ntok(tm, dist)
     lr, clip, eps = 1.0, 5.0, 0.1
 
     eng.stage(src, sm, tgt, tm)

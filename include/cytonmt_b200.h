@@ -96,8 +96,10 @@ int cmt_train_step(cmt_engine* e, const long long* src_ids, const float* src_mas
                    const cmt_step_args* args, cmt_step_result* res);
 int cmt_wait(cmt_engine* e, cmt_step_result* res);
 
-/* data parallel: NCCL communicator from a 128-byte ncclUniqueId */
+/* data parallel: NCCL communicator from a 128-byte ncclUniqueId (from cmt_nccl_unique_id on rank 0).
+   Grads, loss and status are summed over ranks inside every step; pass global_ntok in cmt_step_args. */
 int cmt_set_comm(cmt_engine* e, const void* nccl_unique_id, int rank, int world);
+int cmt_nccl_unique_id(void* out128);
 
 /* timing / introspection */
 int cmt_event_record(cmt_engine* e, int slot);               /* slot 0..15 on the engine stream */

@@ -32,7 +32,7 @@ FLAG_ASYNC = 2
 EXPORTS = [
     "cmt_create", "cmt_destroy", "cmt_last_error", "cmt_num_blocks", "cmt_block_info",
     "cmt_upload_param", "cmt_download_param", "cmt_download_grad", "cmt_stage_batch",
-    "cmt_run_step", "cmt_train_step", "cmt_wait", "cmt_set_comm", "cmt_event_record",
+    "cmt_run_step", "cmt_train_step", "cmt_wait", "cmt_set_comm", "cmt_nccl_unique_id", "cmt_event_record",
     "cmt_event_elapsed", "cmt_launch_count", "cmt_set_option", "cmt_get_stat", "cmt_debug_buffer", "cmt_test_gemm", "cmt_test_dropout",
 ]
 
@@ -85,6 +85,7 @@ def load(path=LIB_PATH):
     lib.cmt_train_step.argtypes = [VP, llp, fp, I, llp, fp, I, I, P(StepArgs), P(StepResult)]
     lib.cmt_wait.argtypes = [VP, P(StepResult)]
     lib.cmt_set_comm.argtypes = [VP, VP, I, I]
+    lib.cmt_nccl_unique_id.argtypes = [VP]
     lib.cmt_event_record.argtypes = [VP, I]
     lib.cmt_event_elapsed.argtypes = [VP, I, I, P(ctypes.c_float)]
     lib.cmt_launch_count.argtypes = []

@@ -77,6 +77,30 @@ static void make_map_kblocks(CUtensorMap* m, const void* ptr, long long rows, lo
   if (r != CUDA_SUCCESS) throw Error(CMT_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed: " + std::to_string((int)r));
 }
 
+// ---------------------------------------------------------------------------
+// NCCL, loaded at runtime (the process may already hold torch's libnccl.so.2)
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  void* h = nullptr;
+  int (*get_unique_id)(void*) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  const char* (*get_error)(int) = nullptr;
+  void load() {
+    if (h) return;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw Error(CMT_ERR_CUDA, std::string("cannot load libnccl.so.2: ") + dlerror());
+    get_unique_id = (int (*)(void*))dlsym(h, "ncclGetUniqueId");
+    all_reduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclAllReduce");
+    comm_destroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+    get_error = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+    if (!get_unique_id || !all_reduce || !comm_destroy) throw Error(CMT_ERR_CUDA, "libnccl.so.2 lacks symbols");
+  }
+};
+static NcclApi g_nccl;
+struct NcclUid { char internal[128]; };
+enum { NCCL_INT32 = 2, NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8, NCCL_SUM = 0 };
+
 struct Mat {
   const void* p;
   long long ld;
@@ -221,6 +245,31 @@ class Engine {
   double* normpart;
   unsigned* flags;
   int persistent = 1;  // option: persistent recurrent kernels in bf16 mode
+  // data parallel (NCCL): dense all-reduce of grads, loss and status
+  void* comm = nullptr;
+  int rank = 0, world = 1;
+  float* demb[2] = {nullptr, nullptr};  // dense embedding grads (DP only)
+  void nccl_check(int r, const char* what) {
+    if (r != 0)
+      throw Error(CMT_ERR_CUDA, std::string(what) + ": " + (g_nccl.get_error ? g_nccl.get_error(r) : "nccl error"));
+  }
+  void set_comm(const void* uid, int rank_, int world_) {
+    if (world_ < 1 || rank_ < 0 || rank_ >= world_) throw Error(CMT_ERR_CONFIG, "bad rank/world");
+    if (comm) throw Error(CMT_ERR_CONFIG, "communicator already set");
+    g_nccl.load();
+    typedef int (*InitFn)(void**, int, NcclUid, int);
+    InitFn init = (InitFn)dlsym(g_nccl.h, "ncclCommInitRank");
+    if (!init) throw Error(CMT_ERR_CUDA, "ncclCommInitRank missing");
+    NcclUid u;
+    std::memcpy(u.internal, uid, 128);
+    nccl_check(init(&comm, world_, u, rank_), "ncclCommInitRank");
+    rank = rank_;
+    world = world_;
+    for (int t = 0; t < n_tables; ++t) CMT_CUDA(cudaMalloc(&demb[t], (size_t)V * E * 4));
+  }
+  void allreduce(void* buf, size_t n, int dtype) {
+    nccl_check(g_nccl.all_reduce(buf, buf, n, dtype, NCCL_SUM, comm, st), "ncclAllReduce");
+  }
   int trace_layer = -1;  // debug: record per-step phase timestamps of this layer's forward scan
   unsigned long long* trace_d = nullptr;
   StepScalars* scal_d;
@@ -260,6 +309,8 @@ class Engine {
       if (i == 0 || !cfg.shared_embeddings) { cudaFree(emb_w[i]); cudaFree(emb_sh[i]); }
     }
     cudaFree(ws);
+    for (int t = 0; t < 2; ++t) if (demb[t]) cudaFree(demb[t]);
+    if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
     for (auto& e : ev) cudaEventDestroy(e);
     cudaStreamDestroy(st);
   }
@@ -1001,14 +1052,31 @@ class Engine {
       CMT_LAUNCHED();
     }
 
+    // ===== data parallel: sum grads / loss / status over ranks (NCCL) =====
+    const bool dp = comm != nullptr;  // (a 1-rank communicator exercises the same path)
+    if (dp) {
+      allreduce(dg, dense_n, NCCL_FLOAT32);
+      for (int t = 0; t < n_tables; ++t) {
+        CMT_CUDA(cudaMemsetAsync(demb[t], 0, (size_t)V * E * 4, st));
+        if (nuniq[t]) {
+          scatter_rows_kernel<<<nuniq[t], 128, 0, st>>>(gcomp[t], E, uniq_d[t], nuniq[t], demb[t]);
+          CMT_LAUNCHED();
+        }
+        allreduce(demb[t], (size_t)V * E, NCCL_FLOAT32);
+      }
+      allreduce(losssum_d, 1, NCCL_FLOAT64);
+      allreduce(status_d, 1, NCCL_INT32);
+    }
     // ===== global-norm clip + SGD (training.py:123-142) =====
     int nparts = 0;
     sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(dg, (long long)dense_n, normpart);
     CMT_LAUNCHED();
     nparts += NORM_BLOCKS;
     for (int t = 0; t < n_tables; ++t) {
-      if (nuniq[t] == 0) continue;
-      sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(gcomp[t], (long long)nuniq[t] * E, normpart + nparts);
+      if (!dp && nuniq[t] == 0) continue;
+      const float* gsrc = dp ? demb[t] : gcomp[t];
+      long long gn = dp ? (long long)V * E : (long long)nuniq[t] * E;
+      sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(gsrc, gn, normpart + nparts);
       CMT_LAUNCHED();
       nparts += NORM_BLOCKS;
     }
@@ -1019,6 +1087,12 @@ class Engine {
                                                                      status_d);
       CMT_LAUNCHED();
       for (int t = 0; t < n_tables; ++t) {
+        if (dp) {  // union of all ranks' rows: dense update (zero rows are exact no-ops)
+          sgd_dense_kernel<<<grid_for((long long)V * E), 256, 0, st>>>(emb_w[t], demb[t], bf ? emb_sh[t] : nullptr,
+                                                                      (long long)V * E, s32_d, status_d);
+          CMT_LAUNCHED();
+          continue;
+        }
         if (nuniq[t] == 0) continue;
         sgd_rows_kernel<<<nuniq[t], 128, 0, st>>>(emb_w[t], bf ? emb_sh[t] : nullptr, E, uniq_d[t], nuniq[t], gcomp[t],
                                                    s32_d, status_d);
@@ -1197,9 +1271,14 @@ int cmt_wait(cmt_engine* e, cmt_step_result* r) {
   int rc = guard(e, [&] { e->eng->wait(r); });
   return rc ? rc : r->status;
 }
-int cmt_set_comm(cmt_engine* e, const void*, int rank, int world) {
-  return guard(e, [&] {
-    if (world != 1 || rank != 0) throw Error(cmt::CMT_ERR_INTERNAL, "NCCL data parallel not built in this version");
+int cmt_set_comm(cmt_engine* e, const void* uid, int rank, int world) {
+  return guard(e, [&] { e->eng->set_comm(uid, rank, world); });
+}
+int cmt_nccl_unique_id(void* out128) {
+  return guard(nullptr, [&] {
+    cmt::g_nccl.load();
+    int r = cmt::g_nccl.get_unique_id(out128);
+    if (r) throw Error(cmt::CMT_ERR_CUDA, "ncclGetUniqueId failed");
   });
 }
 int cmt_event_record(cmt_engine* e, int slot) {

@@ -56,6 +56,14 @@ __global__ void scatter_compact_kernel(const float* __restrict__ dX, int E, cons
   }
 }
 
+// dense[ids[u]][:] = rows[u][:]   (compact embedding grads -> dense, for DP all-reduce)
+__global__ void scatter_rows_kernel(const float* __restrict__ rows, int E, const int* __restrict__ ids, int n,
+                                    float* __restrict__ dense) {
+  int u = blockIdx.x;
+  if (u >= n) return;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) dense[(long long)ids[u] * E + e] = rows[(long long)u * E + e];
+}
+
 // ---------------------------------------------------------------------------
 // elementwise
 // ---------------------------------------------------------------------------

@@ -196,6 +196,11 @@ class Engine:
         self._check(self.lib.cmt_debug_buffer(self.h, name.encode(), _fptr(out), cap, ctypes.byref(n)))
         return out[:n.value].copy()
 
+    # ---- data parallel ----
+    def set_dp(self, dist, rank, world):
+        from . import dp
+        dp.attach(self, dist, rank, world)
+
     # ---- timing ----
     def set_option(self, key, value):
         self._check(self.lib.cmt_set_option(self.h, key.encode(), int(value)))

@@ -230,3 +230,30 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
     for n in og:
         assert O.norm_rel_err(out[1][n], out[0][n]) < BF16_TOL, n
         assert O.norm_rel_err(out[1][n], og[n]) < BF16_TOL, n
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+def test_dp_path_single_rank_nccl_matches_plain(mode):
+    """The data-parallel branch (NCCL all-reduce of grads/loss/status, dense
+    embedding grads, union-of-rows update) on a 1-rank communicator equals the
+    plain single-GPU step."""
+    from paper_1802_07170_b200 import dp
+    from paper_1802_07170_b200.engine import Engine
+    from paper_1802_07170_b200.model import Batch
+    from tests.gpu_helpers import cfg_of
+    d = O.Dims(96, 32, 256, 2, 0.0)
+    params = scaled_params(d, 2, 0.1)
+    src, sm, tgt, tm = O.synthetic_batch(96, 7, 6, 8, seed=2, ragged=True)
+    out = []
+    for use_dp in (False, True):
+        eng = Engine(cfg_of(d), mode=mode)
+        eng.upload(params)
+        if use_dp:
+            dp.attach(eng, None, 0, 1)
+        loss, norm = eng.step(Batch(src, tgt, sm, tm), 1.0, 0.05, 0.1, None)
+        out.append((loss, norm, eng.params()))
+        eng.close()
+    assert abs(out[0][0] - out[1][0]) <= 1e-6 * abs(out[0][0])
+    assert abs(out[0][1] - out[1][1]) <= 1e-5 * out[0][1]
+    for n in out[0][2]:
+        assert O.norm_rel_err(out[1][2][n], out[0][2][n]) < 1e-6, n
