@@ -27,6 +27,7 @@
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "lstm_persistent.cuh"
+#include "lstm_cluster.cuh"
 
 namespace cmt {
 unsigned long long g_launches = 0;
@@ -245,6 +246,7 @@ class Engine {
   double* normpart;
   unsigned* flags;
   int persistent = 1;  // option: persistent recurrent kernels in bf16 mode
+  int clustered = 1;   // option: cluster K-split variant of the persistent kernels
   // data parallel (NCCL): dense all-reduce of grads, loss and status
   void* comm = nullptr;
   int rank = 0, world = 1;
@@ -708,21 +710,32 @@ class Engine {
     return bf && persistent && (H % (64 * pr::KBOX) == 0) && B <= 128 && (H / 16) * ceil_div(B, pr::ROWS) <= g_num_sms &&
            pr::stages_for(H) >= 2;
   }
+  bool use_cluster_fwd() const {
+    return use_persistent() && clustered && H % 256 == 0 && H / 8 <= g_num_sms && cl::fwd_stages(H) >= 2;
+  }
+  bool use_cluster_bwd() const {
+    return use_persistent() && clustered && H % 128 == 0 && H / 8 <= g_num_sms && cl::bwd_stages(H) >= 2;
+  }
   template <typename P>
   void launch_coop(void (*k)(const CUtensorMap, const CUtensorMap, P), int grid, const CUtensorMap& a,
-                   const CUtensorMap& b, const P& prm) {
-    size_t smem = pr::smem_bytes(H);
+                   const CUtensorMap& b, const P& prm, size_t smem = 0, int cluster = 1) {
+    if (!smem) smem = pr::smem_bytes(H);
     CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (cluster > 1) CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     cudaLaunchConfig_t c = {};
     c.gridDim = dim3(grid);
     c.blockDim = dim3(pr::THREADS);
     c.dynamicSmemBytes = smem;
     c.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = cluster;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
     c.attrs = at;
-    c.numAttrs = 1;
+    c.numAttrs = cluster > 1 ? 2 : 1;
     CMT_CUDA(cudaLaunchKernelEx(&c, k, a, b, prm));
     CMT_LAUNCHED();
   }
@@ -750,6 +763,21 @@ class Engine {
     e.bias = dw + ly.b_off;
     gemm((int)N, 4 * H, din, Mat{X, din, 0}, Mat{wv(ly.w_off), 4LL * H, 1}, e);
     ScanViews v = views(l, reverse);
+    if (use_cluster_fwd()) {
+      CUtensorMap tmH, tmW;
+      make_map_kblocks(&tmH, lw[l].yext, (long long)(steps + 1) * B, H, H, cl::ROWS, cl::KBOX);
+      make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 64);
+      LstmFwdP prm;
+      prm.ux = ux; prm.y = (bf16*)v.ybase; prm.hprev = (const bf16*)v.hprev; prm.cst = v.cbase; prm.cprev = v.cprev;
+      prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.mask = mask; prm.flag = flags + (l & 31);
+      prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
+      prm.hrow0 = reverse ? B : 0;
+      prm.trace = (trace_layer == l) ? trace_d : nullptr;
+      prm.stages = cl::fwd_stages(H);
+      CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
+      launch_coop(lstm_fwd_cluster, cl::FWD_KS * (4 * H / cl::FWD_NG), tmH, tmW, prm, cl::fwd_smem(H), cl::FWD_KS);
+      return;
+    }
     if (use_persistent()) {
       CUtensorMap tmH, tmW;
       make_map_kblocks(&tmH, lw[l].yext, (long long)(steps + 1) * B, H, H, pr::ROWS, pr::KBOX);
@@ -791,7 +819,20 @@ class Engine {
     else CMT_CUDA(cudaMemsetAsync(dcc, 0, BH * 4, st));
     const void* WhN = (const char*)wv(ly.w_off) + (size_t)din * 4 * H * asz;  // rows din.. of [din+H][4H]
     auto time_of = [&](int p) { return reverse ? steps - 1 - p : p; };
-    if (use_persistent()) {
+    if (use_cluster_bwd()) {
+      CUtensorMap tmA, tmW;
+      make_map_kblocks(&tmA, dU, N, 4LL * H, 4LL * H, cl::ROWS, cl::KBOX);
+      make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, cl::BWD_NU);
+      LstmBwdP prm;
+      prm.dy = dy; prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.cprev = v.cprev; prm.mask = mask;
+      prm.dU = (bf16*)dU; prm.dh_final = dh_final; prm.dc_final = dc_final; prm.dh0 = dh0; prm.dc0 = dc0;
+      prm.flag = flags + 32 + (l & 31);
+      prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
+      prm.trace = nullptr;
+      prm.stages = cl::bwd_stages(H);
+      CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
+      launch_coop(lstm_bwd_cluster, cl::BWD_KS * (H / cl::BWD_NU), tmA, tmW, prm, cl::bwd_smem(H), cl::BWD_KS);
+    } else if (use_persistent()) {
       CUtensorMap tmA, tmW;
       make_map_kblocks(&tmA, dU, N, 4LL * H, 4LL * H, pr::ROWS, pr::KBOX);
       make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 16);
@@ -1336,6 +1377,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     std::string k(key);
     if (k == "time_dominant") e->eng->time_dominant = (int)value;
     else if (k == "persistent") e->eng->persistent = (int)value;
+    else if (k == "cluster") e->eng->clustered = (int)value;
     else if (k == "trace_layer") {
       e->eng->trace_layer = (int)value;
       if (!e->eng->trace_d) CMT_CUDA(cudaMalloc(&e->eng->trace_d, 4096 * 8));

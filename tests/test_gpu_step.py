@@ -220,16 +220,18 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
     src, sm, tgt, tm = O.synthetic_batch(V, S, T, B, seed=6, ragged=ragged)
     _, _, og, _, _ = oracle_step(d, params, (src, sm, tgt, tm), 0.1, 1.0, 5.0, 3, update=False)
     out = {}
-    for pers in (0, 1):
+    for variant in ("per_step", "persistent", "cluster"):
         eng = Engine(cfg_of(d), mode="bf16")
-        eng.set_option("persistent", pers)
+        eng.set_option("persistent", int(variant != "per_step"))
+        eng.set_option("cluster", int(variant == "cluster"))
         eng.upload(params)
         eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, np.random.Generator(np.random.PCG64(3)), update=False)
-        out[pers] = eng.grads()
+        out[variant] = eng.grads()
         eng.close()
-    for n in og:
-        assert O.norm_rel_err(out[1][n], out[0][n]) < BF16_TOL, n
-        assert O.norm_rel_err(out[1][n], og[n]) < BF16_TOL, n
+    for v in ("persistent", "cluster"):
+        for n in og:
+            assert O.norm_rel_err(out[v][n], out["per_step"][n]) < BF16_TOL, (v, n)
+            assert O.norm_rel_err(out[v][n], og[n]) < BF16_TOL, (v, n)
 
 
 @pytest.mark.parametrize("mode", ["fp32", "bf16"])
