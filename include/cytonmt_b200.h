@@ -113,7 +113,7 @@ int cmt_debug_buffer(cmt_engine* e, const char* name, float* out, long long cap,
 /* test hooks (parity tests only; device pointers): one GEMM C = A B^T (fp32 out), one dropout site */
 /* flags: 1 = accumulate into C, 2 = bf16 C, 4 = tanh; bias may be NULL */
 int cmt_test_gemm(int mode, int M, int N, int K, const void* A, long long lda, int a_mn, const void* B, long long ldb,
-                  int b_mn, void* C, long long ldc, int bn, int flags, const float* bias);
+                  int b_mn, void* C, long long ldc, int bn /* BN; BN+1: CTA-pair tile */, int flags, const float* bias);
 int cmt_test_dropout(unsigned long long state_hi, unsigned long long state_lo, unsigned long long inc_hi,
                      unsigned long long inc_lo, unsigned long long base, int N, int H, double p, const float* x,
                      float* y, unsigned char* keep);

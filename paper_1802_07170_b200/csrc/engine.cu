@@ -110,11 +110,11 @@ struct Mat {
 
 static int g_num_sms = 148;
 
-template <int BN, int AMN, int BMN, class Epi>
+template <int BN, int AMN, int BMN, class Epi, int CG = 1>
 static void launch_tc(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const Epi& e) {
-  using C = tc::Cfg<BN>;
+  using C = tc::Cfg<BN, CG>;
   static bool attr = false;
-  auto kfn = gemm_tc_kernel<BN, AMN, BMN, Epi>;
+  auto kfn = gemm_tc_kernel<BN, AMN, BMN, Epi, CG>;
   if (!attr) {
     CMT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
@@ -125,23 +125,44 @@ static void launch_tc(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const 
   if (AMN) make_map(&ta, ap, M, Kx, A.ld, 64, tc::BK);
   else make_map(&ta, ap, Kx, M, A.ld, tc::BK, tc::BM);
   if (BMN) make_map(&tb, B.p, N, Kx, B.ld, 64, tc::BK);
-  else make_map(&tb, B.p, Kx, N, B.ld, tc::BK, BN);
-  int tiles = ceil_div(M, tc::BM) * ceil_div(N, BN);
-  int grid = std::min(tiles, g_num_sms);
-  gemm_tc_kernel<BN, AMN, BMN, Epi><<<grid, tc::NUM_THREADS, C::SMEM, st>>>(ta, tb, M, N, K, e);
+  else make_map(&tb, B.p, Kx, N, B.ld, tc::BK, C::BNC);
+  int tiles = ceil_div(M, C::TILE_M) * ceil_div(N, BN);
+  int grid = CG * std::min(tiles, g_num_sms / CG);
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(grid);
+  c.blockDim = dim3(tc::NUM_THREADS);
+  c.dynamicSmemBytes = C::SMEM;
+  c.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  c.attrs = at;
+  c.numAttrs = CG > 1 ? 1 : 0;
+  CMT_CUDA(cudaLaunchKernelEx(&c, kfn, ta, tb, M, N, K, e));
   CMT_LAUNCHED();
-  CMT_CUDA(cudaGetLastError());
 }
 
-static int pick_bn(int M, int N) {
-  if (N <= 64) return 64;
-  if (N <= 128) return 128;
-  auto eff = [&](int bn) {
-    long long t = (long long)ceil_div(M, 128) * ceil_div(N, bn);
-    long long waves = (t + g_num_sms - 1) / g_num_sms;
-    return (double)t / (double)(waves * g_num_sms);
-  };
-  return eff(256) + 0.05 >= eff(128) ? 256 : 128;
+// Tile choice for the EpiStore GEMMs: (BN, CG) with the best wave efficiency
+// (tiles / (waves * units)); on ties prefer the CTA pair and the wider tile,
+// whose per-SM operand stream is smallest.  Encoded as BN * 4 + CG.
+static int pick_tile(int M, int N) {
+  if (N <= 64) return 64 * 4 + 1;
+  struct Cand { int bn, cg; double bonus; };
+  const Cand cands[] = {{256, 2, 0.10}, {128, 2, 0.06}, {256, 1, 0.03}, {128, 1, 0.0}};
+  int best = 128 * 4 + 1;
+  double best_s = -1;
+  for (const Cand& c : cands) {
+    if (c.bn > 128 && N <= 128) continue;
+    long long units = g_num_sms / c.cg;
+    long long t = (long long)ceil_div(M, 128 * c.cg) * ceil_div(N, c.bn);
+    long long waves = (t + units - 1) / units;
+    double eff = (double)t / (double)(waves * units);
+    double s = eff + c.bonus;
+    if (s > best_s) { best_s = s; best = c.bn * 4 + c.cg; }
+  }
+  return best;
 }
 
 // ---------------------------------------------------------------------------
@@ -247,6 +268,7 @@ class Engine {
   unsigned* flags;
   int persistent = 1;  // option: persistent recurrent kernels in bf16 mode
   int clustered = 1;   // option: cluster K-split variant of the persistent kernels
+  int cg2 = 1;         // option: CTA-pair (cta_group::2) tiles for the large GEMMs
   // data parallel (NCCL): dense all-reduce of grads, loss and status
   void* comm = nullptr;
   int rank = 0, world = 1;
@@ -658,13 +680,17 @@ class Engine {
     dispatch_tc(M, N, K, A, Bm, e, bn);
   }
   void dispatch_tc(int M, int N, int K, Mat A, Mat Bm, const EpiStore& e, int bn) {
-    if (!bn) bn = pick_bn(M, N);
+    int tile = bn ? bn * 4 + 1 : pick_tile(M, N);
+    if (!cg2 && (tile & 3) == 2) tile = (tile >> 2) * 4 + 1;
     int key = A.mn * 2 + Bm.mn;
-#define CMT_TC(BN_, AMN, BMN) \
-  if (bn == BN_ && key == AMN * 2 + BMN) return launch_tc<BN_, AMN, BMN, EpiStore>(st, M, N, K, A, Bm, e);
-    CMT_TC(64, 0, 1) CMT_TC(128, 0, 1) CMT_TC(256, 0, 1)
-    CMT_TC(64, 0, 0) CMT_TC(128, 0, 0) CMT_TC(256, 0, 0)
-    CMT_TC(64, 1, 1) CMT_TC(128, 1, 1) CMT_TC(256, 1, 1)
+#define CMT_TC(BN_, AMN, BMN, CG_) \
+  if (tile == BN_ * 4 + CG_ && key == AMN * 2 + BMN) return launch_tc<BN_, AMN, BMN, EpiStore, CG_>(st, M, N, K, A, Bm, e);
+    CMT_TC(64, 0, 1, 1) CMT_TC(128, 0, 1, 1) CMT_TC(256, 0, 1, 1)
+    CMT_TC(64, 0, 0, 1) CMT_TC(128, 0, 0, 1) CMT_TC(256, 0, 0, 1)
+    CMT_TC(64, 1, 1, 1) CMT_TC(128, 1, 1, 1) CMT_TC(256, 1, 1, 1)
+    CMT_TC(128, 0, 1, 2) CMT_TC(256, 0, 1, 2)
+    CMT_TC(128, 0, 0, 2) CMT_TC(256, 0, 0, 2)
+    CMT_TC(128, 1, 1, 2) CMT_TC(256, 1, 1, 2)
 #undef CMT_TC
     throw Error(CMT_ERR_INTERNAL, "no tcgen05 GEMM instantiation for this operand layout");
   }
@@ -1351,10 +1377,11 @@ int cmt_test_gemm(int mode, int M, int N, int K, const void* A, long long lda, i
                                                                    M, N, K, e);
     } else {
       int key = a_mn * 2 + b_mn;
-#define T_(BN_, AMN, BMN) else if (bn == BN_ && key == AMN * 2 + BMN) cmt::launch_tc<BN_, AMN, BMN, cmt::EpiStore>(st, M, N, K, a, b, e);
+#define T_(BN_, AMN, BMN, CG_) else if (bn == BN_ + CG_ - 1 && key == AMN * 2 + BMN) cmt::launch_tc<BN_, AMN, BMN, cmt::EpiStore, CG_>(st, M, N, K, a, b, e);
       if (0) {}
-      T_(64, 0, 1) T_(128, 0, 1) T_(256, 0, 1) T_(64, 0, 0) T_(128, 0, 0) T_(256, 0, 0) T_(64, 1, 1) T_(128, 1, 1)
-      T_(256, 1, 1)
+      T_(64, 0, 1, 1) T_(128, 0, 1, 1) T_(256, 0, 1, 1) T_(64, 0, 0, 1) T_(128, 0, 0, 1) T_(256, 0, 0, 1) T_(64, 1, 1, 1)
+      T_(128, 1, 1, 1) T_(256, 1, 1, 1)
+      T_(128, 0, 1, 2) T_(256, 0, 1, 2) T_(128, 0, 0, 2) T_(256, 0, 0, 2) T_(128, 1, 1, 2) T_(256, 1, 1, 2)
       else throw Error(cmt::CMT_ERR_INTERNAL, "no such GEMM instantiation");
 #undef T_
     }
@@ -1378,6 +1405,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     if (k == "time_dominant") e->eng->time_dominant = (int)value;
     else if (k == "persistent") e->eng->persistent = (int)value;
     else if (k == "cluster") e->eng->clustered = (int)value;
+    else if (k == "cg2") e->eng->cg2 = (int)value;
     else if (k == "trace_layer") {
       e->eng->trace_layer = (int)value;
       if (!e->eng->trace_d) CMT_CUDA(cudaMalloc(&e->eng->trace_d, 4096 * 8));

@@ -43,25 +43,63 @@ struct EpiStore {
   float alpha = 1.f;
 
   CMT_D void apply(int m, int n0, const float* v, int M, int N) const {
-    float x[32];
+    const bool full = (n0 + 32 <= N);
+    // Issue every global load of the chunk up front (vectorised where the
+    // row is 16-byte aligned) so their latencies overlap instead of being
+    // paid once per column.
+    float x[32], bv[32], tg[32], ad[32];
+    uint8_t km[32];
+    const long long rm = (long long)m;
+    if (bias) {
+      if (full && (((uintptr_t)(bias + n0)) & 15) == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) *(float4*)&bv[4 * q] = __ldg((const float4*)(bias + n0) + q);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) bv[j] = (n0 + j < N) ? __ldg(bias + n0 + j) : 0.f;
+      }
+    }
+    if (dmask) {
+      const uint8_t* dm = dmask + rm * ld_dmask + n0;
+      if (full && (((uintptr_t)dm) & 15) == 0) {
+        *(uint4*)&km[0] = *(const uint4*)dm;
+        *(uint4*)&km[16] = *(const uint4*)(dm + 16);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) km[j] = (n0 + j < N) ? dm[j] : 0;
+      }
+    }
+    if (tgrad_y) {
+      const float* ty = tgrad_y + rm * ld_tgrad + n0;
+      if (full && (((uintptr_t)ty) & 15) == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) *(float4*)&tg[4 * q] = *((const float4*)ty + q);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) tg[j] = (n0 + j < N) ? ty[j] : 0.f;
+      }
+    }
+    if (add) {
+      const float* aa = add + rm * ld_add + n0;
+      if (full && (((uintptr_t)aa) & 15) == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) *(float4*)&ad[4 * q] = *((const float4*)aa + q);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) ad[j] = (n0 + j < N) ? aa[j] : 0.f;
+      }
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      int n = n0 + j;
       float t = alpha * v[j];
-      if (n < N) {
-        if (bias) t += bias[n];
-        if (act == 1) t = c_bf16 ? ptx::tanh_fast(t) : tanhf(t);
-        if (dmask) t = dmask[(long long)m * ld_dmask + n] ? t * dscale : 0.f * t;
-        if (tgrad_y) {
-          float yy = tgrad_y[(long long)m * ld_tgrad + n];
-          t *= (1.f - yy * yy);
-        }
-        if (add) t += add[(long long)m * ld_add + n];
-      }
+      if (bias) t += bv[j];
+      if (act == 1) t = c_bf16 ? ptx::tanh_fast(t) : tanhf(t);
+      if (dmask) t = km[j] ? t * dscale : 0.f * t;
+      if (tgrad_y) t *= (1.f - tg[j] * tg[j]);
+      if (add) t += ad[j];
       x[j] = t;
     }
-    long long base = (long long)m * ldc + n0;
-    bool full = (n0 + 32 <= N);
+    long long base = rm * ldc + n0;
     if (c_bf16) {
       bf16* c = (bf16*)C + base;
       if (full && ((((uintptr_t)c) & 15) == 0)) {
@@ -80,15 +118,17 @@ struct EpiStore {
     } else {
       float* c = (float*)C + base;
       if (full && ((((uintptr_t)c) & 15) == 0)) {
+        if (beta) {
+          float4 old[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float4 o = make_float4(x[q * 4], x[q * 4 + 1], x[q * 4 + 2], x[q * 4 + 3]);
-          if (beta) {
-            float4 old = *(float4*)(c + q * 4);
-            o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+          for (int q = 0; q < 8; ++q) old[q] = *(float4*)(c + q * 4);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            x[q * 4] += old[q].x; x[q * 4 + 1] += old[q].y; x[q * 4 + 2] += old[q].z; x[q * 4 + 3] += old[q].w;
           }
-          *(float4*)(c + q * 4) = o;
         }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) *(float4*)(c + q * 4) = make_float4(x[q * 4], x[q * 4 + 1], x[q * 4 + 2], x[q * 4 + 3]);
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j)
@@ -218,6 +258,16 @@ struct EpiInitGrad {
 
 // ---------------------------------------------------------------------------
 // tcgen05 persistent GEMM (bf16 -> fp32)
+//
+// CG = 1: one CTA per 128 x BN tile.
+// CG = 2: a CTA pair (cluster of 2, cta_group::2) per 256 x BN tile.  Each CTA
+//   TMA-loads its own 128 rows of A and BN/2 columns of B; the leader's single
+//   MMA thread issues M=256 tcgen05.mma that read both CTAs' smem, so each SM
+//   streams half the B bytes of the CG=1 kernel for the same MMA rate (the
+//   1-CTA 128x256 tile needs ~96 B/clk/SM of TMA, the pair 64 B/clk/SM).
+//   Stage completion bytes of both CTAs land on the leader's full barrier;
+//   MMA commits multicast the stage-empty / accumulator-full signals to both
+//   CTAs; both CTAs' epilogue warps release the accumulator on the leader.
 // ---------------------------------------------------------------------------
 namespace tc {
 constexpr int BM = 128;
@@ -225,23 +275,25 @@ constexpr int BK = 64;
 constexpr int NUM_THREADS = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 epilogue (2 per SMSP)
 constexpr int EPI_WARPS = 8;
 
-template <int BN>
+template <int BN, int CG = 1>
 struct Cfg {
+  static constexpr int BNC = BN / CG;  // B columns held by one CTA
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = BNC * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+  static constexpr int TILE_M = BM * CG;
 };
 }  // namespace tc
 
-template <int BN, int A_MN, int B_MN, class Epi>
+template <int BN, int A_MN, int B_MN, class Epi, int CG = 1>
 __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                    int K, Epi epi) {
-  using C = tc::Cfg<BN>;
+  using C = tc::Cfg<BN, CG>;
   constexpr int S = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -255,7 +307,10 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int tiles_m = (M + tc::BM - 1) / tc::BM;
+  const uint32_t rank = (CG == 2) ? ptx::cluster_rank() : 0u;
+  const int unit = (CG == 2) ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // tile-processing unit (CTA or pair)
+  const int nunits = (CG == 2) ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int tiles_m = (M + C::TILE_M - 1) / C::TILE_M;
   const int tiles_n = (N + BN - 1) / BN;
   const int num_tiles = tiles_m * tiles_n;
   const int num_kb = (K + tc::BK - 1) / tc::BK;
@@ -269,24 +324,28 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], tc::EPI_WARPS);
+      ptx::mbar_init(&tempty[i], tc::EPI_WARPS * CG);
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (CG == 2) ptx::tmem_alloc_cg2(tmem_slot, C::TMEM_COLS);
+    else ptx::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync_all();
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0 && num_kb > 0) {
-      // ===== TMA producer =====
+      // ===== TMA producer (both CTAs of a pair load their own halves) =====
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % tiles_m) * tc::BM;
-        const int n0 = (tile / tiles_m) * BN;
+      for (int tile = unit; tile < num_tiles; tile += nunits) {
+        const int m0 = (tile % tiles_m) * C::TILE_M + (int)rank * tc::BM;
+        const int n0 = (tile / tiles_m) * BN + (int)rank * C::BNC;
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * C::A_BYTES;
@@ -294,31 +353,50 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
           // stagger the K order per tile so concurrent CTAs sharing an operand
           // tile do not request the same L2 lines at the same moment
           const int k0 = ((kb + tile) % num_kb) * tc::BK;
-          if (A_MN) {
-            ptx::tma_load_2d(&tmA, &full[stage], a, m0, k0);
-            ptx::tma_load_2d(&tmA, &full[stage], a + 64 * tc::BK * 2, m0 + 64, k0);
-          } else {
-            ptx::tma_load_2d(&tmA, &full[stage], a, k0, m0);
-          }
-          if (B_MN) {
+          if constexpr (CG == 2) {
+            const uint32_t fb = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
+            if (rank == 0) ptx::mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            if (A_MN) {
+              ptx::tma_load_2d_cg2(&tmA, fb, a, m0, k0);
+              ptx::tma_load_2d_cg2(&tmA, fb, a + 64 * tc::BK * 2, m0 + 64, k0);
+            } else {
+              ptx::tma_load_2d_cg2(&tmA, fb, a, k0, m0);
+            }
+            if (B_MN) {
 #pragma unroll
-            for (int q = 0; q < BN / 64; ++q) ptx::tma_load_2d(&tmB, &full[stage], b + q * 64 * tc::BK * 2, n0 + q * 64, k0);
+              for (int q = 0; q < C::BNC / 64; ++q)
+                ptx::tma_load_2d_cg2(&tmB, fb, b + q * 64 * tc::BK * 2, n0 + q * 64, k0);
+            } else {
+              ptx::tma_load_2d_cg2(&tmB, fb, b, k0, n0);
+            }
           } else {
-            ptx::tma_load_2d(&tmB, &full[stage], b, k0, n0);
+            if (A_MN) {
+              ptx::tma_load_2d(&tmA, &full[stage], a, m0, k0);
+              ptx::tma_load_2d(&tmA, &full[stage], a + 64 * tc::BK * 2, m0 + 64, k0);
+            } else {
+              ptx::tma_load_2d(&tmA, &full[stage], a, k0, m0);
+            }
+            if (B_MN) {
+#pragma unroll
+              for (int q = 0; q < BN / 64; ++q)
+                ptx::tma_load_2d(&tmB, &full[stage], b + q * 64 * tc::BK * 2, n0 + q * 64, k0);
+            } else {
+              ptx::tma_load_2d(&tmB, &full[stage], b, k0, n0);
+            }
+            ptx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           }
-          ptx::mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && num_kb > 0) {
-      // ===== MMA issuer =====
-      const uint32_t idesc = ptx::idesc_bf16(tc::BM, BN, A_MN, B_MN);
+    if (lane == 0 && num_kb > 0 && rank == 0) {
+      // ===== MMA issuer (the leader CTA of a pair) =====
+      const uint32_t idesc = ptx::idesc_bf16(C::TILE_M, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int iter = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+      for (int tile = unit; tile < num_tiles; tile += nunits, ++iter) {
         const int buf = iter & 1;
         const uint32_t aphase = (iter >> 1) & 1;
         ptx::mbar_wait(&tempty[buf], aphase ^ 1);
@@ -335,10 +413,16 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
                                : ptx::smem_desc_sw128(a_addr + kk * 32, 16, 1024);
             uint64_t bd = B_MN ? ptx::smem_desc_sw128(b_addr + kk * 2048, 64 * tc::BK * 2, 1024)
                                : ptx::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
-            ptx::umma_bf16(dtm, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+            if constexpr (CG == 2) ptx::umma_bf16_cg2(dtm, ad, bd, idesc, (kb | kk) ? 1u : 0u);
+            else ptx::umma_bf16(dtm, ad, bd, idesc, (kb | kk) ? 1u : 0u);
           }
-          ptx::umma_commit(&empty[stage]);
-          if (kb == num_kb - 1) ptx::umma_commit(&tfull[buf]);
+          if constexpr (CG == 2) {
+            ptx::umma_commit_cg2_mc(&empty[stage], 3);
+            if (kb == num_kb - 1) ptx::umma_commit_cg2_mc(&tfull[buf], 3);
+          } else {
+            ptx::umma_commit(&empty[stage]);
+            if (kb == num_kb - 1) ptx::umma_commit(&tfull[buf]);
+          }
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
@@ -349,9 +433,10 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
     constexpr int NCH = BN / 32;
     const int c_lo = (warp < 8) ? 0 : (NCH + 1) / 2;
     const int c_hi = (warp < 8) ? (NCH + 1) / 2 : NCH;
+    const uint32_t tempty_leader0 = (CG == 2) ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
     int iter = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
-      const int m0 = (tile % tiles_m) * tc::BM;
+    for (int tile = unit; tile < num_tiles; tile += nunits, ++iter) {
+      const int m0 = (tile % tiles_m) * C::TILE_M + (int)rank * tc::BM;
       const int n0 = (tile / tiles_m) * BN;
       const int buf = iter & 1;
       const uint32_t aphase = (iter >> 1) & 1;
@@ -373,14 +458,19 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0 && num_kb > 0) ptx::mbar_arrive(&tempty[buf]);
+      if (lane == 0 && num_kb > 0) {
+        if constexpr (CG == 2) ptx::mbar_arrive_remote_relaxed(tempty_leader0 + buf * 8);
+        else ptx::mbar_arrive_relaxed(&tempty[buf]);
+      }
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync_all();
+  else __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if constexpr (CG == 2) ptx::tmem_dealloc_cg2(tmem_base, C::TMEM_COLS);
+    else ptx::tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 

@@ -210,3 +210,58 @@ CMT_D void cluster_sync_all() {
 }
 }  // namespace ptx
 }  // namespace cmt
+
+namespace cmt {
+namespace ptx {
+// ---- CTA-pair (cta_group::2) tcgen05 GEMM primitives ----
+// 2-D TMA load into this CTA's smem whose completion bytes are counted on an
+// mbarrier that may live in the peer CTA (cluster address from mapa).
+CMT_D void tma_load_2d_cg2(const void* tmap, uint32_t bar_cluster, void* smem, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(smem)),
+      "l"((uint64_t)tmap), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+CMT_D void tmem_alloc_cg2(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::);
+}
+CMT_D void tmem_dealloc_cg2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+// D[tmem of both CTAs] (+)= A[smem, 128 rows per CTA] * B[smem, N/2 cols per CTA]^T
+CMT_D void umma_bf16_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// arrive on the mbarrier at the same smem offset in every CTA of `mask` once
+// this thread's prior cta_group::2 MMAs complete
+CMT_D void umma_commit_cg2_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+}  // namespace ptx
+}  // namespace cmt
+
+namespace cmt {
+namespace ptx {
+// Relaxed arrives: the consumer only needs this thread's tcgen05.ld reads to be
+// done (ordered by tcgen05.fence::before_thread_sync), not its global stores,
+// so no release fence (MEMBAR) is paid per accumulator hand-back.
+CMT_D void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+CMT_D void mbar_arrive_remote_relaxed(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+}  // namespace ptx
+}  // namespace cmt

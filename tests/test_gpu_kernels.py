@@ -31,7 +31,7 @@ def _gemm(mode, M, N, K, a_mn, b_mn, bn, beta=0, seed=0):
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 1), (0, 0), (1, 1)])
-@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("bn", [64, 128, 256, 129, 257])  # 129/257: CTA-pair (cta_group::2) 256-row tiles
 @pytest.mark.parametrize("shape", [(128, 256, 64), (300, 520, 200), (1000, 1100, 1024), (64, 96, 40)])
 def test_tcgen05_gemm_layouts(a_mn, b_mn, bn, shape):
     M, N, K = shape
@@ -44,8 +44,9 @@ def test_tcgen05_gemm_layouts(a_mn, b_mn, bn, shape):
     assert err < 1e-5, err  # bf16 inputs are exact in both; only fp32 summation order differs
 
 
-def test_tcgen05_gemm_accumulate_and_many_tiles():
-    C, ref = _gemm(_lib.MODE_BF16, 6400, 2048, 1024, 0, 1, 256, beta=1, seed=3)
+@pytest.mark.parametrize("bn", [256, 257])
+def test_tcgen05_gemm_accumulate_and_many_tiles(bn):
+    C, ref = _gemm(_lib.MODE_BF16, 6400, 2048, 1024, 0, 1, bn, beta=1, seed=3)
     assert (C - ref).abs().max().item() / ref.abs().max().item() < 1e-5
 
 
