@@ -21,6 +21,7 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/cytonmt_b200.h"
@@ -59,6 +60,24 @@ static void make_map(CUtensorMap* m, const void* ptr, long long d0, long long d1
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(CMT_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+// Epilogue output map for the TMA-store GEMM epilogue: C [rows][cols] (row
+// stride ld elements), box 32 x 32, fp32 rows 128 B (SWIZZLE_128B) or bf16
+// rows 64 B (SWIZZLE_64B), matching the smem staging layout in gemm.cuh.
+static bool c_map_ok(const void* ptr, long long ld, bool bf16) {
+  return !(((uintptr_t)ptr & 15) || ((ld * (bf16 ? 2 : 4)) & 15));
+}
+static void make_map_c(CUtensorMap* m, const void* ptr, long long cols, long long rows, long long ld, bool bf16) {
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstr[1] = {(cuuint64_t)(ld * (bf16 ? 2 : 4))};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = get_encode()(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                            const_cast<void*>(ptr), gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(CMT_ERR_CUDA, "cuTensorMapEncodeTiled (C) failed: " + std::to_string((int)r));
 }
 
 // bf16 3-D map over a row-major [rows][cols] matrix viewed as {64, rows, cols/64}
@@ -110,22 +129,25 @@ struct Mat {
 
 static int g_num_sms = 148;
 
-template <int BN, int AMN, int BMN, class Epi, int CG = 1>
-static void launch_tc(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const Epi& e) {
-  using C = tc::Cfg<BN, CG>;
+static int g_gemm_opt = 0;  // option: bit 0 natural K order, bit 1 N-fastest tile order
+template <int BN, int AMN, int BMN, class Epi, int CG = 1, int ST = 0>
+static void launch_tc_impl(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const Epi& e) {
+  using C = tc::Cfg<BN, CG, ST>;
   static bool attr = false;
-  auto kfn = gemm_tc_kernel<BN, AMN, BMN, Epi, CG>;
+  auto kfn = gemm_tc_kernel<BN, AMN, BMN, Epi, CG, ST>;
   if (!attr) {
     CMT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tcm;
   const void* ap = A.p ? A.p : B.p;
   long long Kx = std::max(K, 64);
   if (AMN) make_map(&ta, ap, M, Kx, A.ld, 64, tc::BK);
   else make_map(&ta, ap, Kx, M, A.ld, tc::BK, tc::BM);
   if (BMN) make_map(&tb, B.p, N, Kx, B.ld, 64, tc::BK);
   else make_map(&tb, B.p, Kx, N, B.ld, tc::BK, C::BNC);
+  if constexpr (ST) make_map_c(&tcm, e.C, N, M, e.ldc, e.c_bf16 != 0);
+  else tcm = ta;
   int tiles = ceil_div(M, C::TILE_M) * ceil_div(N, BN);
   int grid = CG * std::min(tiles, g_num_sms / CG);
   cudaLaunchConfig_t c = {};
@@ -140,8 +162,19 @@ static void launch_tc(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const 
   at[0].val.clusterDim.z = 1;
   c.attrs = at;
   c.numAttrs = CG > 1 ? 1 : 0;
-  CMT_CUDA(cudaLaunchKernelEx(&c, kfn, ta, tb, M, N, K, e));
+  CMT_CUDA(cudaLaunchKernelEx(&c, kfn, ta, tb, tcm, M, N, K, e, g_gemm_opt));
   CMT_LAUNCHED();
+}
+
+static int g_tma_store = 1;  // option: TMA-store epilogue for EpiStore GEMMs
+
+template <int BN, int AMN, int BMN, class Epi, int CG = 1>
+static void launch_tc(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const Epi& e) {
+  if constexpr (std::is_same<Epi, EpiStore>::value) {
+    if (g_tma_store && c_map_ok(e.C, e.ldc, e.c_bf16 != 0) && !(e.beta && e.c_bf16))
+      return launch_tc_impl<BN, AMN, BMN, Epi, CG, 1>(st, M, N, K, A, B, e);
+  }
+  launch_tc_impl<BN, AMN, BMN, Epi, CG, 0>(st, M, N, K, A, B, e);
 }
 
 // Tile choice for the EpiStore GEMMs: (BN, CG) with the best wave efficiency
@@ -1406,6 +1439,8 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "persistent") e->eng->persistent = (int)value;
     else if (k == "cluster") e->eng->clustered = (int)value;
     else if (k == "cg2") e->eng->cg2 = (int)value;
+    else if (k == "tma_store") cmt::g_tma_store = (int)value;
+    else if (k == "gemm_opt") cmt::g_gemm_opt = (int)value;
     else if (k == "trace_layer") {
       e->eng->trace_layer = (int)value;
       if (!e->eng->trace_d) CMT_CUDA(cudaMalloc(&e->eng->trace_d, 4096 * 8));

@@ -42,14 +42,16 @@ struct EpiStore {
   long long ld_tgrad = 0;
   float alpha = 1.f;
 
-  CMT_D void apply(int m, int n0, const float* v, int M, int N) const {
+  // x[j] = epilogue value of (m, n0 + j); rows m >= M read no row operands.
+  CMT_D void compute(int m, int n0, const float* v, int M, int N, float* x) const {
     const bool full = (n0 + 32 <= N);
+    const bool row_ok = m < M;
     // Issue every global load of the chunk up front (vectorised where the
     // row is 16-byte aligned) so their latencies overlap instead of being
     // paid once per column.
-    float x[32], bv[32], tg[32], ad[32];
+    float bv[32], tg[32], ad[32];
     uint8_t km[32];
-    const long long rm = (long long)m;
+    const long long rm = row_ok ? (long long)m : 0;
     if (bias) {
       if (full && (((uintptr_t)(bias + n0)) & 15) == 0) {
 #pragma unroll
@@ -59,7 +61,7 @@ struct EpiStore {
         for (int j = 0; j < 32; ++j) bv[j] = (n0 + j < N) ? __ldg(bias + n0 + j) : 0.f;
       }
     }
-    if (dmask) {
+    if (dmask && row_ok) {
       const uint8_t* dm = dmask + rm * ld_dmask + n0;
       if (full && (((uintptr_t)dm) & 15) == 0) {
         *(uint4*)&km[0] = *(const uint4*)dm;
@@ -69,7 +71,7 @@ struct EpiStore {
         for (int j = 0; j < 32; ++j) km[j] = (n0 + j < N) ? dm[j] : 0;
       }
     }
-    if (tgrad_y) {
+    if (tgrad_y && row_ok) {
       const float* ty = tgrad_y + rm * ld_tgrad + n0;
       if (full && (((uintptr_t)ty) & 15) == 0) {
 #pragma unroll
@@ -79,7 +81,7 @@ struct EpiStore {
         for (int j = 0; j < 32; ++j) tg[j] = (n0 + j < N) ? ty[j] : 0.f;
       }
     }
-    if (add) {
+    if (add && row_ok) {
       const float* aa = add + rm * ld_add + n0;
       if (full && (((uintptr_t)aa) & 15) == 0) {
 #pragma unroll
@@ -94,12 +96,18 @@ struct EpiStore {
       float t = alpha * v[j];
       if (bias) t += bv[j];
       if (act == 1) t = c_bf16 ? ptx::tanh_fast(t) : tanhf(t);
-      if (dmask) t = km[j] ? t * dscale : 0.f * t;
-      if (tgrad_y) t *= (1.f - tg[j] * tg[j]);
-      if (add) t += ad[j];
+      if (dmask && row_ok) t = km[j] ? t * dscale : 0.f * t;
+      if (tgrad_y && row_ok) t *= (1.f - tg[j] * tg[j]);
+      if (add && row_ok) t += ad[j];
       x[j] = t;
     }
-    long long base = rm * ldc + n0;
+  }
+
+  CMT_D void apply(int m, int n0, const float* v, int M, int N) const {
+    const bool full = (n0 + 32 <= N);
+    float x[32];
+    compute(m, n0, v, M, N, x);
+    long long base = (long long)m * ldc + n0;
     if (c_bf16) {
       bf16* c = (bf16*)C + base;
       if (full && ((((uintptr_t)c) & 15) == 0)) {
@@ -275,31 +283,37 @@ constexpr int BK = 64;
 constexpr int NUM_THREADS = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 epilogue (2 per SMSP)
 constexpr int EPI_WARPS = 8;
 
-template <int BN, int CG = 1>
+constexpr int STG_BYTES = 32 * 32 * 4;  // one epilogue staging buffer: 32 rows x 128 B
+template <int BN, int CG = 1, int ST = 0>
 struct Cfg {
   static constexpr int BNC = BN / CG;  // B columns held by one CTA
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BNC * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGING = ST ? EPI_WARPS * 2 * STG_BYTES : 0;  // double-buffered per epilogue warp
+  static constexpr int STAGES_RAW = (ST ? (227 * 1024 - 2048 - STAGING) : 200 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
-  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STAGING + 1024 /*barriers*/;
   static constexpr int TILE_M = BM * CG;
 };
 }  // namespace tc
 
-template <int BN, int A_MN, int B_MN, class Epi, int CG = 1>
+// ST = 1 (EpiStore only): the epilogue stages each warp's 32x32 result block
+// in 128B/64B-swizzled smem and writes it with a TMA store (or a TMA
+// reduce-add for beta) instead of per-row global stores.
+template <int BN, int A_MN, int B_MN, class Epi, int CG = 1, int ST = 0>
 __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, Epi epi) {
-  using C = tc::Cfg<BN, CG>;
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, int M, int N, int K, Epi epi, int opt) {
+  using C = tc::Cfg<BN, CG, ST>;
   constexpr int S = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * C::A_BYTES;
-  uint64_t* full = (uint64_t*)(smem + S * C::STAGE_BYTES);
+  uint8_t* stg = smem + S * C::STAGE_BYTES;  // epilogue staging (ST), 1024-aligned
+  uint64_t* full = (uint64_t*)(stg + C::STAGING);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -318,6 +332,7 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
+    if (ST) ptx::prefetch_tmap(&tmC);
     for (int i = 0; i < S; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1);
@@ -344,15 +359,17 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = unit; tile < num_tiles; tile += nunits) {
-        const int m0 = (tile % tiles_m) * C::TILE_M + (int)rank * tc::BM;
-        const int n0 = (tile / tiles_m) * BN + (int)rank * C::BNC;
+        const int tm_ = (opt & 2) ? tile / tiles_n : tile % tiles_m;
+        const int tn_ = (opt & 2) ? tile % tiles_n : tile / tiles_m;
+        const int m0 = tm_ * C::TILE_M + (int)rank * tc::BM;
+        const int n0 = tn_ * BN + (int)rank * C::BNC;
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * C::A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
           // stagger the K order per tile so concurrent CTAs sharing an operand
           // tile do not request the same L2 lines at the same moment
-          const int k0 = ((kb + tile) % num_kb) * tc::BK;
+          const int k0 = ((opt & 1) ? kb : (kb + tile) % num_kb) * tc::BK;
           if constexpr (CG == 2) {
             const uint32_t fb = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
             if (rank == 0) ptx::mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -434,10 +451,14 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
     const int c_lo = (warp < 8) ? 0 : (NCH + 1) / 2;
     const int c_hi = (warp < 8) ? (NCH + 1) / 2 : NCH;
     const uint32_t tempty_leader0 = (CG == 2) ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
+    uint8_t* stg_w = stg + (warp - 4) * 2 * tc::STG_BYTES;
+    uint32_t sc = 0;  // staged chunks (buffer parity)
     int iter = 0;
     for (int tile = unit; tile < num_tiles; tile += nunits, ++iter) {
-      const int m0 = (tile % tiles_m) * C::TILE_M + (int)rank * tc::BM;
-      const int n0 = (tile / tiles_m) * BN;
+      const int tm_ = (opt & 2) ? tile / tiles_n : tile % tiles_m;
+      const int tn_ = (opt & 2) ? tile % tiles_n : tile / tiles_m;
+      const int m0 = tm_ * C::TILE_M + (int)rank * tc::BM;
+      const int n0 = tn_ * BN;
       const int buf = iter & 1;
       const uint32_t aphase = (iter >> 1) & 1;
       const int m = m0 + q * 32 + lane;
@@ -454,7 +475,40 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = 0.f;
         }
-        if (m < M && n0 + c * 32 < N) epi.apply(m, n0 + c * 32, v, M, N);
+        if constexpr (ST) {
+          const int nc = n0 + c * 32, mw = m0 + q * 32;
+          if (nc < N && mw < M) {
+            float x[32];
+            epi.compute(m, nc, v, M, N, x);
+            uint8_t* sb = stg_w + (sc & 1) * tc::STG_BYTES;
+            if (lane == 0) ptx::bulk_wait_read1();  // the store that used this buffer 2 chunks ago has read it
+            __syncwarp();
+            if (epi.c_bf16) {  // 64 B rows, SWIZZLE_64B: 16 B chunk j of row r at j ^ ((r >> 1) & 3)
+              uint4* row = (uint4*)(sb + lane * 64);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                __align__(16) bf16 t8[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) t8[u] = __float2bfloat16_rn(x[j * 8 + u]);
+                row[j ^ ((lane >> 1) & 3)] = *(uint4*)t8;
+              }
+            } else {  // 128 B rows, SWIZZLE_128B: chunk j of row r at j ^ (r & 7)
+              float4* row = (float4*)(sb + lane * 128);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) row[j ^ (lane & 7)] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (epi.beta) ptx::tma_reduce_add_2d(&tmC, sb, nc, mw);
+              else ptx::tma_store_2d(&tmC, sb, nc, mw);
+              ptx::bulk_commit();
+            }
+            ++sc;
+          }
+        } else {
+          if (m < M && n0 + c * 32 < N) epi.apply(m, n0 + c * 32, v, M, N);
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -462,6 +516,9 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
         if constexpr (CG == 2) ptx::mbar_arrive_remote_relaxed(tempty_leader0 + buf * 8);
         else ptx::mbar_arrive_relaxed(&tempty[buf]);
       }
+    }
+    if constexpr (ST) {
+      if (lane == 0) ptx::bulk_wait_all();
     }
   }
   ptx::tc_fence_before();

@@ -265,3 +265,25 @@ CMT_D void mbar_arrive_remote_relaxed(uint32_t remote_bar) {
 }
 }  // namespace ptx
 }  // namespace cmt
+
+namespace cmt {
+namespace ptx {
+// ---- TMA stores (smem -> global) through bulk async-groups ----
+CMT_D void tma_store_2d(const void* tmap, const void* smem, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"((uint64_t)tmap),
+               "r"(smem_u32(smem)), "r"(c0), "r"(c1)
+               : "memory");
+}
+// global += smem (fp32 add performed at L2), used for accumulating epilogues
+CMT_D void tma_reduce_add_2d(const void* tmap, const void* smem, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   (uint64_t)tmap),
+               "r"(smem_u32(smem)), "r"(c0), "r"(c1)
+               : "memory");
+}
+CMT_D void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+CMT_D void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+CMT_D void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+CMT_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+}  // namespace ptx
+}  // namespace cmt

@@ -14,9 +14,13 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1802_07170_b200 import _lib  # noqa: E402
 
-# name: (M, N, K, a_mn, b_mn, flags)  flags: 1 beta, 2 bf16 out, 4 tanh
+# name: (M, N, K, a_mn, b_mn, flags)  flags: 1 beta, 2 bf16 out, 4 tanh, 8 no bias
 SHAPES = {
     "logits": (6400, 50000, 1024, 0, 1, 2 | 4),        # tanh(H_o W_o + b_o), bf16 out
+    "logits_nobias": (6400, 50000, 1024, 0, 1, 2 | 4 | 8),   # epilogue ablations (8: no bias)
+    "logits_notanh": (6400, 50000, 1024, 0, 1, 2),
+    "logits_plain": (6400, 50000, 1024, 0, 1, 2 | 8),
+    "logits_f32": (6400, 50000, 1024, 0, 1, 0),
     "dWo": (1024, 50000, 6400, 1, 1, 0),               # H_o^T dY
     "dHo": (6400, 1024, 50000, 0, 0, 2),               # dY W_o^T
     "ux": (6400, 4096, 1024, 0, 1, 0),                 # X W_x + b (hoisted input projection)
@@ -32,6 +36,8 @@ def run(name, tiles, iters):
     B = torch.randn((K, N) if b_mn else (N, K), generator=g).to(torch.bfloat16).cuda()
     C = torch.zeros(M, N, dtype=torch.bfloat16 if flags & 2 else torch.float32, device="cuda")
     bias = torch.zeros(N, device="cuda")
+    use_bias = not (flags & 8)
+    flags &= 7
     lda = M if a_mn else K
     ldb = N if b_mn else K
     lib = _lib.load()
@@ -39,7 +45,7 @@ def run(name, tiles, iters):
     for bn in tiles:
         def call():
             rc = lib.cmt_test_gemm(_lib.MODE_BF16, M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn,
-                                   C.data_ptr(), N, bn, flags, bias.data_ptr())
+                                   C.data_ptr(), N, bn, flags, bias.data_ptr() if use_bias else None)
             assert rc == 0, lib.cmt_last_error(None)
         call()
         ts = []
@@ -64,7 +70,10 @@ if __name__ == "__main__":
     ap.add_argument("--only", default=None)
     ap.add_argument("--iters", type=int, default=7)
     ap.add_argument("--tiles", default="128,256,129,257")
+    ap.add_argument("--opt", type=int, default=None, help="engine gemm_opt bits (1: natural K order, 2: N-fastest)")
     a = ap.parse_args()
+    if a.opt is not None:
+        assert _lib.load().cmt_set_option(None, b"gemm_opt", a.opt) == 0
     tiles = [int(x) for x in a.tiles.split(",")]
     for n in SHAPES:
         if a.only and n not in a.only.split(","):

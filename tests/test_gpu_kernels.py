@@ -73,3 +73,23 @@ def test_dropout_kernel_matches_numpy_pcg64(N, H, base, p):
     scale = np.float32(1.0) / np.float32(1.0 - p)
     ref_y = x.cpu().numpy() * (ref_keep.astype(np.float32) * scale)
     assert np.array_equal(y.cpu().numpy(), ref_y)
+
+
+@pytest.mark.parametrize("bn", [128, 256, 257])
+@pytest.mark.parametrize("shape", [(6400, 1000, 256), (300, 520, 200)])
+def test_tcgen05_gemm_bias_tanh_bf16_out(bn, shape):
+    """The logits epilogue: C = bf16(tanh(A B^T + bias)), via the TMA-store path."""
+    M, N, K = shape
+    g = torch.Generator(device="cpu").manual_seed(7)
+    Al = (0.05 * torch.randn(M, K, generator=g)).to(torch.bfloat16)
+    Bw = (0.05 * torch.randn(K, N, generator=g)).to(torch.bfloat16)  # MN-major weight (dim_in, dim_out)
+    bias = 0.1 * torch.randn(N, generator=g)
+    A, B, bd = Al.cuda(), Bw.cuda(), bias.cuda()
+    C = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    lib = _lib.load()
+    rc = lib.cmt_test_gemm(_lib.MODE_BF16, M, N, K, A.data_ptr(), K, 0, B.data_ptr(), N, 1, C.data_ptr(), N, bn,
+                           2 | 4, bd.data_ptr())
+    assert rc == 0, lib.cmt_last_error(None)
+    ref = torch.tanh(Al.float() @ Bw.float() + bias)
+    err = (C.float().cpu() - ref).abs().max().item()
+    assert err < 1.5e-2 * max(1.0, ref.abs().max().item()), err  # bf16 output rounding + tanh.approx
