@@ -109,6 +109,8 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value); /* "time_do
 int cmt_get_stat(cmt_engine* e, const char* key, double* value, double* count); /* "dominant_ms": mean launch ms */
 
 /* debug: copy an internal buffer (e.g. "Y", "yext:3", "dy:0") as fp32; *n = element count */
+/* debug: per-launch device times ("label\tms\n") recorded since set_option("timeline", 1) */
+int cmt_timeline(cmt_engine* e, char* buf, long long cap);
 int cmt_debug_buffer(cmt_engine* e, const char* name, float* out, long long cap, long long* n);
 /* test hooks (parity tests only; device pointers): one GEMM C = A B^T (fp32 out), one dropout site */
 /* flags: 1 = accumulate into C, 2 = bf16 C, 4 = tanh; bias may be NULL */

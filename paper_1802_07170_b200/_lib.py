@@ -33,7 +33,7 @@ EXPORTS = [
     "cmt_create", "cmt_destroy", "cmt_last_error", "cmt_num_blocks", "cmt_block_info",
     "cmt_upload_param", "cmt_download_param", "cmt_download_grad", "cmt_stage_batch",
     "cmt_run_step", "cmt_train_step", "cmt_wait", "cmt_set_comm", "cmt_nccl_unique_id", "cmt_event_record",
-    "cmt_event_elapsed", "cmt_launch_count", "cmt_set_option", "cmt_get_stat", "cmt_debug_buffer", "cmt_test_gemm", "cmt_test_dropout",
+    "cmt_event_elapsed", "cmt_launch_count", "cmt_set_option", "cmt_get_stat", "cmt_debug_buffer", "cmt_test_gemm", "cmt_test_dropout", "cmt_timeline",
 ]
 
 
@@ -95,6 +95,7 @@ def load(path=LIB_PATH):
     lib.cmt_get_stat.argtypes = [VP, ctypes.c_char_p, P(D), P(D)]
     lib.cmt_test_gemm.argtypes = [I, I, I, I, VP, LL, I, VP, LL, I, VP, LL, I, I, VP]
     U = ctypes.c_ulonglong
+    lib.cmt_timeline.argtypes = [VP, ctypes.c_char_p, LL]
     lib.cmt_test_dropout.argtypes = [U, U, U, U, U, I, I, D, VP, VP, VP]
     _lib = lib
     return lib

@@ -29,6 +29,7 @@
 #include "kernels.cuh"
 #include "lstm_persistent.cuh"
 #include "lstm_cluster.cuh"
+#include "lstm_multi.cuh"
 
 namespace cmt {
 unsigned long long g_launches = 0;
@@ -129,6 +130,27 @@ struct Mat {
 
 static int g_num_sms = 148;
 
+// ---- kernel timeline (debug option "timeline"): an event after every launch
+// on the engine stream; consecutive event deltas are the per-launch device
+// times measured in the real step, not under a profiler ----
+struct Timeline {
+  bool on = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  cudaEvent_t start = nullptr;
+};
+static Timeline g_tl;
+static void tl_mark(cudaStream_t st, const std::string& label) {
+  if (!g_tl.on) return;
+  cudaEvent_t ev;
+  CMT_CUDA(cudaEventCreate(&ev));
+  CMT_CUDA(cudaEventRecord(ev, st));
+  g_tl.marks.push_back({label, ev});
+}
+static std::string gemm_label(int M, int N, int K, int BN, int CG) {
+  return "gemm " + std::to_string(M) + "x" + std::to_string(N) + "x" + std::to_string(K) + " t" + std::to_string(BN) +
+         (CG == 2 ? "x2" : "");
+}
+
 static int g_gemm_opt = 0;  // option: bit 0 natural K order, bit 1 N-fastest tile order
 template <int BN, int AMN, int BMN, class Epi, int CG = 1, int ST = 0>
 static void launch_tc_impl(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const Epi& e) {
@@ -163,7 +185,7 @@ static void launch_tc_impl(cudaStream_t st, int M, int N, int K, Mat A, Mat B, c
   c.attrs = at;
   c.numAttrs = CG > 1 ? 1 : 0;
   CMT_CUDA(cudaLaunchKernelEx(&c, kfn, ta, tb, tcm, M, N, K, e, g_gemm_opt));
-  CMT_LAUNCHED();
+  CMT_LAUNCHED(); tl_mark(st, gemm_label(M, N, K, BN, CG));
 }
 
 static int g_tma_store = 1;  // option: TMA-store epilogue for EpiStore GEMMs
@@ -285,7 +307,7 @@ class Engine {
   int *src_ids_d, *tgt_in_d, *tgt_out_d;
   float *src_mask_d, *tgt_mask_d;
   void *Xs, *Xt, *top, *u_att, *cst_att, *hod, *Y, *dhpre, *du_att, *dU;
-  float *ux, *alpha, *ho, *losstok, *dcst, *dXemb, *dtop, *dhc, *dcc, *colpart;
+  float *ux, *ux2, *alpha, *ho, *losstok, *dcst, *dXemb, *dtop, *dhc, *dcc, *colpart;
   std::vector<void*> drop_enc, drop_dec;
   std::vector<uint8_t*> keep_enc, keep_dec;
   uint8_t* keep_o;
@@ -300,8 +322,10 @@ class Engine {
   double* normpart;
   unsigned* flags;
   int persistent = 1;  // option: persistent recurrent kernels in bf16 mode
-  int clustered = 1;   // option: cluster K-split variant of the persistent kernels
+  int clustered = 1;   // option: cluster K-split variant of the persistent kernels (backward)
+  int clustered_fwd = 0;  // option: cluster K-split forward (slower than the plain persistent one at c3)
   int cg2 = 1;         // option: CTA-pair (cta_group::2) tiles for the large GEMMs
+  int dual = 1;        // option: run independent scans of the layer graph two at a time
   // data parallel (NCCL): dense all-reduce of grads, loss and status
   void* comm = nullptr;
   int rank = 0, world = 1;
@@ -477,7 +501,7 @@ class Engine {
   }
   void refresh_shadow(const float* s, bf16* d, size_t n) {
     to_bf16_kernel<<<std::min<long long>(4096, ceil_div(n, 256)), 256, 0, st>>>(s, d, (long long)n);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "to_bf16_kernel");
     CMT_CUDA(cudaStreamSynchronize(st));
   }
   void download(int idx, float* h, long long rows, long long cols, bool grad) {
@@ -550,6 +574,7 @@ class Engine {
     Xt = carve<char>(cur, NT * E * asz);
     top = carve<char>(cur, NS * H * asz);
     ux = carve<float>(cur, Nmax * 4 * H * 4);
+    ux2 = carve<float>(cur, Nmax * 4 * H * 4);
     dU = carve<char>(cur, Nmax * 4 * H * asz);
     drop_enc.assign(L + 1, nullptr); keep_enc.assign(L + 1, nullptr);
     drop_dec.assign(L + 1, nullptr); keep_dec.assign(L + 1, nullptr);
@@ -696,7 +721,7 @@ class Engine {
       dim3 grid(ceil_div(N, 64), ceil_div(M, 64));
       gemm_simt_kernel<Epi><<<grid, 256, 0, st>>>((const float*)A.p, A.ld, A.mn, (const float*)Bm.p, Bm.ld, Bm.mn, M,
                                                    N, K, e);
-      CMT_LAUNCHED();
+      CMT_LAUNCHED(); tl_mark(st, "gemm_simt_kernel");
       CMT_CUDA(cudaGetLastError());
       return;
     }
@@ -706,7 +731,7 @@ class Engine {
       dim3 grid(ceil_div(N, 64), ceil_div(M, 64));
       gemm_simt_kernel<Epi, bf16><<<grid, 256, 0, st>>>((const bf16*)A.p, A.ld, A.mn, (const bf16*)Bm.p, Bm.ld, Bm.mn,
                                                           M, N, K, e);
-      CMT_LAUNCHED();
+      CMT_LAUNCHED(); tl_mark(st, "gemm_simt_kernel");
       CMT_CUDA(cudaGetLastError());
       return;
     }
@@ -749,7 +774,7 @@ class Engine {
   template <typename T>
   void launch_gather(const void* table, const int* ids, int N, void* out) {
     gather_rows_kernel<T><<<N, 128, 0, st>>>((const T*)table, E, ids, N, (T*)out);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "gather_rows_kernel");
   }
   void gather(int t, const int* ids, int N, void* out) {
     if (bf) launch_gather<bf16>(table_v(t), ids, N, out);
@@ -761,7 +786,7 @@ class Engine {
     dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, 32), 8));
     float scale = 1.0f / (float)(1.0 - cfg.dropout);
     dropout_fwd_kernel2<TI, TO><<<grid, blk, 0, st>>>((const TI*)x, (TO*)y, keep, N, H, pcg, base, cfg.dropout, scale);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "dropout_fwd_kernel2");
   }
 
   // ---- persistent recurrent kernels (bf16) ----
@@ -797,6 +822,8 @@ class Engine {
     c.numAttrs = cluster > 1 ? 2 : 1;
     CMT_CUDA(cudaLaunchKernelEx(&c, k, a, b, prm));
     CMT_LAUNCHED();
+    tl_mark(st, std::string(std::is_same<P, LstmFwdP>::value ? "lstm_fwd" : "lstm_bwd") +
+                    (cluster > 1 ? "_cluster" : "_persistent"));
   }
 
   // ---- LSTM scans ----
@@ -814,6 +841,67 @@ class Engine {
     return {y, y + slot * asz, c, c + slot};
   }
 
+  // ---- paired forward scans (lstm_multi.cuh) ----
+  struct FwdScan {
+    int l;
+    const void* X;
+    int din, steps;
+    bool reverse;
+    const float* mask;
+    float* uxb;  // hoisted input projection buffer of this scan
+  };
+  bool use_dual_fwd() const {
+    return bf && persistent && dual && H % 64 == 0 && B <= 128 && 2 * mc::Fwd<128>::ctas(H, B) <= g_num_sms &&
+           mc::Fwd<128>::stages(H) >= 2;
+  }
+  void fwd_prep(const FwdScan& f) {  // Ux = X W_x + b (layers.py:354-357, K3)
+    const Layer& ly = layers[f.l];
+    EpiStore e = store(f.uxb, 4LL * H, false);
+    e.bias = dw + ly.b_off;
+    gemm(f.steps * B, 4 * H, f.din, Mat{f.X, f.din, 0}, Mat{wv(ly.w_off), 4LL * H, 1}, e);
+  }
+  template <int ROWS>
+  LstmFwdP fwd_params(const FwdScan& f, CUtensorMap* tmH, CUtensorMap* tmW) {
+    const Layer& ly = layers[f.l];
+    ScanViews v = views(f.l, f.reverse);
+    make_map_kblocks(tmH, lw[f.l].yext, (long long)(f.steps + 1) * B, H, H, ROWS, mc::Fwd<ROWS>::KBOX);
+    make_map(tmW, wv(ly.w_off), 4LL * H, f.din + H, 4LL * H, 64, 64);
+    LstmFwdP prm;
+    prm.ux = f.uxb; prm.y = (bf16*)v.ybase; prm.hprev = (const bf16*)v.hprev; prm.cst = v.cbase; prm.cprev = v.cprev;
+    prm.acts = lw[f.l].acts; prm.tcache = lw[f.l].tc; prm.mask = f.mask; prm.flag = flags + (f.l & 31);
+    prm.steps = f.steps; prm.B = B; prm.H = H; prm.din = f.din; prm.reverse = f.reverse ? 1 : 0;
+    prm.hrow0 = f.reverse ? B : 0;
+    prm.trace = (trace_layer == f.l) ? trace_d : nullptr;
+    prm.stages = mc::Fwd<ROWS>::stages(H);
+    CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
+    return prm;
+  }
+  // two independent scans in one cooperative launch (64 CTAs each at H=1024, B=128)
+  void fwd_pair(const FwdScan& a, const FwdScan& b) {
+    CUtensorMap tm[4];
+    LstmFwdMulti m;
+    m.c[0] = fwd_params<128>(a, &tm[0], &tm[1]);
+    m.c[1] = fwd_params<128>(b, &tm[2], &tm[3]);
+    const int g = mc::Fwd<128>::ctas(H, B);
+    m.split = g;
+    auto k = lstm_fwd_multi<128>;
+    const size_t smem = mc::Fwd<128>::smem(H);
+    CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3(2 * g);
+    c.blockDim = dim3(mc::THREADS);
+    c.dynamicSmemBytes = smem;
+    c.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    c.attrs = at;
+    c.numAttrs = 1;
+    CMT_CUDA(cudaLaunchKernelEx(&c, k, tm[0], tm[1], tm[2], tm[3], m));
+    CMT_LAUNCHED();
+    tl_mark(st, "lstm_fwd_pair");
+  }
+
   void scan_fwd(int l, const void* X, int din, int steps, bool reverse, const float* mask) {
     const Layer& ly = layers[l];
     long long N = (long long)steps * B;
@@ -822,7 +910,7 @@ class Engine {
     e.bias = dw + ly.b_off;
     gemm((int)N, 4 * H, din, Mat{X, din, 0}, Mat{wv(ly.w_off), 4LL * H, 1}, e);
     ScanViews v = views(l, reverse);
-    if (use_cluster_fwd()) {
+    if (use_cluster_fwd() && clustered_fwd) {
       CUtensorMap tmH, tmW;
       make_map_kblocks(&tmH, lw[l].yext, (long long)(steps + 1) * B, H, H, cl::ROWS, cl::KBOX);
       make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 64);
@@ -943,15 +1031,15 @@ class Engine {
     dim3 grid(ceil_div(cols, 256), chunks);
     if (is_act && bf) colsum_partial_kernel<bf16><<<grid, 256, 0, st>>>((const bf16*)D, cols, (int)rows, cols, rows_per, colpart);
     else colsum_partial_kernel<float><<<grid, 256, 0, st>>>((const float*)D, cols, (int)rows, cols, rows_per, colpart);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "colsum_partial_kernel");
     colsum_final_kernel<<<ceil_div(cols, 256), 256, 0, st>>>(colpart, chunks, cols, out);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "colsum_final_kernel");
   }
 
   template <typename T>
   void copy2d(const void* s, long long lds, void* d, long long ldd, int rows, int cols) {
     copy2d_kernel<T, T><<<grid_for((long long)rows * cols), 256, 0, st>>>((const T*)s, lds, (T*)d, ldd, rows, cols);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "copy2d_kernel");
   }
   void copy_act(const void* s, long long lds, void* d, long long ldd, int rows, int cols) {
     if (bf) copy2d<bf16>(s, lds, d, ldd, rows, cols);
@@ -967,6 +1055,7 @@ class Engine {
     double ntok = a.global_ntok > 0 ? a.global_ntok : ntok_local;
     float inv_ntok = (float)(1.0 / (double)(float)ntok);
     CMT_CUDA(cudaMemsetAsync(out_d, 0, sizeof(StepOut), st));
+    tl_mark(st, "<start>");
 
     // ===== forward =====
     gather(0, src_ids_d, (int)NS, Xs);
@@ -976,55 +1065,82 @@ class Engine {
       CMT_CUDA(cudaMemsetAsync((char*)v.hprev + (size_t)(l == 1 ? (S - 1) : 0) * BH * asz, 0, BH * asz, st));
       CMT_CUDA(cudaMemsetAsync((float*)v.cprev + (size_t)(l == 1 ? (S - 1) : 0) * BH, 0, BH * 4, st));
     }
-    scan_fwd(0, Xs, E, S, false, src_mask_d);
-    scan_fwd(1, Xs, E, S, true, src_mask_d);
-    {
+    // dropout draw bases in the reference's draw order: encoder
+    // sites k=2..L, then decoder sites k=2..L, then H_o
+    auto enc_base = [&](int k) { return (unsigned long long)(k - 2) * NS * H; };
+    auto dec_base = [&](int k) { return (unsigned long long)(L - 1) * NS * H + (unsigned long long)(k - 2) * NT * H; };
+    unsigned long long draw = drop ? (unsigned long long)(L - 1) * (NS + NT) * H : 0;
+    auto dropout_site = [&](const void* in, void* out, uint8_t* keep, long long n, unsigned long long base) {
+      if (bf) launch_dropout<bf16, bf16>(in, out, keep, (int)n, base, pcg);
+      else launch_dropout<float, float>(in, out, keep, (int)n, base, pcg);
+    };
+    // decoder layer k starts from encoder layer k's final state (model.py:292-305);
+    // l1.bwd's final sits in slot 0, deep layers' in slot S
+    auto dec_init = [&](int k) {
+      int el = (k == 1) ? 1 : k;
+      size_t fslot = (k == 1) ? 0 : (size_t)S;
+      copy_act((char*)lw[el].yext + fslot * BH * asz, H, lw[L + k].yext, H, B, H);
+      CMT_CUDA(cudaMemcpyAsync(lw[L + k].cext, lw[el].cext + fslot * BH, BH * 4, cudaMemcpyDeviceToDevice, st));
+    };
+    // input of decoder layer k (k >= 2: dropout of layer k-1's output)
+    auto dec_input = [&](int k) -> const void* {
+      if (k == 1) return Xt;
+      const void* prev = views(L + k - 1, false).ybase;
+      if (!drop) { drop_dec[k] = const_cast<void*>(prev); return prev; }
+      dropout_site(prev, drop_dec[k], keep_dec[k], NT, dec_base(k));
+      return drop_dec[k];
+    };
+    auto enc_input = [&](int k, const void* cur) -> const void* {
+      if (!drop) { drop_enc[k] = const_cast<void*>(cur); return cur; }
+      dropout_site(cur, drop_enc[k], keep_enc[k], NS, enc_base(k));
+      return drop_enc[k];
+    };
+    auto add_top = [&]() {
       ScanViews f = views(0, false), r = views(1, true);
       if (bf) add2_kernel<bf16><<<grid_for(NS * H), 256, 0, st>>>((const bf16*)f.ybase, (const bf16*)r.ybase, (bf16*)top, NS * H);
       else add2_kernel<float><<<grid_for(NS * H), 256, 0, st>>>((const float*)f.ybase, (const float*)r.ybase, (float*)top, NS * H);
-      CMT_LAUNCHED();
-    }
-    unsigned long long draw = 0;
-    const void* cur = top;
-    for (int k = 2; k <= L; ++k) {
-      const void* in = cur;
-      if (drop) {
-        if (bf) launch_dropout<bf16, bf16>(cur, drop_enc[k], keep_enc[k], (int)NS, draw, pcg);
-        else launch_dropout<float, float>(cur, drop_enc[k], keep_enc[k], (int)NS, draw, pcg);
-        draw += (unsigned long long)NS * H;
-        in = drop_enc[k];
-      } else {
-        drop_enc[k] = const_cast<void*>(cur);
-      }
+      CMT_LAUNCHED(); tl_mark(st, "add2_kernel");
+    };
+    auto zero_enc_state = [&](int k) {
       CMT_CUDA(cudaMemsetAsync(lw[k].yext, 0, BH * asz, st));
       CMT_CUDA(cudaMemsetAsync(lw[k].cext, 0, BH * 4, st));
-      scan_fwd(k, in, H, S, false, src_mask_d);
-      cur = views(k, false).ybase;
+    };
+    if (use_dual_fwd()) {
+      // two independent scans per launch: (e1f, e1b), (e2, d1), ..., (eL, d(L-1)), then dL
+      FwdScan a{0, Xs, E, S, false, src_mask_d, ux}, b{1, Xs, E, S, true, src_mask_d, ux2};
+      fwd_prep(a); fwd_prep(b); fwd_pair(a, b);
+      add_top();
+      const void* cur = top;
+      for (int k = 2; k <= L; ++k) {
+        const void* in = enc_input(k, cur);
+        zero_enc_state(k);
+        const void* xd = dec_input(k - 1);
+        dec_init(k - 1);
+        FwdScan e{k, in, H, S, false, src_mask_d, ux}, d{L + k - 1, xd, k - 1 == 1 ? E : H, T, false, nullptr, ux2};
+        fwd_prep(e); fwd_prep(d); fwd_pair(e, d);
+        cur = views(k, false).ybase;
+      }
+      const void* xd = dec_input(L);
+      dec_init(L);
+      scan_fwd(2 * L, xd, L == 1 ? E : H, T, false, nullptr);
+    } else {
+      scan_fwd(0, Xs, E, S, false, src_mask_d);
+      scan_fwd(1, Xs, E, S, true, src_mask_d);
+      add_top();
+      const void* cur = top;
+      for (int k = 2; k <= L; ++k) {
+        const void* in = enc_input(k, cur);
+        zero_enc_state(k);
+        scan_fwd(k, in, H, S, false, src_mask_d);
+        cur = views(k, false).ybase;
+      }
+      for (int k = 1; k <= L; ++k) {
+        const void* x = dec_input(k);
+        dec_init(k);
+        scan_fwd(L + k, x, k == 1 ? E : H, T, false, nullptr);
+      }
     }
     const void* Hs = (L == 1) ? top : views(L, false).ybase;
-    // decoder: layer k starts from encoder layer k's final state (model.py:292-305)
-    const void* x = Xt;
-    for (int k = 1; k <= L; ++k) {
-      int l = L + k;
-      if (k > 1) {
-        const void* prev = views(l - 1, false).ybase;
-        if (drop) {
-          if (bf) launch_dropout<bf16, bf16>(prev, drop_dec[k], keep_dec[k], (int)NT, draw, pcg);
-          else launch_dropout<float, float>(prev, drop_dec[k], keep_dec[k], (int)NT, draw, pcg);
-          draw += (unsigned long long)NT * H;
-          x = drop_dec[k];
-        } else {
-          drop_dec[k] = const_cast<void*>(prev);
-          x = prev;
-        }
-      }
-      // encoder final: l1.bwd final sits in slot 0; deep layers in slot S
-      int el = (k == 1) ? 1 : k;
-      size_t fslot = (k == 1) ? 0 : (size_t)S;
-      copy_act((char*)lw[el].yext + fslot * BH * asz, H, lw[l].yext, H, B, H);
-      CMT_CUDA(cudaMemcpyAsync(lw[l].cext, lw[el].cext + fslot * BH, BH * 4, cudaMemcpyDeviceToDevice, st));
-      scan_fwd(l, x, k == 1 ? E : H, T, false, nullptr);
-    }
     const void* Ht = views(2 * L, false).ybase;
     // attention (attention.py:146-173)
     copy_act(Ht, H, (char*)cst_att + (size_t)H * asz, 2LL * H, (int)NT, H);
@@ -1040,7 +1156,7 @@ class Engine {
         attn_fwd_kernel<float><<<B, ATT_THREADS, smem, st>>>((const float*)Hs, (const float*)u_att, src_mask_d, S, T, B,
                                                                H, alpha, (float*)cst_att, 2LL * H, status_d);
       }
-      CMT_LAUNCHED();
+      CMT_LAUNCHED(); tl_mark(st, "attn_fwd_kernel");
       CMT_CUDA(cudaGetLastError());
     }
     {
@@ -1057,7 +1173,7 @@ class Engine {
     } else {
       if (bf) {
         copy2d_kernel<float, bf16><<<grid_for(NT * H), 256, 0, st>>>(ho, H, (bf16*)hod, H, (int)NT, H);
-        CMT_LAUNCHED();
+        CMT_LAUNCHED(); tl_mark(st, "copy2d_kernel");
       } else {
         CMT_CUDA(cudaMemcpyAsync(hod, ho, NT * H * 4, cudaMemcpyDeviceToDevice, st));
       }
@@ -1085,9 +1201,9 @@ class Engine {
                                                            cfg.output_tanh, losstok, status_d);
     else ce_kernel<float><<<(int)NT, CE_THREADS, 0, st>>>((float*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon, inv_ntok,
                                                          cfg.output_tanh, losstok, status_d);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "ce_kernel");
     sum_to_double_kernel<<<1, 1024, 0, st>>>(losstok, (int)NT, losssum_d);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "sum_to_double_kernel");
 
     if (stop_after == 2) { CMT_CUDA(cudaStreamSynchronize(st)); return; }
     // ===== backward =====
@@ -1117,7 +1233,7 @@ class Engine {
         attn_bwd_kernel<float><<<B, ATT_THREADS, smem, st>>>((const float*)Hs, (const float*)u_att, alpha, dcst, 2LL * H, S,
                                                                T, B, H, dHs, (float*)du_att);
       }
-      CMT_LAUNCHED();
+      CMT_LAUNCHED(); tl_mark(st, "attn_bwd_kernel");
       CMT_CUDA(cudaGetLastError());
     }
     // W_a (attention.py:166): dW_a and dH_t = du W_a^T + dC_st[:, H:]
@@ -1149,7 +1265,7 @@ class Engine {
     for (int t = 0; t < n_tables; ++t) {
       if (nuniq[t] == 0) continue;
       scatter_compact_kernel<<<nuniq[t], 128, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t], gcomp[t]);
-      CMT_LAUNCHED();
+      CMT_LAUNCHED(); tl_mark(st, "scatter_compact_kernel");
     }
 
     // ===== data parallel: sum grads / loss / status over ranks (NCCL) =====
@@ -1160,7 +1276,7 @@ class Engine {
         CMT_CUDA(cudaMemsetAsync(demb[t], 0, (size_t)V * E * 4, st));
         if (nuniq[t]) {
           scatter_rows_kernel<<<nuniq[t], 128, 0, st>>>(gcomp[t], E, uniq_d[t], nuniq[t], demb[t]);
-          CMT_LAUNCHED();
+          CMT_LAUNCHED(); tl_mark(st, "scatter_rows_kernel");
         }
         allreduce(demb[t], (size_t)V * E, NCCL_FLOAT32);
       }
@@ -1170,33 +1286,33 @@ class Engine {
     // ===== global-norm clip + SGD (training.py:123-142) =====
     int nparts = 0;
     sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(dg, (long long)dense_n, normpart);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "sumsq_partial_kernel");
     nparts += NORM_BLOCKS;
     for (int t = 0; t < n_tables; ++t) {
       if (!dp && nuniq[t] == 0) continue;
       const float* gsrc = dp ? demb[t] : gcomp[t];
       long long gn = dp ? (long long)V * E : (long long)nuniq[t] * E;
       sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(gsrc, gn, normpart + nparts);
-      CMT_LAUNCHED();
+      CMT_LAUNCHED(); tl_mark(st, "sumsq_partial_kernel");
       nparts += NORM_BLOCKS;
     }
     clip_scale_kernel<<<1, 32, 0, st>>>(normpart, nparts, a.lr, a.clip_norm, normscal_d, s32_d, status_d);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "clip_scale_kernel");
     if (!(a.flags & CMT_FLAG_NO_UPDATE)) {
       sgd_dense_kernel<<<grid_for((long long)dense_n), 256, 0, st>>>(dw, dg, bf ? dsh : nullptr, (long long)dense_n, s32_d,
                                                                      status_d);
-      CMT_LAUNCHED();
+      CMT_LAUNCHED(); tl_mark(st, "sgd_dense_kernel");
       for (int t = 0; t < n_tables; ++t) {
         if (dp) {  // union of all ranks' rows: dense update (zero rows are exact no-ops)
           sgd_dense_kernel<<<grid_for((long long)V * E), 256, 0, st>>>(emb_w[t], demb[t], bf ? emb_sh[t] : nullptr,
                                                                       (long long)V * E, s32_d, status_d);
-          CMT_LAUNCHED();
+          CMT_LAUNCHED(); tl_mark(st, "sgd_dense_kernel");
           continue;
         }
         if (nuniq[t] == 0) continue;
         sgd_rows_kernel<<<nuniq[t], 128, 0, st>>>(emb_w[t], bf ? emb_sh[t] : nullptr, E, uniq_d[t], nuniq[t], gcomp[t],
                                                    s32_d, status_d);
-        CMT_LAUNCHED();
+        CMT_LAUNCHED(); tl_mark(st, "sgd_rows_kernel");
       }
     }
     CMT_CUDA(cudaGetLastError());
@@ -1439,8 +1555,15 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "persistent") e->eng->persistent = (int)value;
     else if (k == "cluster") e->eng->clustered = (int)value;
     else if (k == "cg2") e->eng->cg2 = (int)value;
+    else if (k == "dual") e->eng->dual = (int)value;
+    else if (k == "cluster_fwd") e->eng->clustered_fwd = (int)value;
     else if (k == "tma_store") cmt::g_tma_store = (int)value;
     else if (k == "gemm_opt") cmt::g_gemm_opt = (int)value;
+    else if (k == "timeline") {
+      cmt::g_tl.on = value != 0;
+      for (auto& m : cmt::g_tl.marks) cudaEventDestroy(m.second);
+      cmt::g_tl.marks.clear();
+    }
     else if (k == "trace_layer") {
       e->eng->trace_layer = (int)value;
       if (!e->eng->trace_d) CMT_CUDA(cudaMalloc(&e->eng->trace_d, 4096 * 8));
@@ -1448,6 +1571,25 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     }
     else if (k == "stop_after") e->eng->stop_after = (int)value;
     else throw Error(cmt::CMT_ERR_CONFIG, "unknown option " + k);
+  });
+}
+// Timeline of the launches recorded since the option "timeline" was set:
+// "label<TAB>ms" per launch (ms since the previous mark), newline separated.
+int cmt_timeline(cmt_engine* e, char* buf, long long cap) {
+  return guard(e, [&] {
+    CMT_CUDA(cudaDeviceSynchronize());
+    std::string out;
+    auto& mk = cmt::g_tl.marks;
+    for (size_t i = 1; i < mk.size(); ++i) {
+      if (mk[i].first == "<start>") continue;
+      float ms = 0;
+      CMT_CUDA(cudaEventElapsedTime(&ms, mk[i - 1].second, mk[i].second));
+      out += mk[i].first + "\t" + std::to_string(ms) + "\n";
+    }
+    for (auto& m : mk) cudaEventDestroy(m.second);
+    mk.clear();
+    if ((long long)out.size() + 1 > cap) throw Error(cmt::CMT_ERR_SHAPE, "timeline buffer too small");
+    memcpy(buf, out.c_str(), out.size() + 1);
   });
 }
 int cmt_debug_buffer(cmt_engine* e, const char* name, float* out, long long cap, long long* n) {

@@ -1,0 +1,240 @@
+// Multi-chain persistent recurrent LSTM forward (bf16 production path).
+//
+// Same per-CTA contract as lstm_fwd_persistent (W_h slice resident in smem,
+// h_{t-1} streamed by TMA into a stage ring, tcgen05.mma into TMEM, fused cell
+// epilogue with c/h in registers, grid step counter instead of launches), but
+// one cooperative launch runs up to two INDEPENDENT scans side by side on
+// disjoint CTA ranges.  The encoder/decoder layer graph has two independent
+// scans at every level (enc.l1 fwd || bwd, enc.l(k+1) || dec.lk), so the
+// forward's critical path shrinks from 2L+1 scans to L+1.
+//
+// ROWS = batch rows per CTA.  ROWS = 128 (whole batch, 64 CTAs per chain at
+// H=1024) is the paired configuration: each CTA streams the full h_{t-1}
+// (B x H bf16) per step and every accumulator row is useful.  ROWS = 64 splits
+// the batch over two CTAs (128 CTAs, the single-chain configuration).
+// Reference semantics: layers.py:344-363 (cell), layers.py:440-470 (scan).
+#pragma once
+#include "lstm_persistent.cuh"
+
+namespace cmt {
+namespace mc {
+constexpr int THREADS = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4.. cell epilogue (ROWS/32 warps)
+constexpr int MAX_STAGES = 8;
+constexpr int STAGE_BYTES = 32 * 1024;
+constexpr int FWD_NG = 64;  // gate columns (16 units) per CTA
+constexpr size_t SMEM_LIMIT = 227 * 1024;
+template <int ROWS>
+struct Fwd {
+  static constexpr int KBLK = ROWS * 128;            // [ROWS rows][64] bf16 k-block tile
+  static constexpr int KBOX = STAGE_BYTES / KBLK;    // k-blocks per (3-D) TMA = one stage
+  static constexpr int PAD = ROWS < 128 ? KBLK : 0;  // UMMA M=128 reads 128 rows past the last tile
+  static int stages(int H) {
+    long long room = (long long)SMEM_LIMIT - 1024 - 256 - PAD - (long long)H * 128;
+    long long s = room / STAGE_BYTES;
+    return (int)(s > MAX_STAGES ? MAX_STAGES : s);
+  }
+  static size_t smem(int H) { return 1024 + (size_t)H * 128 + (size_t)stages(H) * STAGE_BYTES + PAD + 256; }
+  static int ctas(int H, int B) { return (4 * H / FWD_NG) * ((B + ROWS - 1) / ROWS); }
+};
+}  // namespace mc
+
+struct LstmFwdMulti {
+  LstmFwdP c[2];
+  int split;  // CTAs [0, split) run chain 0, [split, grid) chain 1
+};
+
+template <int ROWS>
+__global__ void __launch_bounds__(mc::THREADS, 1)
+    lstm_fwd_multi(const __grid_constant__ CUtensorMap tmH0, const __grid_constant__ CUtensorMap tmW0,
+                   const __grid_constant__ CUtensorMap tmH1, const __grid_constant__ CUtensorMap tmW1,
+                   const LstmFwdMulti m) {
+  using F = mc::Fwd<ROWS>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int ch = (int)blockIdx.x >= m.split ? 1 : 0;
+  const LstmFwdP p = ch ? m.c[1] : m.c[0];
+  const int bid = ch ? (int)blockIdx.x - m.split : (int)blockIdx.x;
+  const int G = ch ? (int)gridDim.x - m.split : m.split;
+  const void* tmH = ch ? (const void*)&tmH1 : (const void*)&tmH0;
+  const void* tmW = ch ? (const void*)&tmW1 : (const void*)&tmW0;
+
+  const int KB = p.H / 64;
+  uint8_t* sW = smem;                      // KB x [64 K rows][64 N] (MN-major atoms)
+  uint8_t* sA = smem + (size_t)KB * 8192;  // stages x KBOX x [ROWS][64] (K-major) + pad
+  uint64_t* full = (uint64_t*)(sA + p.stages * mc::STAGE_BYTES + F::PAD);
+  uint64_t* empty = full + mc::MAX_STAGES;
+  uint64_t* wfull = empty + mc::MAX_STAGES;
+  uint64_t* tfull = wfull + 1;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
+  constexpr int EPI_W = ROWS / 32;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nh = (p.B + ROWS - 1) / ROWS;
+  const int half = bid % nh;
+  const int n0 = (bid / nh) * mc::FWD_NG;
+  const int u0 = n0 >> 2;
+  const int r0 = half * ROWS;
+  if (threadIdx.x == 0) {
+    ptx::prefetch_tmap(tmH);
+    ptx::prefetch_tmap(tmW);
+    for (int i = 0; i < p.stages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    ptx::mbar_init(wfull, 1);
+    ptx::mbar_init(tfull, 1);
+    ptx::mbar_init(tempty, EPI_W);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, 64);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_expect_tx(wfull, KB * 8192);
+      for (int kb = 0; kb < KB; ++kb) ptx::tma_load_2d(tmW, wfull, sW + kb * 8192, n0, p.din + kb * 64);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int s = 0; s < p.steps; ++s) {
+        const int t = p.reverse ? p.steps - 1 - s : s;
+        if (s > 0) {
+          const unsigned target = (unsigned)(G * s);
+          while (ptx::ld_relaxed(p.flag) < target) {}
+          ptx::fence_acquire_gpu();
+          ptx::fence_proxy_async_global();
+        }
+        if (p.trace && bid == 0) p.trace[s * 8 + 0] = gtimer();
+        const int hrow = p.hrow0 + t * p.B + r0;
+        for (int kb = 0; kb < KB; kb += F::KBOX) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::tma_load_3d(tmH, &full[stage], sA + stage * mc::STAGE_BYTES, 0, hrow, kb);
+          ptx::mbar_expect_tx(&full[stage], mc::STAGE_BYTES);
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_bf16(128, mc::FWD_NG, 0, 1);
+      ptx::mbar_wait(wfull, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t wbase = ptx::smem_u32(sW);
+      for (int s = 0; s < p.steps; ++s) {
+        ptx::mbar_wait(tempty, (s & 1) ^ 1);
+        ptx::tc_fence_after();
+        for (int kb0 = 0; kb0 < KB; kb0 += F::KBOX) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a0 = ptx::smem_u32(sA + stage * mc::STAGE_BYTES);
+#pragma unroll
+          for (int j = 0; j < F::KBOX; ++j) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              uint64_t ad = ptx::smem_desc_sw128(a0 + j * F::KBLK + kk * 32, 16, 1024);
+              uint64_t bd = ptx::smem_desc_sw128(wbase + (kb0 + j) * 8192 + kk * 2048, 8192, 1024);
+              ptx::umma_bf16(tmem, ad, bd, idesc, (kb0 | j | kk) ? 1u : 0u);
+            }
+          }
+          ptx::umma_commit(&empty[stage]);
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+        ptx::umma_commit(tfull);
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + EPI_W) {
+    const int q = warp & 3;
+    const int b = r0 + q * 32 + lane;
+    const bool valid = b < p.B;
+    const long long H = p.H;
+    float c[16], h[16];
+    {
+      const int t0 = p.reverse ? p.steps - 1 : 0;
+      const long long rr = (long long)t0 * p.B + b;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        c[u] = valid ? p.cprev[rr * H + u0 + u] : 0.f;
+        h[u] = valid ? __bfloat162float(p.hprev[rr * H + u0 + u]) : 0.f;
+      }
+    }
+    for (int s = 0; s < p.steps; ++s) {
+      const int t = p.reverse ? p.steps - 1 - s : s;
+      const long long row = (long long)t * p.B + b;
+      float4 x[16];
+      float mk = 1.f;
+      if (valid) {
+        const float4* uxr = (const float4*)(p.ux + row * 4 * H + n0);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) x[u] = __ldg(uxr + u);
+        if (p.mask) mk = __ldg(p.mask + row);
+      }
+      ptx::mbar_wait(tfull, s & 1);
+      ptx::tc_fence_after();
+      if (p.trace && bid == 0 && threadIdx.x == 128) p.trace[s * 8 + 1] = gtimer();
+      float v[64];
+      ptx::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16), v);
+      ptx::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 32, v + 32);
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(tempty);
+      float tcv[16];
+      if (valid) {
+        __align__(16) bf16 hb[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const float gi = ptx::sigmoid_fast(v[4 * u + 0] + x[u].x);
+          const float gf = ptx::sigmoid_fast(v[4 * u + 1] + x[u].y);
+          const float gg = ptx::tanh_fast(v[4 * u + 2] + x[u].z);
+          const float go = ptx::sigmoid_fast(v[4 * u + 3] + x[u].w);
+          const float cn = gf * c[u] + gi * gg;
+          const float tcn = ptx::tanh_fast(cn);
+          const float hn = go * tcn;
+          if (p.mask) {
+            h[u] = mk * hn + (1.f - mk) * h[u];
+            c[u] = mk * cn + (1.f - mk) * c[u];
+          } else {
+            h[u] = hn;
+            c[u] = cn;
+          }
+          x[u] = make_float4(gi, gf, gg, go);  // reuse: activations for the cache
+          tcv[u] = tcn;
+          hb[u] = __float2bfloat16_rn(h[u]);
+        }
+        uint4* yr = (uint4*)(p.y + row * H + u0);
+        yr[0] = ((uint4*)hb)[0];
+        yr[1] = ((uint4*)hb)[1];
+      }
+      if (p.trace && bid == 0 && threadIdx.x == 128) p.trace[s * 8 + 2] = gtimer();
+      // publish h_t (the only value other CTAs need), then write the BPTT caches
+      ptx::named_bar_sync(1, ROWS);
+      if (threadIdx.x == 128) {
+        ptx::red_release_add(p.flag, 1u);
+        if (p.trace && bid == 0) p.trace[s * 8 + 3] = gtimer();
+      }
+      if (valid) {
+        float4* ar = (float4*)(p.acts + row * 4 * H + n0);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) ar[u] = x[u];
+        float4* tcr = (float4*)(p.tcache + row * H + u0);
+        float4* csr = (float4*)(p.cst + row * H + u0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          tcr[k] = make_float4(tcv[4 * k], tcv[4 * k + 1], tcv[4 * k + 2], tcv[4 * k + 3]);
+          csr[k] = make_float4(c[4 * k], c[4 * k + 1], c[4 * k + 2], c[4 * k + 3]);
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 64);
+  }
+}
+
+}  // namespace cmt

@@ -205,6 +205,16 @@ class Engine:
     def set_option(self, key, value):
         self._check(self.lib.cmt_set_option(self.h, key.encode(), int(value)))
 
+    def timeline(self, cap=1 << 22):
+        """[(label, ms)] per launch since set_option("timeline", 1) (debug)."""
+        buf = ctypes.create_string_buffer(cap)
+        self._check(self.lib.cmt_timeline(self.h, buf, cap))
+        out = []
+        for line in buf.value.decode().splitlines():
+            lab, ms = line.rsplit("\t", 1)
+            out.append((lab, float(ms)))
+        return out
+
     def stat(self, key):
         v, c = ctypes.c_double(), ctypes.c_double()
         self._check(self.lib.cmt_get_stat(self.h, key.encode(), ctypes.byref(v), ctypes.byref(c)))

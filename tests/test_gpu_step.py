@@ -220,15 +220,21 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
     src, sm, tgt, tm = O.synthetic_batch(V, S, T, B, seed=6, ragged=ragged)
     _, _, og, _, _ = oracle_step(d, params, (src, sm, tgt, tm), 0.1, 1.0, 5.0, 3, update=False)
     out = {}
-    for variant in ("per_step", "persistent", "cluster"):
+    variants = {  # option settings per variant ("dual" = the default configuration)
+        "per_step": dict(persistent=0, dual=0, cluster=0),
+        "persistent": dict(persistent=1, dual=0, cluster=0),
+        "cluster": dict(persistent=1, dual=0, cluster=1, cluster_fwd=1),
+        "dual": dict(),
+    }
+    for variant, opts in variants.items():
         eng = Engine(cfg_of(d), mode="bf16")
-        eng.set_option("persistent", int(variant != "per_step"))
-        eng.set_option("cluster", int(variant == "cluster"))
+        for k, v in opts.items():
+            eng.set_option(k, v)
         eng.upload(params)
         eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, np.random.Generator(np.random.PCG64(3)), update=False)
         out[variant] = eng.grads()
         eng.close()
-    for v in ("persistent", "cluster"):
+    for v in ("persistent", "cluster", "dual"):
         for n in og:
             assert O.norm_rel_err(out[v][n], out["per_step"][n]) < BF16_TOL, (v, n)
             assert O.norm_rel_err(out[v][n], og[n]) < BF16_TOL, (v, n)
