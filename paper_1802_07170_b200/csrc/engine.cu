@@ -30,6 +30,7 @@
 #include "lstm_persistent.cuh"
 #include "lstm_cluster.cuh"
 #include "lstm_multi.cuh"
+#include "attention.cuh"
 
 namespace cmt {
 unsigned long long g_launches = 0;
@@ -1145,7 +1146,20 @@ class Engine {
     // attention (attention.py:146-173)
     copy_act(Ht, H, (char*)cst_att + (size_t)H * asz, 2LL * H, (int)NT, H);
     gemm((int)NT, H, H, Mat{Ht, H, 0}, Mat{wv(off_wa), H, 1}, store(u_att, H, true));
-    {
+    if (S <= att::P && T <= att::P) {
+      const size_t smem = att::fwd_smem();
+      if (bf) {
+        CMT_CUDA(cudaFuncSetAttribute(attn_fwd_tiled<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attn_fwd_tiled<bf16><<<B, att::THREADS, smem, st>>>((const bf16*)Hs, (const bf16*)u_att, src_mask_d, S, T, B, H,
+                                                            alpha, (bf16*)cst_att, 2LL * H, status_d);
+      } else {
+        CMT_CUDA(cudaFuncSetAttribute(attn_fwd_tiled<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attn_fwd_tiled<float><<<B, att::THREADS, smem, st>>>((const float*)Hs, (const float*)u_att, src_mask_d, S, T, B,
+                                                             H, alpha, (float*)cst_att, 2LL * H, status_d);
+      }
+      CMT_LAUNCHED(); tl_mark(st, "attn_fwd_tiled");
+      CMT_CUDA(cudaGetLastError());
+    } else {
       size_t smem = attn_fwd_smem(S, T);
       if (bf) {
         cudaFuncSetAttribute(attn_fwd_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1222,7 +1236,20 @@ class Engine {
     // attention core backward
     float* dHs = (L == 1) ? dtop : lw[L].dy;
     CMT_CUDA(cudaMemsetAsync(dHs, 0, NS * H * 4, st));
-    {
+    if (S <= att::P && T <= att::P) {
+      const size_t smem = att::bwd_smem();
+      if (bf) {
+        CMT_CUDA(cudaFuncSetAttribute(attn_bwd_tiled<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attn_bwd_tiled<bf16><<<B, att::THREADS, smem, st>>>((const bf16*)Hs, (const bf16*)u_att, alpha, dcst, 2LL * H, S, T,
+                                                            B, H, dHs, (bf16*)du_att);
+      } else {
+        CMT_CUDA(cudaFuncSetAttribute(attn_bwd_tiled<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attn_bwd_tiled<float><<<B, att::THREADS, smem, st>>>((const float*)Hs, (const float*)u_att, alpha, dcst, 2LL * H, S,
+                                                             T, B, H, dHs, (float*)du_att);
+      }
+      CMT_LAUNCHED(); tl_mark(st, "attn_bwd_tiled");
+      CMT_CUDA(cudaGetLastError());
+    } else {
       size_t smem = attn_bwd_smem(S, T);
       if (bf) {
         cudaFuncSetAttribute(attn_bwd_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
