@@ -307,7 +307,7 @@ class Engine {
   std::vector<LayerWS> lw;
   int *src_ids_d, *tgt_in_d, *tgt_out_d;
   float *src_mask_d, *tgt_mask_d;
-  void *Xs, *Xt, *top, *u_att, *cst_att, *hod, *Y, *dhpre, *du_att, *dU;
+  void *Xs, *Xt, *top, *u_att, *cst_att, *hod, *Y, *dhpre, *du_att, *dU, *dU2;
   float *ux, *ux2, *alpha, *ho, *losstok, *dcst, *dXemb, *dtop, *dhc, *dcc, *colpart;
   std::vector<void*> drop_enc, drop_dec;
   std::vector<uint8_t*> keep_enc, keep_dec;
@@ -577,6 +577,7 @@ class Engine {
     ux = carve<float>(cur, Nmax * 4 * H * 4);
     ux2 = carve<float>(cur, Nmax * 4 * H * 4);
     dU = carve<char>(cur, Nmax * 4 * H * asz);
+    dU2 = carve<char>(cur, Nmax * 4 * H * asz);
     drop_enc.assign(L + 1, nullptr); keep_enc.assign(L + 1, nullptr);
     drop_dec.assign(L + 1, nullptr); keep_dec.assign(L + 1, nullptr);
     for (int k = 2; k <= L; ++k) {
@@ -852,7 +853,8 @@ class Engine {
     float* uxb;  // hoisted input projection buffer of this scan
   };
   bool use_dual_fwd() const {
-    return bf && persistent && dual && H % 64 == 0 && B <= 128 && 2 * mc::Fwd<128>::ctas(H, B) <= g_num_sms &&
+    return bf && persistent && dual && H % (64 * mc::Fwd<128>::KBOX) == 0 && B <= 128 &&
+           2 * mc::Fwd<128>::ctas(H, B) <= g_num_sms &&
            mc::Fwd<128>::stages(H) >= 2;
   }
   void fwd_prep(const FwdScan& f) {  // Ux = X W_x + b (layers.py:354-357, K3)
@@ -954,6 +956,89 @@ class Engine {
   }
 
   // BPTT for layer l; writes dX (= or +=, optional dropout mask) and param grads.
+  // ---- paired backward scans (lstm_multi.cuh) ----
+  struct BwdScan {
+    int l;
+    const void* X;
+    int din, steps;
+    bool reverse;
+    const float* mask;
+    const float* dy;
+    const float* dh_final;
+    const float* dc_final;
+    float* dh0;
+    float* dc0;
+    float* dX;
+    int dx_beta;
+    const uint8_t* dx_keep;
+    void* dUb;
+  };
+  bool use_dual_bwd() const {
+    return bf && persistent && dual && H % mc::BWD_NU == 0 && (H / 64) % mc::BWD_KBOX == 0 && B <= 128 &&
+           2 * mc::bwd_ctas(H) <= g_num_sms &&
+           mc::bwd_stages(H) >= 1 && (size_t)mc::bwd_stages(H) * mc::STAGE_BYTES >= (size_t)128 * mc::XROW;
+  }
+  LstmBwdP bwd_params(const BwdScan& f, CUtensorMap* tmA, CUtensorMap* tmW) {
+    const Layer& ly = layers[f.l];
+    ScanViews v = views(f.l, f.reverse);
+    long long N = (long long)f.steps * B;
+    make_map_kblocks(tmA, f.dUb, N, 4LL * H, 4LL * H, 128, mc::BWD_KBOX);
+    make_map(tmW, wv(ly.w_off), 4LL * H, f.din + H, 4LL * H, 64, mc::BWD_NU);
+    LstmBwdP prm;
+    prm.dy = f.dy; prm.acts = lw[f.l].acts; prm.tcache = lw[f.l].tc; prm.cprev = v.cprev; prm.mask = f.mask;
+    prm.dU = (bf16*)f.dUb; prm.dh_final = f.dh_final; prm.dc_final = f.dc_final; prm.dh0 = f.dh0; prm.dc0 = f.dc0;
+    prm.flag = flags + 32 + (f.l & 31);
+    prm.steps = f.steps; prm.B = B; prm.H = H; prm.din = f.din; prm.reverse = f.reverse ? 1 : 0;
+    prm.trace = (trace_layer == 100 + f.l) ? trace_d : nullptr;
+    prm.stages = mc::bwd_stages(H);
+    CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
+    return prm;
+  }
+  void bwd_pair(const BwdScan& a, const BwdScan& b) {
+    CUtensorMap tm[4];
+    LstmBwdMulti m;
+    m.c[0] = bwd_params(a, &tm[0], &tm[1]);
+    m.c[1] = bwd_params(b, &tm[2], &tm[3]);
+    const int g = mc::bwd_ctas(H);
+    m.split = g;
+    auto k = lstm_bwd_multi;
+    const size_t smem = mc::bwd_smem(H);
+    CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3(2 * g);
+    c.blockDim = dim3(mc::BWD_THREADS);
+    c.dynamicSmemBytes = smem;
+    c.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = mc::BWD_KS;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    c.attrs = at;
+    c.numAttrs = 2;
+    CMT_CUDA(cudaLaunchKernelEx(&c, k, tm[0], tm[1], tm[2], tm[3], m));
+    CMT_LAUNCHED();
+    tl_mark(st, "lstm_bwd_pair");
+  }
+  // weight grads, bias grads and input grads of a finished BPTT scan
+  void bwd_post(const BwdScan& f) {
+    const Layer& ly = layers[f.l];
+    ScanViews v = views(f.l, f.reverse);
+    long long N = (long long)f.steps * B;
+    // dW[0:din] = X^T dU, dW[din:] = Hprev^T dU  (layers.py:389-391, batched; K6)
+    gemm(f.din, 4 * H, (int)N, Mat{f.X, f.din, 1}, Mat{f.dUb, 4LL * H, 1}, store(dg + ly.w_off, 4LL * H, false));
+    gemm(H, 4 * H, (int)N, Mat{v.hprev, H, 1}, Mat{f.dUb, 4LL * H, 1},
+         store(dg + ly.w_off + (size_t)f.din * 4 * H, 4LL * H, false));
+    colsum(f.dUb, true, N, 4 * H, dg + ly.b_off);
+    // dX = dU W_x^T (layers.py:392; K7), dropout backward fused (layers.py:292-296)
+    EpiStore e = store(f.dX, f.din, false);
+    e.beta = f.dx_beta;
+    if (f.dx_keep) { e.dmask = f.dx_keep; e.ld_dmask = f.din; e.dscale = 1.0f / (float)(1.0 - cfg.dropout); }
+    gemm((int)N, f.din, 4 * H, Mat{f.dUb, 4LL * H, 0}, Mat{wv(ly.w_off), 4LL * H, 0}, e);
+  }
+
   void scan_bwd(int l, const void* X, int din, int steps, bool reverse, const float* mask, const float* dy,
                 const float* dh_final, const float* dc_final, float* dh0, float* dc0, float* dX, int dx_beta,
                 const uint8_t* dx_keep) {
@@ -976,7 +1061,7 @@ class Engine {
       prm.dU = (bf16*)dU; prm.dh_final = dh_final; prm.dc_final = dc_final; prm.dh0 = dh0; prm.dc0 = dc0;
       prm.flag = flags + 32 + (l & 31);
       prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
-      prm.trace = nullptr;
+      prm.trace = (trace_layer == 100 + l) ? trace_d : nullptr;
       prm.stages = cl::bwd_stages(H);
       CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
       launch_coop(lstm_bwd_cluster, cl::BWD_KS * (H / cl::BWD_NU), tmA, tmW, prm, cl::bwd_smem(H), cl::BWD_KS);
@@ -1271,23 +1356,53 @@ class Engine {
       gemm((int)NT, H, H, Mat{du_att, H, 0}, Mat{wv(off_wa), H, 0}, e);
     }
     // decoder BPTT, top layer first (graph.py:112-115); init-state grads -> encoder finals
-    for (int k = L; k >= 1; --k) {
-      int l = L + k;
-      const void* X = (k == 1) ? Xt : drop_dec[k];
-      int din = (k == 1) ? E : H;
-      float* dX = (k == 1) ? dXemb + NS * E : lw[l - 1].dy;
-      const uint8_t* kp = (k > 1 && drop) ? keep_dec[k] : nullptr;
-      scan_bwd(l, X, din, T, false, nullptr, lw[l].dy, nullptr, nullptr, fin_dh[k], fin_dc[k], dX, 0, kp);
-    }
-    // encoder deep layers, top first
-    for (int k = L; k >= 2; --k) {
-      float* dX = (k == 2) ? dtop : lw[k - 1].dy;
-      const uint8_t* kp = drop ? keep_enc[k] : nullptr;
-      scan_bwd(k, drop_enc[k], H, S, false, src_mask_d, lw[k].dy, fin_dh[k], fin_dc[k], nullptr, nullptr, dX, 0, kp);
-    }
+    auto dec_scan = [&](int k, void* dub) {
+      BwdScan f;
+      f.l = L + k; f.X = (k == 1) ? Xt : drop_dec[k]; f.din = (k == 1) ? E : H; f.steps = T; f.reverse = false;
+      f.mask = nullptr; f.dy = lw[L + k].dy; f.dh_final = nullptr; f.dc_final = nullptr;
+      f.dh0 = fin_dh[k]; f.dc0 = fin_dc[k];
+      f.dX = (k == 1) ? dXemb + NS * E : lw[L + k - 1].dy; f.dx_beta = 0;
+      f.dx_keep = (k > 1 && drop) ? keep_dec[k] : nullptr; f.dUb = dub;
+      return f;
+    };
+    auto enc_scan = [&](int k, void* dub) {  // k >= 2
+      BwdScan f;
+      f.l = k; f.X = drop_enc[k]; f.din = H; f.steps = S; f.reverse = false; f.mask = src_mask_d; f.dy = lw[k].dy;
+      f.dh_final = fin_dh[k]; f.dc_final = fin_dc[k]; f.dh0 = nullptr; f.dc0 = nullptr;
+      f.dX = (k == 2) ? dtop : lw[k - 1].dy; f.dx_beta = 0; f.dx_keep = drop ? keep_enc[k] : nullptr; f.dUb = dub;
+      return f;
+    };
     // layer 1: top = y_f + y_b so both directions receive dtop (layers.py:176-180)
-    scan_bwd(1, Xs, E, S, true, src_mask_d, dtop, fin_dh[1], fin_dc[1], nullptr, nullptr, dXemb, 0, nullptr);
-    scan_bwd(0, Xs, E, S, false, src_mask_d, dtop, nullptr, nullptr, nullptr, nullptr, dXemb, 1, nullptr);
+    auto l1_scan = [&](bool bwd_dir, void* dub) {
+      BwdScan f;
+      f.l = bwd_dir ? 1 : 0; f.X = Xs; f.din = E; f.steps = S; f.reverse = bwd_dir; f.mask = src_mask_d; f.dy = dtop;
+      f.dh_final = bwd_dir ? fin_dh[1] : nullptr; f.dc_final = bwd_dir ? fin_dc[1] : nullptr;
+      f.dh0 = nullptr; f.dc0 = nullptr; f.dX = dXemb; f.dx_beta = bwd_dir ? 0 : 1; f.dx_keep = nullptr; f.dUb = dub;
+      return f;
+    };
+    auto single = [&](const BwdScan& f) {
+      scan_bwd(f.l, f.X, f.din, f.steps, f.reverse, f.mask, f.dy, f.dh_final, f.dc_final, f.dh0, f.dc0, f.dX,
+               f.dx_beta, f.dx_keep);
+    };
+    if (use_dual_bwd()) {
+      // pairs of independent scans: dL alone, then (d(k), e(k+1)) for k = L-1..1, then (e1 bwd, e1 fwd)
+      single(dec_scan(L, dU));
+      for (int k = L - 1; k >= 1; --k) {
+        BwdScan d = dec_scan(k, dU), e = enc_scan(k + 1, dU2);
+        bwd_pair(d, e);
+        bwd_post(d);
+        bwd_post(e);
+      }
+      BwdScan b1 = l1_scan(true, dU), f1 = l1_scan(false, dU2);
+      bwd_pair(b1, f1);
+      bwd_post(b1);
+      bwd_post(f1);
+    } else {
+      for (int k = L; k >= 1; --k) single(dec_scan(k, dU));
+      for (int k = L; k >= 2; --k) single(enc_scan(k, dU));
+      single(l1_scan(true, dU));
+      single(l1_scan(false, dU));
+    }
     // embedding grads: deterministic segmented scatter (tensor.py:208-216)
     for (int t = 0; t < n_tables; ++t) {
       if (nuniq[t] == 0) continue;

@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(cl::THREADS, 1)
     ptx::mbar_init(wfull, 1);
     ptx::mbar_init(tfull, 1);
     ptx::mbar_init(tempty, 4);
-    ptx::mbar_init(xfull, 4 * (cl::BWD_KS - 1));
+    ptx::mbar_init(xfull, 1);  // the owner's expect_tx; partner bytes arrive by st.async complete_tx
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 32);
@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(cl::THREADS, 1)
         while (ptx::ld_relaxed(p.flag) < target) {}
         ptx::fence_acquire_gpu();
         ptx::fence_proxy_async_global();
+        if (p.trace && blockIdx.x == 0) p.trace[i * 8 + 0] = gtimer();
         const int arow = time_of(p.steps - i) * p.B;
         for (int kb = 0; kb < KBL; kb += cl::KBOX) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -382,28 +383,26 @@ __global__ void __launch_bounds__(cl::THREADS, 1)
       if (i > 0) {
         ptx::mbar_wait(tfull, (i - 1) & 1);
         ptx::tc_fence_after();
+        if (p.trace && blockIdx.x == 0 && threadIdx.x == 128) p.trace[i * 8 + 1] = gtimer();
         float v[32];
         ptx::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16), v);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(tempty);
-        // send each partner its 8 columns of my partial sum
+        // send each partner its 8 columns of my partial sum (async remote stores
+        // whose bytes complete the partner's xfull phase)
 #pragma unroll
         for (int pr_ = 0; pr_ < cl::BWD_KS; ++pr_) {
           if (pr_ == (int)r) continue;
-          ptx::st_cluster_v4(x_remote[pr_], v[8 * pr_], v[8 * pr_ + 1], v[8 * pr_ + 2], v[8 * pr_ + 3]);
-          ptx::st_cluster_v4(x_remote[pr_] + 16, v[8 * pr_ + 4], v[8 * pr_ + 5], v[8 * pr_ + 6], v[8 * pr_ + 7]);
+          ptx::st_async_v4(x_remote[pr_], v[8 * pr_], v[8 * pr_ + 1], v[8 * pr_ + 2], v[8 * pr_ + 3], xf_remote[pr_]);
+          ptx::st_async_v4(x_remote[pr_] + 16, v[8 * pr_ + 4], v[8 * pr_ + 5], v[8 * pr_ + 6], v[8 * pr_ + 7],
+                           xf_remote[pr_]);
         }
-        ptx::fence_acq_rel_cluster();
-        __syncwarp();
-        if (lane == 0) {
-#pragma unroll
-          for (int pr_ = 0; pr_ < cl::BWD_KS; ++pr_)
-            if (pr_ != (int)r) ptx::mbar_arrive_remote(xf_remote[pr_]);
-        }
+        if (threadIdx.x == 128) ptx::mbar_expect_tx(xfull, (cl::BWD_KS - 1) * cl::ROWS * cl::UPC * 4);
 #pragma unroll
         for (int u = 0; u < cl::UPC; ++u) acc[u] = v[8 * r + u];
         ptx::mbar_wait_cluster(xfull, (i - 1) & 1);
+        if (p.trace && blockIdx.x == 0 && threadIdx.x == 128) p.trace[i * 8 + 2] = gtimer();
 #pragma unroll
         for (int pr_ = 0; pr_ < cl::BWD_KS; ++pr_) {
           if (pr_ == (int)r) continue;
@@ -455,8 +454,12 @@ __global__ void __launch_bounds__(cl::THREADS, 1)
           }
         }
       }
+      if (p.trace && blockIdx.x == 0 && threadIdx.x == 128) p.trace[i * 8 + 3] = gtimer();
       ptx::named_bar_sync(1, 128);
-      if (threadIdx.x == 128) ptx::red_release_add(p.flag, 1u);
+      if (threadIdx.x == 128) {
+        ptx::red_release_add(p.flag, 1u);
+        if (p.trace && blockIdx.x == 0) p.trace[i * 8 + 4] = gtimer();
+      }
     }
   }
   ptx::tc_fence_before();

@@ -237,4 +237,290 @@ __global__ void __launch_bounds__(mc::THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-chain cluster K-split recurrent backward (BPTT) kernel.
+//
+// dh_t[b][j] = sum_gc dU_{t+1}[b][gc] W_h[j][gc]: a cluster of 4 CTAs owns 64
+// units; CTA rank kq contracts the gate columns [kq*H, (kq+1)*H) of dU_{t+1}
+// for all 64 units (M = B <= 128 rows, N = 64, K = H) with its W_h slice
+// resident in smem, then the four partial sums are combined through
+// distributed shared memory: every CTA parks its partials in its own (idle)
+// TMA stage ring and each CTA pulls the 16-unit slice it owns from the other
+// three (ld.shared::cluster).  8 epilogue warps run the cell backward for
+// 16 units x 128 rows.  Two independent scans can share one cooperative
+// launch (the backward layer graph pairs dec.lk with enc.l(k+1), and
+// enc.l1 bwd with enc.l1 fwd).  Reference: layers.py:366-395, 472-493.
+// ---------------------------------------------------------------------------
+namespace mc {
+constexpr int BWD_THREADS = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 cell epilogue
+constexpr int BWD_KS = 4;         // cluster size = K quarters of the 4H gate columns
+constexpr int BWD_NU = 64;        // units per cluster
+constexpr int BWD_UPT = 8;        // units per epilogue thread
+constexpr int BWD_KBLK = 128 * 128;  // [128 rows][64] bf16
+constexpr int BWD_KBOX = STAGE_BYTES / BWD_KBLK;
+constexpr int XROW = BWD_NU * 4;     // bytes of one row of parked partials
+inline size_t bwd_w_bytes(int H) { return (size_t)(H / 64) * BWD_NU * 128; }
+inline int bwd_stages(int H) {
+  long long room = (long long)SMEM_LIMIT - 1024 - 512 - (long long)bwd_w_bytes(H);
+  long long s = room / STAGE_BYTES;
+  return (int)(s > MAX_STAGES ? MAX_STAGES : s);
+}
+inline size_t bwd_smem(int H) { return 1024 + bwd_w_bytes(H) + (size_t)bwd_stages(H) * STAGE_BYTES + 512; }
+inline int bwd_ctas(int H) { return (H / BWD_NU) * BWD_KS; }
+// parked partial of (row b, 16-byte chunk c) at a swizzled offset (conflict-free 16 B stores)
+CMT_D uint32_t xoff(int b, int c) { return (uint32_t)(b * XROW + ((c ^ (b & 15)) << 4)); }
+}  // namespace mc
+
+struct LstmBwdMulti {
+  LstmBwdP c[2];
+  int split;  // multiple of BWD_KS
+};
+
+__global__ void __launch_bounds__(mc::BWD_THREADS, 1)
+    lstm_bwd_multi(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmW0,
+                   const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmW1,
+                   const LstmBwdMulti m) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int ch = (int)blockIdx.x >= m.split ? 1 : 0;
+  const LstmBwdP p = ch ? m.c[1] : m.c[0];
+  const int bid = ch ? (int)blockIdx.x - m.split : (int)blockIdx.x;
+  const int G = ch ? (int)gridDim.x - m.split : m.split;
+  const void* tmA = ch ? (const void*)&tmA1 : (const void*)&tmA0;
+  const void* tmW = ch ? (const void*)&tmW1 : (const void*)&tmW0;
+
+  const int KBL = p.H / 64;  // k-blocks of this CTA's gate-column quarter
+  uint8_t* sW = smem;                                    // KBL x [64 units][64] (K-major)
+  uint8_t* sA = smem + (size_t)KBL * (mc::BWD_NU * 128);  // stage ring; also the parked partials
+  uint64_t* full = (uint64_t*)(sA + (size_t)p.stages * mc::STAGE_BYTES);
+  uint64_t* empty = full + mc::MAX_STAGES;
+  uint64_t* wfull = empty + mc::MAX_STAGES;
+  uint64_t* tfull = wfull + 1;
+  uint64_t* tempty = tfull + 1;
+  uint64_t* pready = tempty + 1;
+  uint32_t* tmem_slot = (uint32_t*)(pready + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kq = (int)ptx::cluster_rank();
+  const int ug = (bid / mc::BWD_KS) * mc::BWD_NU;  // cluster's first unit
+  const int kb_base = kq * KBL;
+  const int rounds = p.steps + (p.dh0 ? 1 : 0);
+  auto time_of = [&](int pos) { return p.reverse ? p.steps - 1 - pos : pos; };
+  if (threadIdx.x == 0) {
+    ptx::prefetch_tmap(tmA);
+    ptx::prefetch_tmap(tmW);
+    for (int i = 0; i < p.stages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    ptx::mbar_init(wfull, 1);
+    ptx::mbar_init(tfull, 1);
+    ptx::mbar_init(tempty, 8);
+    ptx::mbar_init(pready, (mc::BWD_KS - 1) * 8);  // every warp of the three partners
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, 64);
+  ptx::tc_fence_before();
+  ptx::cluster_sync_all();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_expect_tx(wfull, KBL * mc::BWD_NU * 128);
+      for (int kb = 0; kb < KBL; ++kb)
+        ptx::tma_load_2d(tmW, wfull, sW + kb * (mc::BWD_NU * 128), (kb_base + kb) * 64, p.din + ug);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 1; i < rounds; ++i) {
+        const unsigned target = (unsigned)(G * i);
+        while (ptx::ld_relaxed(p.flag) < target) {}
+        ptx::fence_acquire_gpu();
+        ptx::fence_proxy_async_global();
+        ptx::fence_proxy_async_shared();
+        if (p.trace && bid == 0) p.trace[i * 8 + 0] = gtimer();
+        const int arow = time_of(p.steps - i) * p.B;
+        for (int kb = 0; kb < KBL; kb += mc::BWD_KBOX) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::tma_load_3d(tmA, &full[stage], sA + stage * mc::STAGE_BYTES, 0, arow, kb_base + kb);
+          ptx::mbar_expect_tx(&full[stage], mc::STAGE_BYTES);
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_bf16(128, mc::BWD_NU, 0, 0);
+      ptx::mbar_wait(wfull, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t wbase = ptx::smem_u32(sW);
+      for (int i = 1; i < rounds; ++i) {
+        ptx::mbar_wait(tempty, ((i - 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        for (int kb0 = 0; kb0 < KBL; kb0 += mc::BWD_KBOX) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a0 = ptx::smem_u32(sA + stage * mc::STAGE_BYTES);
+#pragma unroll
+          for (int j = 0; j < mc::BWD_KBOX; ++j) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              uint64_t ad = ptx::smem_desc_sw128(a0 + j * mc::BWD_KBLK + kk * 32, 16, 1024);
+              uint64_t bd = ptx::smem_desc_sw128(wbase + (kb0 + j) * (mc::BWD_NU * 128) + kk * 32, 16, 1024);
+              ptx::umma_bf16(tmem, ad, bd, idesc, (kb0 | j | kk) ? 1u : 0u);
+            }
+          }
+          ptx::umma_commit(&empty[stage]);
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+        ptx::umma_commit(tfull);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int uh = (warp - 4) >> 2;  // unit half of this CTA's 16 units
+    const int b = q * 32 + lane;
+    const bool valid = b < p.B;
+    const long long H = p.H;
+    const int u0 = ug + kq * 16 + uh * 8;  // my 8 units
+    const uint32_t xbase = ptx::smem_u32(sA);
+    uint32_t rbase[mc::BWD_KS], rpready[mc::BWD_KS];
+#pragma unroll
+    for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
+      rbase[pr_] = ptx::mapa(xbase, pr_);
+      rpready[pr_] = ptx::mapa(ptx::smem_u32(pready), pr_);
+    }
+    float dhc[mc::BWD_UPT], dc[mc::BWD_UPT];
+#pragma unroll
+    for (int u = 0; u < mc::BWD_UPT; ++u) {
+      dhc[u] = (valid && p.dh_final) ? p.dh_final[(long long)b * H + u0 + u] : 0.f;
+      dc[u] = (valid && p.dc_final) ? p.dc_final[(long long)b * H + u0 + u] : 0.f;
+    }
+    for (int i = 0; i < rounds; ++i) {
+      const bool cell = i < p.steps;
+      const int t = cell ? time_of(p.steps - 1 - i) : 0;
+      const long long row = (long long)t * p.B + b;
+      float4 dy4[2], tc4[2], cp4[2], a4[mc::BWD_UPT];
+      float mk = 1.f;
+      if (valid && cell) {
+        const float4* dyr = (const float4*)(p.dy + row * H + u0);
+        const float4* tcr = (const float4*)(p.tcache + row * H + u0);
+        const float4* cpr = (const float4*)(p.cprev + row * H + u0);
+        const float4* ar = (const float4*)(p.acts + row * 4 * H + 4 * u0);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          dy4[k] = __ldg(dyr + k);
+          tc4[k] = __ldg(tcr + k);
+          cp4[k] = __ldg(cpr + k);
+        }
+#pragma unroll
+        for (int u = 0; u < mc::BWD_UPT; ++u) a4[u] = __ldg(ar + u);
+        if (p.mask) mk = __ldg(p.mask + row);
+      }
+      float acc[mc::BWD_UPT];
+      if (i > 0) {
+        ptx::mbar_wait(tfull, (i - 1) & 1);
+        ptx::tc_fence_after();
+        if (p.trace && bid == 0 && threadIdx.x == 128) p.trace[i * 8 + 1] = gtimer();
+        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+        float v[mc::BWD_KS][mc::BWD_UPT];
+#pragma unroll
+        for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) ptx::tmem_ld8(tl + pr_ * 16 + uh * 8, v[pr_]);
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(tempty);
+        // park the partner slices in my (idle) stage ring, then tell the partners
+#pragma unroll
+        for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
+          if (pr_ == kq) continue;
+          const int c0 = (pr_ * 16 + uh * 8) >> 2;
+          *(float4*)(sA + mc::xoff(b, c0)) = make_float4(v[pr_][0], v[pr_][1], v[pr_][2], v[pr_][3]);
+          *(float4*)(sA + mc::xoff(b, c0 + 1)) = make_float4(v[pr_][4], v[pr_][5], v[pr_][6], v[pr_][7]);
+        }
+#pragma unroll
+        for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_)
+          if (pr_ == kq) {
+#pragma unroll
+            for (int u = 0; u < mc::BWD_UPT; ++u) acc[u] = v[pr_][u];
+          }
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_)
+            if (pr_ != kq) ptx::mbar_arrive_remote(rpready[pr_]);
+        }
+        ptx::mbar_wait_cluster(pready, (i - 1) & 1);
+        // pull my 8 units' partials from the three partners
+        const int cm = (kq * 16 + uh * 8) >> 2;
+#pragma unroll
+        for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
+          if (pr_ == kq) continue;
+          const float4 z0 = ptx::ld_cluster_v4(rbase[pr_] + mc::xoff(b, cm));
+          const float4 z1 = ptx::ld_cluster_v4(rbase[pr_] + mc::xoff(b, cm + 1));
+          acc[0] += z0.x; acc[1] += z0.y; acc[2] += z0.z; acc[3] += z0.w;
+          acc[4] += z1.x; acc[5] += z1.y; acc[6] += z1.z; acc[7] += z1.w;
+        }
+        if (p.trace && bid == 0 && threadIdx.x == 128) p.trace[i * 8 + 2] = gtimer();
+      } else {
+#pragma unroll
+        for (int u = 0; u < mc::BWD_UPT; ++u) acc[u] = 0.f;
+      }
+      if (valid) {
+        if (cell) {
+          __align__(16) bf16 du[4 * mc::BWD_UPT];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const float dyv[4] = {dy4[k].x, dy4[k].y, dy4[k].z, dy4[k].w};
+            const float tcv[4] = {tc4[k].x, tc4[k].y, tc4[k].z, tc4[k].w};
+            const float cpv[4] = {cp4[k].x, cp4[k].y, cp4[k].z, cp4[k].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int u = 4 * k + e;
+              const float dh = acc[u] + dhc[u] + dyv[e];
+              float dhn = dh, dcn = dc[u], dhcar = 0.f, dccar = 0.f;
+              if (p.mask) {
+                dhn = mk * dh; dcn = mk * dc[u];
+                dhcar = (1.f - mk) * dh; dccar = (1.f - mk) * dc[u];
+              }
+              const float4 a = a4[u];  // i f g o
+              const float tc = tcv[e];
+              const float dct = dhn * a.w * (1.f - tc * tc) + dcn;
+              du[4 * u + 0] = __float2bfloat16_rn(dct * a.z * (a.x * (1.f - a.x)));
+              du[4 * u + 1] = __float2bfloat16_rn(dct * cpv[e] * (a.y * (1.f - a.y)));
+              du[4 * u + 2] = __float2bfloat16_rn(dct * a.x * (1.f - a.z * a.z));
+              du[4 * u + 3] = __float2bfloat16_rn(dhn * tc * (a.w * (1.f - a.w)));
+              dc[u] = dct * a.y + dccar;
+              dhc[u] = dhcar;
+            }
+          }
+          uint4* dur = (uint4*)(p.dU + row * 4 * H + 4 * u0);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) dur[k] = ((uint4*)du)[k];
+        } else {
+#pragma unroll
+          for (int u = 0; u < mc::BWD_UPT; ++u) {
+            p.dh0[(long long)b * H + u0 + u] = acc[u] + dhc[u];
+            p.dc0[(long long)b * H + u0 + u] = dc[u];
+          }
+        }
+      }
+      if (p.trace && bid == 0 && threadIdx.x == 128) p.trace[i * 8 + 3] = gtimer();
+      ptx::named_bar_sync(1, 256);
+      if (threadIdx.x == 128) {
+        ptx::red_release_add(p.flag, 1u);
+        if (p.trace && bid == 0) p.trace[i * 8 + 4] = gtimer();
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::cluster_sync_all();  // no CTA leaves while a partner may still read its parked partials
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 64);
+  }
+}
+
 }  // namespace cmt

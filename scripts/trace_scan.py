@@ -1,0 +1,39 @@
+"""Per-step phase timestamps (globaltimer) of CTA 0 of one recurrent scan in a
+c3 step.  python scripts/trace_scan.py LAYER   (LAYER >= 100: backward scan of layer LAYER-100)"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_1802_07170_b200.engine import Engine  # noqa: E402
+from paper_1802_07170_b200.model import Model, ModelConfig, Rng  # noqa: E402
+
+layer = int(sys.argv[1]) if len(sys.argv) > 1 else 102
+V, E, H, L, B, S, T = bench.CONFIGS["c3"]
+cfg = ModelConfig(V, E, H, L, 0.2)
+eng = Engine(cfg, mode="bf16")
+eng.upload(Model.new(cfg, Rng(1)).params)
+for a in sys.argv[2:]:
+    k, v = a.split("=")
+    eng.set_option(k, int(v))
+src, sm, tgt, tm = bench.synthetic_batch(V, S, T, B, seed=0)
+eng.stage(src, sm, tgt, tm)
+rng = Rng(5)
+eng.run(1.0, 5.0, 0.1, rng)
+eng.set_option("trace_layer", layer)
+eng.run(1.0, 5.0, 0.1, rng)
+X = np.array([eng.stat(f"trace:{i}")[0] for i in range(51 * 8)]).reshape(51, 8).astype(np.float64)
+names = ["t0", "t1", "t2", "t3", "t4", "t5", "t6", "t7"]
+rows = slice(3, 40)
+per = np.diff(X[:, 0])[rows]
+print(f"layer {layer}: step period us median {np.median(per) / 1e3:.2f}")
+for a, b in [(0, 1), (1, 2), (2, 3), (3, 4)]:
+    d = (X[:, b] - X[:, a])[rows] / 1e3
+    if np.all(X[rows, a] > 0) and np.all(X[rows, b] > 0):
+        print(f"  {names[a]}->{names[b]} us median {np.median(d):.2f}")
+d = (X[1:, 0] - X[:-1, 4])[rows] / 1e3
+print(f"  t4->next t0 us median {np.median(d):.2f}")
+d = (X[1:, 0] - X[:-1, 3])[rows] / 1e3
+print(f"  t3->next t0 us median {np.median(d):.2f}")
