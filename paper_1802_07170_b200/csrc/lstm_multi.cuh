@@ -244,9 +244,10 @@ __global__ void __launch_bounds__(mc::THREADS, 1)
 // units; CTA rank kq contracts the gate columns [kq*H, (kq+1)*H) of dU_{t+1}
 // for all 64 units (M = B <= 128 rows, N = 64, K = H) with its W_h slice
 // resident in smem, then the four partial sums are combined through
-// distributed shared memory: every CTA parks its partials in its own (idle)
-// TMA stage ring and each CTA pulls the 16-unit slice it owns from the other
-// three (ld.shared::cluster).  8 epilogue warps run the cell backward for
+// distributed shared memory: once a CTA's MMA is done its (idle) TMA stage
+// ring can receive, and each CTA pushes every partner the slice of partials
+// for the partner's 16 units with st.async (bytes complete the partner's
+// mbarrier, so no cluster fence is paid per step).  8 epilogue warps run the cell backward for
 // 16 units x 128 rows.  Two independent scans can share one cooperative
 // launch (the backward layer graph pairs dec.lk with enc.l(k+1), and
 // enc.l1 bwd with enc.l1 fwd).  Reference: layers.py:366-395, 472-493.
@@ -297,8 +298,9 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
   uint64_t* wfull = empty + mc::MAX_STAGES;
   uint64_t* tfull = wfull + 1;
   uint64_t* tempty = tfull + 1;
-  uint64_t* pready = tempty + 1;
-  uint32_t* tmem_slot = (uint32_t*)(pready + 1);
+  uint64_t* rfree = tempty + 1;  // the three partners' MMAs are done: their rings may receive partials
+  uint64_t* xfull = rfree + 1;   // all partials for my units have landed in my ring
+  uint32_t* tmem_slot = (uint32_t*)(xfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kq = (int)ptx::cluster_rank();
@@ -316,7 +318,8 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
     ptx::mbar_init(wfull, 1);
     ptx::mbar_init(tfull, 1);
     ptx::mbar_init(tempty, 8);
-    ptx::mbar_init(pready, (mc::BWD_KS - 1) * 8);  // every warp of the three partners
+    ptx::mbar_init(rfree, mc::BWD_KS - 1);
+    ptx::mbar_init(xfull, 1);  // my expect_tx; the partners' st.async bytes complete it
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 64);
@@ -384,12 +387,14 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
     const bool valid = b < p.B;
     const long long H = p.H;
     const int u0 = ug + kq * 16 + uh * 8;  // my 8 units
-    const uint32_t xbase = ptx::smem_u32(sA);
-    uint32_t rbase[mc::BWD_KS], rpready[mc::BWD_KS];
+    // partials parked in the receiver's stage ring: xbuf[sender][uh][row][8] floats
+    const uint32_t xslot = ptx::smem_u32(sA) + (uint32_t)((kq * 2 + uh) * 128 + b) * 32;  // my slot in a receiver
+    uint32_t rx[mc::BWD_KS], rxf[mc::BWD_KS], rrf[mc::BWD_KS];
 #pragma unroll
     for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
-      rbase[pr_] = ptx::mapa(xbase, pr_);
-      rpready[pr_] = ptx::mapa(ptx::smem_u32(pready), pr_);
+      rx[pr_] = ptx::mapa(xslot, pr_);
+      rxf[pr_] = ptx::mapa(ptx::smem_u32(xfull), pr_);
+      rrf[pr_] = ptx::mapa(ptx::smem_u32(rfree), pr_);
     }
     float dhc[mc::BWD_UPT], dc[mc::BWD_UPT];
 #pragma unroll
@@ -423,6 +428,7 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
         ptx::mbar_wait(tfull, (i - 1) & 1);
         ptx::tc_fence_after();
         if (p.trace && bid == 0 && threadIdx.x == 128) p.trace[i * 8 + 1] = gtimer();
+        if (p.trace && bid < 8 && threadIdx.x == 128) p.trace[1024 + i * 8 + bid] = gtimer();
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
         float v[mc::BWD_KS][mc::BWD_UPT];
 #pragma unroll
@@ -431,13 +437,12 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(tempty);
-        // park the partner slices in my (idle) stage ring, then tell the partners
+        // my MMA is done: my ring may now receive the partners' partials
+        if (threadIdx.x == 128) {
+          ptx::mbar_expect_tx(xfull, (mc::BWD_KS - 1) * 2 * 128 * 32);
 #pragma unroll
-        for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
-          if (pr_ == kq) continue;
-          const int c0 = (pr_ * 16 + uh * 8) >> 2;
-          *(float4*)(sA + mc::xoff(b, c0)) = make_float4(v[pr_][0], v[pr_][1], v[pr_][2], v[pr_][3]);
-          *(float4*)(sA + mc::xoff(b, c0 + 1)) = make_float4(v[pr_][4], v[pr_][5], v[pr_][6], v[pr_][7]);
+          for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_)
+            if (pr_ != kq) ptx::mbar_arrive_remote_relaxed(rrf[pr_]);
         }
 #pragma unroll
         for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_)
@@ -445,20 +450,20 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
 #pragma unroll
             for (int u = 0; u < mc::BWD_UPT; ++u) acc[u] = v[pr_][u];
           }
-        __syncwarp();
-        if (lane == 0) {
-#pragma unroll
-          for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_)
-            if (pr_ != kq) ptx::mbar_arrive_remote(rpready[pr_]);
-        }
-        ptx::mbar_wait_cluster(pready, (i - 1) & 1);
-        // pull my 8 units' partials from the three partners
-        const int cm = (kq * 16 + uh * 8) >> 2;
+        // push each partner its 8 columns (async remote stores completing its xfull)
+        ptx::mbar_wait_cluster(rfree, (i - 1) & 1);
 #pragma unroll
         for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
           if (pr_ == kq) continue;
-          const float4 z0 = ptx::ld_cluster_v4(rbase[pr_] + mc::xoff(b, cm));
-          const float4 z1 = ptx::ld_cluster_v4(rbase[pr_] + mc::xoff(b, cm + 1));
+          ptx::st_async_v4(rx[pr_], v[pr_][0], v[pr_][1], v[pr_][2], v[pr_][3], rxf[pr_]);
+          ptx::st_async_v4(rx[pr_] + 16, v[pr_][4], v[pr_][5], v[pr_][6], v[pr_][7], rxf[pr_]);
+        }
+        ptx::mbar_wait_cluster(xfull, (i - 1) & 1);
+#pragma unroll
+        for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
+          if (pr_ == kq) continue;
+          const float4* xr = (const float4*)(sA + ((pr_ * 2 + uh) * 128 + b) * 32);
+          const float4 z0 = xr[0], z1 = xr[1];
           acc[0] += z0.x; acc[1] += z0.y; acc[2] += z0.z; acc[3] += z0.w;
           acc[4] += z1.x; acc[5] += z1.y; acc[6] += z1.z; acc[7] += z1.w;
         }
@@ -516,7 +521,7 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  ptx::cluster_sync_all();  // no CTA leaves while a partner may still read its parked partials
+  ptx::cluster_sync_all();  // no CTA leaves while a partner may still write into its ring
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 64);

@@ -37,3 +37,10 @@ d = (X[1:, 0] - X[:-1, 4])[rows] / 1e3
 print(f"  t4->next t0 us median {np.median(d):.2f}")
 d = (X[1:, 0] - X[:-1, 3])[rows] / 1e3
 print(f"  t3->next t0 us median {np.median(d):.2f}")
+
+if layer >= 100:
+    Y = np.array([eng.stat(f"trace:{1024 + i}")[0] for i in range(51 * 8)]).reshape(51, 8).astype(np.float64)
+    if Y[5, 0] > 0:
+        rel = (Y - Y[:, :1])[rows] / 1e3
+        print("  tfull of CTAs 0..7 relative to CTA 0 (us), median:", np.round(np.median(rel, axis=0), 2))
+        print("  max spread within cluster 0 (us), median:", np.median(rel[:, :4].max(1) - rel[:, :4].min(1)))
