@@ -308,6 +308,7 @@ class Engine {
   int *src_ids_d, *tgt_in_d, *tgt_out_d;
   float *src_mask_d, *tgt_mask_d;
   void *Xs, *Xt, *top, *u_att, *cst_att, *hod, *Y, *dhpre, *du_att, *dU, *dU2;
+  float* cepart = nullptr;  // per-CTA dY column sums of the fused CE kernel
   float *ux, *ux2, *alpha, *ho, *losstok, *dcst, *dXemb, *dtop, *dhc, *dcc, *colpart;
   std::vector<void*> drop_enc, drop_dec;
   std::vector<uint8_t*> keep_enc, keep_dec;
@@ -327,6 +328,9 @@ class Engine {
   int clustered_fwd = 0;  // option: cluster K-split forward (slower than the plain persistent one at c3)
   int cg2 = 1;         // option: CTA-pair (cta_group::2) tiles for the large GEMMs
   int dual = 1;        // option: run independent scans of the layer graph two at a time
+  int use_jump = 1;    // option: table-driven PCG64 jump-ahead dropout kernel
+  int ce2 = 1;         // option: fused CE + bias-grad column sums (persistent, 16-byte vectors)
+  bool use_ce2() const { return bf && ce2 && V % 8 == 0 && V <= CE2_MAXV; }
   // data parallel (NCCL): dense all-reduce of grads, loss and status
   void* comm = nullptr;
   int rank = 0, world = 1;
@@ -391,6 +395,7 @@ class Engine {
       if (i == 0 || !cfg.shared_embeddings) { cudaFree(emb_w[i]); cudaFree(emb_sh[i]); }
     }
     cudaFree(ws);
+    if (jump_d) cudaFree(jump_d);
     for (int t = 0; t < 2; ++t) if (demb[t]) cudaFree(demb[t]);
     if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
     for (auto& e : ev) cudaEventDestroy(e);
@@ -608,6 +613,7 @@ class Engine {
     }
     long long colmax = std::max<long long>(V, 4LL * H);
     colpart = carve<float>(cur, 64 * colmax * 4);
+    cepart = use_ce2() ? carve<float>(cur, (long long)g_num_sms * V * 4) : nullptr;
     for (int t = 0; t < 2; ++t) {
       seg_off_d[t] = carve<int>(cur, (NS + NT + 1) * 4);
       seg_pos_d[t] = carve<int>(cur, (NS + NT) * 4);
@@ -782,8 +788,29 @@ class Engine {
     if (bf) launch_gather<bf16>(table_v(t), ids, N, out);
     else launch_gather<float>(table_v(t), ids, N, out);
   }
+  PcgJump* jump_d = nullptr;  // PCG64 jump-ahead table for jump_inc
+  unsigned long long jump_inc[2] = {0, 0};
+  bool jump_ok = false;
+  void ensure_jump(const Pcg& pcg) {
+    if (jump_ok && jump_inc[0] == pcg.inc_hi && jump_inc[1] == pcg.inc_lo) return;
+    if (!jump_d) CMT_CUDA(cudaMalloc(&jump_d, sizeof(PcgJump)));
+    pcg_jump_table_kernel<<<1, 1, 0, st>>>(jump_d, pcg.inc_hi, pcg.inc_lo);
+    CMT_LAUNCHED(); tl_mark(st, "pcg_jump_table_kernel");
+    jump_inc[0] = pcg.inc_hi; jump_inc[1] = pcg.inc_lo;
+    jump_ok = true;
+  }
   template <typename TI, typename TO>
   void launch_dropout(const void* x, void* y, uint8_t* keep, int N, unsigned long long base, const Pcg& pcg) {
+    if (use_jump) {
+      ensure_jump(pcg);
+      dim3 blk(32, 8);
+      dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, DROP_DPT), 8));
+      float scale = 1.0f / (float)(1.0 - cfg.dropout);
+      dropout_fwd_kernel3<TI, TO><<<grid, blk, 0, st>>>((const TI*)x, (TO*)y, keep, N, H, pcg, jump_d, base,
+                                                        dropout_threshold(cfg.dropout), scale);
+      CMT_LAUNCHED(); tl_mark(st, "dropout_fwd_kernel3");
+      return;
+    }
     dim3 blk(32, 8);
     dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, 32), 8));
     float scale = 1.0f / (float)(1.0 - cfg.dropout);
@@ -1296,7 +1323,17 @@ class Engine {
     }
     if (stop_after == 1) { CMT_CUDA(cudaStreamSynchronize(st)); return; }
     // fused log-softmax + smoothed CE + grad (training.py:96-120, tensor.py:146-151)
-    if (bf) ce_kernel<bf16><<<(int)NT, CE_THREADS, 0, st>>>((bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon, inv_ntok,
+    const bool fused_ce = use_ce2() && cepart;
+    if (fused_ce) {
+      const size_t smem = (size_t)V * 4;
+      CMT_CUDA(cudaFuncSetAttribute(ce_colsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ce_colsum_kernel<<<g_num_sms, CE2_THREADS, smem, st>>>((bf16*)Y, V, (int)NT, tgt_out_d, tgt_mask_d,
+                                                              (float)a.epsilon, inv_ntok, cfg.output_tanh, losstok,
+                                                              status_d, cepart);
+      CMT_LAUNCHED(); tl_mark(st, "ce_colsum_kernel");
+      colsum_final_kernel<<<ceil_div(V, 256), 256, 0, st>>>(cepart, g_num_sms, V, dg + off_bo);
+      CMT_LAUNCHED(); tl_mark(st, "colsum_final_kernel");
+    } else if (bf) ce_kernel<bf16><<<(int)NT, CE_THREADS, 0, st>>>((bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon, inv_ntok,
                                                            cfg.output_tanh, losstok, status_d);
     else ce_kernel<float><<<(int)NT, CE_THREADS, 0, st>>>((float*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon, inv_ntok,
                                                          cfg.output_tanh, losstok, status_d);
@@ -1308,7 +1345,7 @@ class Engine {
     // ===== backward =====
     // output projection (layers.py:64-73): dW_o, db_o, dH_o (+ dropout bwd + tanh' of H_o)
     gemm(H, V, (int)NT, Mat{hin, H, 1}, Mat{Y, V, 1}, store(dg + off_wo, V, false));
-    colsum(Y, true, NT, V, dg + off_bo);
+    if (!fused_ce) colsum(Y, true, NT, V, dg + off_bo);
     {
       EpiStore e = store(dhpre, H, true);
       if (drop) { e.dmask = keep_o; e.ld_dmask = H; e.dscale = 1.0f / (float)(1.0 - cfg.dropout); }
@@ -1685,7 +1722,16 @@ int cmt_test_dropout(unsigned long long sh, unsigned long long sl, unsigned long
   return guard(nullptr, [&] {
     cmt::Pcg pcg{sh, sl, ih, il};
     dim3 blk(32, 8), grid(cmt::ceil_div(H, 32), cmt::ceil_div(cmt::ceil_div(N, 32), 8));
-    cmt::dropout_fwd_kernel2<float, float><<<grid, blk>>>(x, y, keep, N, H, pcg, base, p, 1.0f / (float)(1.0 - p));
+    (void)grid;
+    cmt::PcgJump* jt = nullptr;
+    CMT_CUDA(cudaMalloc(&jt, sizeof(cmt::PcgJump)));
+    cmt::pcg_jump_table_kernel<<<1, 1>>>(jt, ih, il);
+    dim3 grid3(cmt::ceil_div(H, 32), cmt::ceil_div(cmt::ceil_div(N, cmt::DROP_DPT), 8));
+    cmt::dropout_fwd_kernel3<float, float><<<grid3, blk>>>(x, y, keep, N, H, pcg, jt, base, cmt::dropout_threshold(p),
+                                                            1.0f / (float)(1.0 - p));
+    cudaError_t err = cudaDeviceSynchronize();
+    cudaFree(jt);
+    CMT_CUDA(err);
     CMT_CUDA(cudaGetLastError());
     CMT_CUDA(cudaDeviceSynchronize());
   });
@@ -1698,6 +1744,11 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "cluster") e->eng->clustered = (int)value;
     else if (k == "cg2") e->eng->cg2 = (int)value;
     else if (k == "dual") e->eng->dual = (int)value;
+    else if (k == "jump") e->eng->use_jump = (int)value;
+    else if (k == "ce2") {
+      if (e->eng->staged && (value != 0) != (e->eng->ce2 != 0)) throw Error(cmt::CMT_ERR_CONFIG, "set ce2 before staging");
+      e->eng->ce2 = (int)value;
+    }
     else if (k == "cluster_fwd") e->eng->clustered_fwd = (int)value;
     else if (k == "tma_store") cmt::g_tma_store = (int)value;
     else if (k == "gemm_opt") cmt::g_gemm_opt = (int)value;

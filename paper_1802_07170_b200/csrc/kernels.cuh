@@ -3,6 +3,7 @@
 // attention forward/backward, fused log-softmax + label-smoothed CE + grad,
 // column sums (bias grads), global-norm reduction and the clipped SGD update.
 #pragma once
+#include <cmath>
 #include "common.cuh"
 
 namespace cmt {
@@ -123,6 +124,59 @@ CMT_D unsigned long long pcg_out(u128 s) {
   unsigned rot = (unsigned)(s >> 122);
   unsigned long long x = hi ^ lo;
   return (x >> rot) | (x << ((64 - rot) & 63));
+}
+
+// Jump-ahead table of the PCG64 LCG for one stream increment: advancing by
+// 2^i steps is s -> m[i] s + p[i].  Built once per increment (one thread), it
+// turns each thread's jump to its first draw into one 128-bit multiply-add per
+// set bit of the offset instead of a square-and-multiply loop.
+struct PcgJump {
+  u128 m[64], p[64];
+};
+__global__ void pcg_jump_table_kernel(PcgJump* t, unsigned long long inc_hi, unsigned long long inc_lo) {
+  u128 m = pcg_mult(), pl = ((u128)inc_hi << 64) | inc_lo;
+  for (int i = 0; i < 64; ++i) {
+    t->m[i] = m;
+    t->p[i] = pl;
+    pl = (m + 1) * pl;
+    m = m * m;
+  }
+}
+CMT_D u128 pcg_jump(const PcgJump* __restrict__ t, u128 s, unsigned long long delta) {
+  while (delta) {
+    const int i = __ffsll((long long)delta) - 1;
+    s = t->m[i] * s + t->p[i];
+    delta &= delta - 1;
+  }
+  return s;
+}
+
+// Same contract as dropout_fwd_kernel2 with the table jump and 64 draws per
+// thread (the jump is amortised over twice as many draws).
+constexpr int DROP_DPT = 64;
+// keep  <=>  (r >> 11) * 2^-53 >= p  <=>  (r >> 11) >= ceil(p * 2^53): the
+// reference's double comparison done exactly in integers (p * 2^53 is exact).
+inline unsigned long long dropout_threshold(double p) { return (unsigned long long)std::ceil(p * 9007199254740992.0); }
+template <typename TI, typename TO>
+__global__ void dropout_fwd_kernel3(const TI* __restrict__ x, TO* __restrict__ y, uint8_t* __restrict__ keep, int N,
+                                    int H, Pcg pcg, const PcgJump* __restrict__ jt, unsigned long long base,
+                                    unsigned long long thr, float scale) {
+  const int h = blockIdx.x * 32 + threadIdx.x;
+  const int n0 = (blockIdx.y * blockDim.y + threadIdx.y) * DROP_DPT;
+  if (h >= H || n0 >= N) return;
+  const u128 inc = ((u128)pcg.inc_hi << 64) | pcg.inc_lo;
+  u128 s = pcg_jump(jt, ((u128)pcg.state_hi << 64) | pcg.state_lo, base + (unsigned long long)h * N + n0);
+  const u128 mult = pcg_mult();
+  const int nend = min(N, n0 + DROP_DPT);
+#pragma unroll 4
+  for (int n = n0; n < nend; ++n) {
+    s = s * mult + inc;
+    const bool k = (pcg_out(s) >> 11) >= thr;
+    const long long i = (long long)n * H + h;
+    keep[i] = k;
+    const float xv = to_f<TI>(x[i]);
+    y[i] = from_f<TO>(k ? xv * scale : xv * 0.f);
+  }
 }
 
 // y = x * keep/(1-p) for one dropout site of shape (H, N) in the reference's
@@ -421,6 +475,136 @@ __global__ void sum_to_double_kernel(const float* __restrict__ x, int n, double*
 // Column sums (bias grads: layers.py:72-73, 391): partial over row chunks,
 // then a fixed-order combine -> deterministic.
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Fused log-softmax + smoothed CE + gradient + bias-gradient column sums over
+// bf16 logits (production path; rows 16-byte aligned, V <= CE2_MAXV).  A
+// persistent CTA walks rows blockIdx.x, +gridDim.x, ...; each row is read with
+// 16-byte loads (pass 1: max / sum-exp / sum), then rewritten in place with
+// the gradient (pass 2) while the CTA accumulates d over its rows into a
+// shared-memory column sum (each thread owns fixed columns, so no atomics).
+// The per-CTA partial sums of d are reduced by colsum_final_kernel into
+// db_o = sum_n dY[n][v] (layers.py:72-73).  With the output tanh on, the
+// logits are in [-1, 1] and the sum of exponentials needs no max shift.
+// Same math as ce_kernel (training.py:96-120, tensor.py:146-151).
+// ---------------------------------------------------------------------------
+constexpr int CE2_THREADS = 512;
+constexpr int CE2_MAXV = 55 * 1024;  // smem column sums (fp32)
+constexpr int CE2_UNROLL = 4;        // 16-byte loads in flight per thread
+__global__ void __launch_bounds__(CE2_THREADS, 1)
+    ce_colsum_kernel(bf16* __restrict__ Y, int V, int rows, const int* __restrict__ tgt,
+                     const float* __restrict__ tmask, float eps, float inv_ntok, int tanh_on,
+                     float* __restrict__ losstok, int* __restrict__ status, float* __restrict__ part) {
+  extern __shared__ float csum[];  // [V]
+  __shared__ float red_m[CE2_THREADS / 32], red_s[CE2_THREADS / 32], red_y[CE2_THREADS / 32];
+  __shared__ float bc[2];
+  const int nv = V >> 3;  // 16-byte vectors per row
+  for (int v = threadIdx.x; v < V; v += CE2_THREADS) csum[v] = 0.f;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float eV = eps / (float)V;
+  for (int n = blockIdx.x; n < rows; n += gridDim.x) {
+    uint4* row = (uint4*)(Y + (long long)n * V);
+    float mx = tanh_on ? 0.f : -INFINITY, se = 0.f, sy = 0.f;
+    bool bad = false;
+    for (int i0 = threadIdx.x; i0 < nv; i0 += CE2_UNROLL * CE2_THREADS) {
+      uint4 qv[CE2_UNROLL];
+#pragma unroll
+      for (int u = 0; u < CE2_UNROLL; ++u) {  // all loads in flight before any use
+        const int i = i0 + u * CE2_THREADS;
+        qv[u] = i < nv ? row[i] : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < CE2_UNROLL; ++u) {
+      if (i0 + u * CE2_THREADS >= nv) break;
+      const bf16* e = (const bf16*)&qv[u];
+      float y[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        y[j] = __bfloat162float(e[j]);
+        bad |= !isfinite(y[j]);
+        sy += y[j];
+      }
+      if (tanh_on) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) se += __expf(y[j]);
+      } else {
+        float lm = y[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) lm = fmaxf(lm, y[j]);
+        if (lm > mx) {
+          se = (mx == -INFINITY) ? 0.f : se * __expf(mx - lm);
+          mx = lm;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) se += __expf(y[j] - mx);
+      }
+      }
+    }
+    float wm = warp_max(mx);
+    se = (mx == -INFINITY) ? 0.f : se * __expf(mx - wm);
+    se = warp_sum(se);
+    sy = warp_sum(sy);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_LOGITS);
+    if (lane == 0) { red_m[warp] = wm; red_s[warp] = se; red_y[warp] = sy; }
+    __syncthreads();
+    if (warp == 0) {
+      float m2 = lane < CE2_THREADS / 32 ? red_m[lane] : -INFINITY;
+      float s2 = lane < CE2_THREADS / 32 ? red_s[lane] : 0.f;
+      float y2 = lane < CE2_THREADS / 32 ? red_y[lane] : 0.f;
+      float gm = warp_max(m2);
+      s2 = (m2 == -INFINITY) ? 0.f : s2 * __expf(m2 - gm);
+      s2 = warp_sum(s2);
+      y2 = warp_sum(y2);
+      if (lane == 0) {
+        const float lse = gm + logf(s2);
+        const int g = tgt[n];
+        const float gold = __bfloat162float(Y[(long long)n * V + g]);
+        const float per = lse - (1.f - eps) * gold - eV * y2;
+        const float m = tmask[n];
+        losstok[n] = per * m;
+        if (!isfinite(per)) atomicOr(status, ST_LOSS);
+        bc[0] = lse;
+        bc[1] = m * inv_ntok;
+      }
+    }
+    __syncthreads();
+    const float lse = bc[0], w = bc[1];
+    const int g = tgt[n];
+    for (int i0 = threadIdx.x; i0 < nv; i0 += CE2_UNROLL * CE2_THREADS) {
+      uint4 qv[CE2_UNROLL];
+#pragma unroll
+      for (int u = 0; u < CE2_UNROLL; ++u) {
+        const int i = i0 + u * CE2_THREADS;
+        qv[u] = i < nv ? row[i] : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < CE2_UNROLL; ++u) {
+      const int i = i0 + u * CE2_THREADS;
+      if (i >= nv) break;
+      const bf16* e = (const bf16*)&qv[u];
+      __align__(16) bf16 o[8];
+      float* cs = csum + i * 8;
+      const float4 c0 = *(const float4*)cs, c1 = *(const float4*)(cs + 4);
+      float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float y = __bfloat162float(e[j]);
+        float d = __expf(y - lse) - eV - (i * 8 + j == g ? (1.f - eps) : 0.f);
+        d *= w;
+        if (tanh_on) d *= (1.f - y * y);
+        const bf16 db = __float2bfloat16_rn(d);
+        o[j] = db;
+        c[j] += __bfloat162float(db);  // the bias grad sums the stored (bf16) dY, as colsum did
+      }
+      row[i] = *(const uint4*)o;
+      *(float4*)cs = make_float4(c[0], c[1], c[2], c[3]);
+      *(float4*)(cs + 4) = make_float4(c[4], c[5], c[6], c[7]);
+      }
+    }
+    __syncthreads();  // bc / red reuse
+  }
+  for (int v = threadIdx.x; v < V; v += CE2_THREADS) part[(long long)blockIdx.x * V + v] = csum[v];
+}
+
 template <typename T>
 __global__ void colsum_partial_kernel(const T* __restrict__ D, long long ld, int rows, int cols, int rows_per,
                                       float* __restrict__ part) {
