@@ -154,7 +154,7 @@ static std::string gemm_label(int M, int N, int K, int BN, int CG) {
 
 static int g_gemm_opt = 0;  // option: bit 0 natural K order, bit 1 N-fastest tile order
 template <int BN, int AMN, int BMN, class Epi, int CG = 1, int ST = 0>
-static void launch_tc_impl(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const Epi& e) {
+static void launch_tc_impl(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const Epi& e, int ks = 1) {
   using C = tc::Cfg<BN, CG, ST>;
   static bool attr = false;
   auto kfn = gemm_tc_kernel<BN, AMN, BMN, Epi, CG, ST>;
@@ -171,7 +171,7 @@ static void launch_tc_impl(cudaStream_t st, int M, int N, int K, Mat A, Mat B, c
   else make_map(&tb, B.p, Kx, N, B.ld, tc::BK, C::BNC);
   if constexpr (ST) make_map_c(&tcm, e.C, N, M, e.ldc, e.c_bf16 != 0);
   else tcm = ta;
-  int tiles = ceil_div(M, C::TILE_M) * ceil_div(N, BN);
+  int tiles = ceil_div(M, C::TILE_M) * ceil_div(N, BN) * ks;
   int grid = CG * std::min(tiles, g_num_sms / CG);
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3(grid);
@@ -185,17 +185,42 @@ static void launch_tc_impl(cudaStream_t st, int M, int N, int K, Mat A, Mat B, c
   at[0].val.clusterDim.z = 1;
   c.attrs = at;
   c.numAttrs = CG > 1 ? 1 : 0;
-  CMT_CUDA(cudaLaunchKernelEx(&c, kfn, ta, tb, tcm, M, N, K, e, g_gemm_opt));
+  CMT_CUDA(cudaLaunchKernelEx(&c, kfn, ta, tb, tcm, M, N, K, e, g_gemm_opt, ks));
   CMT_LAUNCHED(); tl_mark(st, gemm_label(M, N, K, BN, CG));
 }
 
 static int g_tma_store = 1;  // option: TMA-store epilogue for EpiStore GEMMs
 
+static int g_splitk = 1;  // option: split-K (TMA reduce-add) for linear fp32 epilogues
+// K slices for a linear fp32 EpiStore GEMM whose tile count leaves CTA pairs
+// idle in the last wave: minimise waves(tiles * ks) / ks (+ a per-slice cost).
+static int pick_ks(int M, int N, int K, int BN, int CG) {
+  if (!g_splitk) return 1;
+  const long long tiles = (long long)ceil_div(M, 128 * CG) * ceil_div(N, BN);
+  const long long units = g_num_sms / CG;
+  const int nkb = ceil_div(K, 64);
+  int best = 1;
+  double best_t = (double)((tiles + units - 1) / units);
+  for (int ks = 2; ks <= 4; ++ks) {
+    if (nkb / ks < 16) break;
+    double t = (double)((tiles * ks + units - 1) / units) / ks + 0.04 * (ks - 1);
+    if (t < best_t * 0.95) { best = ks; best_t = t; }
+  }
+  return best;
+}
+
 template <int BN, int AMN, int BMN, class Epi, int CG = 1>
 static void launch_tc(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const Epi& e) {
   if constexpr (std::is_same<Epi, EpiStore>::value) {
-    if (g_tma_store && c_map_ok(e.C, e.ldc, e.c_bf16 != 0) && !(e.beta && e.c_bf16))
-      return launch_tc_impl<BN, AMN, BMN, Epi, CG, 1>(st, M, N, K, A, B, e);
+    if (g_tma_store && c_map_ok(e.C, e.ldc, e.c_bf16 != 0) && !(e.beta && e.c_bf16)) {
+      int ks = 1;
+      if (!e.c_bf16 && !e.bias && e.act == 0 && !e.add) ks = pick_ks(M, N, K, BN, CG);
+      if (ks > 1 && !e.beta) {  // slices reduce-add into a zeroed C
+        if (e.ldc == N) CMT_CUDA(cudaMemsetAsync(e.C, 0, (size_t)M * N * 4, st));
+        else CMT_CUDA(cudaMemset2DAsync(e.C, (size_t)e.ldc * 4, 0, (size_t)N * 4, M, st));
+      }
+      return launch_tc_impl<BN, AMN, BMN, Epi, CG, 1>(st, M, N, K, A, B, e, ks);
+    }
   }
   launch_tc_impl<BN, AMN, BMN, Epi, CG, 0>(st, M, N, K, A, B, e);
 }
@@ -205,8 +230,10 @@ static void launch_tc(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const 
 // whose per-SM operand stream is smallest.  Encoded as BN * 4 + CG.
 static int pick_tile(int M, int N) {
   if (N <= 64) return 64 * 4 + 1;
-  struct Cand { int bn, cg; double bonus; };
-  const Cand cands[] = {{256, 2, 0.10}, {128, 2, 0.06}, {256, 1, 0.03}, {128, 1, 0.0}};
+  // relative per-tile throughput measured with scripts/gemm_bench.py at the c3
+  // shapes (256-wide CTA-pair tiles stream the fewest operand bytes per FLOP)
+  struct Cand { int bn, cg; double rate; };
+  const Cand cands[] = {{256, 2, 1.0}, {128, 2, 0.65}, {256, 1, 0.8}, {128, 1, 0.6}};
   int best = 128 * 4 + 1;
   double best_s = -1;
   for (const Cand& c : cands) {
@@ -215,7 +242,7 @@ static int pick_tile(int M, int N) {
     long long t = (long long)ceil_div(M, 128 * c.cg) * ceil_div(N, c.bn);
     long long waves = (t + units - 1) / units;
     double eff = (double)t / (double)(waves * units);
-    double s = eff + c.bonus;
+    double s = eff * c.rate;
     if (s > best_s) { best_s = s; best = c.bn * 4 + c.cg; }
   }
   return best;
@@ -1752,6 +1779,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "cluster_fwd") e->eng->clustered_fwd = (int)value;
     else if (k == "tma_store") cmt::g_tma_store = (int)value;
     else if (k == "gemm_opt") cmt::g_gemm_opt = (int)value;
+    else if (k == "splitk") cmt::g_splitk = (int)value;
     else if (k == "timeline") {
       cmt::g_tl.on = value != 0;
       for (auto& m : cmt::g_tl.marks) cudaEventDestroy(m.second);

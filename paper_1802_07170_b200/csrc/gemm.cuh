@@ -305,7 +305,7 @@ struct Cfg {
 template <int BN, int A_MN, int B_MN, class Epi, int CG = 1, int ST = 0>
 __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, int M, int N, int K, Epi epi, int opt) {
+                   const __grid_constant__ CUtensorMap tmC, int M, int N, int K, Epi epi, int opt, int ks) {
   using C = tc::Cfg<BN, CG, ST>;
   constexpr int S = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -328,6 +328,10 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
   const int tiles_n = (N + BN - 1) / BN;
   const int num_tiles = tiles_m * tiles_n;
   const int num_kb = (K + tc::BK - 1) / tc::BK;
+  // split-K (ST only, linear epilogues): work unit w -> tile w / ks, K slice w % ks;
+  // every slice reduce-adds its partial tile into C
+  const int num_work = num_tiles * ks;
+  auto kb_lo = [&](int sp) { return sp * num_kb / ks; };
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -358,18 +362,20 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
       // ===== TMA producer (both CTAs of a pair load their own halves) =====
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = unit; tile < num_tiles; tile += nunits) {
+      for (int w = unit; w < num_work; w += nunits) {
+        const int tile = w / ks, sp = w % ks;
         const int tm_ = (opt & 2) ? tile / tiles_n : tile % tiles_m;
         const int tn_ = (opt & 2) ? tile % tiles_n : tile / tiles_m;
         const int m0 = tm_ * C::TILE_M + (int)rank * tc::BM;
         const int n0 = tn_ * BN + (int)rank * C::BNC;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kbl = kb_lo(sp), nk = kb_lo(sp + 1) - kbl;
+        for (int kk_ = 0; kk_ < nk; ++kk_) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * C::A_BYTES;
           uint8_t* b = sB + stage * C::B_BYTES;
           // stagger the K order per tile so concurrent CTAs sharing an operand
           // tile do not request the same L2 lines at the same moment
-          const int k0 = ((opt & 1) ? kb : (kb + tile) % num_kb) * tc::BK;
+          const int k0 = (kbl + ((opt & 1) ? kk_ : (kk_ + tile) % nk)) * tc::BK;
           if constexpr (CG == 2) {
             const uint32_t fb = ptx::mapa(ptx::smem_u32(&full[stage]), 0);
             if (rank == 0) ptx::mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -413,13 +419,14 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int iter = 0;
-      for (int tile = unit; tile < num_tiles; tile += nunits, ++iter) {
+      for (int w = unit; w < num_work; w += nunits, ++iter) {
+        const int nk = kb_lo(w % ks + 1) - kb_lo(w % ks);
         const int buf = iter & 1;
         const uint32_t aphase = (iter >> 1) & 1;
         ptx::mbar_wait(&tempty[buf], aphase ^ 1);
         ptx::tc_fence_after();
         const uint32_t dtm = tmem_base + buf * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = 0; kb < nk; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
           const uint32_t a_addr = ptx::smem_u32(sA + stage * C::A_BYTES);
@@ -435,10 +442,10 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
           }
           if constexpr (CG == 2) {
             ptx::umma_commit_cg2_mc(&empty[stage], 3);
-            if (kb == num_kb - 1) ptx::umma_commit_cg2_mc(&tfull[buf], 3);
+            if (kb == nk - 1) ptx::umma_commit_cg2_mc(&tfull[buf], 3);
           } else {
             ptx::umma_commit(&empty[stage]);
-            if (kb == num_kb - 1) ptx::umma_commit(&tfull[buf]);
+            if (kb == nk - 1) ptx::umma_commit(&tfull[buf]);
           }
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
@@ -454,7 +461,8 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
     uint8_t* stg_w = stg + (warp - 4) * 2 * tc::STG_BYTES;
     uint32_t sc = 0;  // staged chunks (buffer parity)
     int iter = 0;
-    for (int tile = unit; tile < num_tiles; tile += nunits, ++iter) {
+    for (int w = unit; w < num_work; w += nunits, ++iter) {
+      const int tile = w / ks;
       const int tm_ = (opt & 2) ? tile / tiles_n : tile % tiles_m;
       const int tn_ = (opt & 2) ? tile % tiles_n : tile / tiles_m;
       const int m0 = tm_ * C::TILE_M + (int)rank * tc::BM;
@@ -500,7 +508,7 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              if (epi.beta) ptx::tma_reduce_add_2d(&tmC, sb, nc, mw);
+              if (epi.beta || ks > 1) ptx::tma_reduce_add_2d(&tmC, sb, nc, mw);
               else ptx::tma_store_2d(&tmC, sb, nc, mw);
               ptx::bulk_commit();
             }

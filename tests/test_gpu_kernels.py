@@ -93,3 +93,12 @@ def test_tcgen05_gemm_bias_tanh_bf16_out(bn, shape):
     ref = torch.tanh(Al.float() @ Bw.float() + bias)
     err = (C.float().cpu() - ref).abs().max().item()
     assert err < 1.5e-2 * max(1.0, ref.abs().max().item()), err  # bf16 output rounding + tanh.approx
+
+
+@pytest.mark.parametrize("beta", [0, 1])
+@pytest.mark.parametrize("bn", [256, 257])
+def test_tcgen05_gemm_split_k(beta, bn):
+    """dX-shaped GEMM (M=6400, N=1024, K=4096): the launcher splits K and the
+    slices TMA-reduce-add into C (zeroed first unless accumulating)."""
+    C, ref = _gemm(_lib.MODE_BF16, 6400, 1024, 4096, 0, 0, bn, beta=beta, seed=5)
+    assert (C - ref).abs().max().item() / ref.abs().max().item() < 1e-5
