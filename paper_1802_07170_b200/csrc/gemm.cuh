@@ -40,19 +40,21 @@ struct EpiStore {
   float dscale = 1.f;
   const float* tgrad_y = nullptr;  // multiply by (1 - y^2): tanh' from its output
   long long ld_tgrad = 0;
-  float alpha = 1.f;
 
   // x[j] = epilogue value of (m, n0 + j); rows m >= M read no row operands.
-  CMT_D void compute(int m, int n0, const float* v, int M, int N, float* x) const {
+  // F (compile-time): 1 bias, 2 tanh, 4 dropout mask, 8 tanh' from output, 16 add;
+  // F = 63: any combination, each stage gated at run time.
+  // Every global load of the chunk is issued up front (vectorised where the
+  // row is 16-byte aligned) and the element loop is branch-free.
+  template <int F>
+  CMT_D void compute_t(int m, int n0, const float* v, int M, int N, float* x) const {
     const bool full = (n0 + 32 <= N);
     const bool row_ok = m < M;
-    // Issue every global load of the chunk up front (vectorised where the
-    // row is 16-byte aligned) so their latencies overlap instead of being
-    // paid once per column.
-    float bv[32], tg[32], ad[32];
-    uint8_t km[32];
     const long long rm = row_ok ? (long long)m : 0;
-    if (bias) {
+    const int fl = (F & 32) ? flags() : F;
+    float bv[(F & 1) ? 32 : 1], tg[(F & 8) ? 32 : 1], ad[(F & 16) ? 32 : 1];
+    uint8_t km[(F & 4) ? 32 : 1];
+    if ((F & 1) && (fl & 1)) {
       if (full && (((uintptr_t)(bias + n0)) & 15) == 0) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) *(float4*)&bv[4 * q] = __ldg((const float4*)(bias + n0) + q);
@@ -61,45 +63,61 @@ struct EpiStore {
         for (int j = 0; j < 32; ++j) bv[j] = (n0 + j < N) ? __ldg(bias + n0 + j) : 0.f;
       }
     }
-    if (dmask && row_ok) {
+    if ((F & 4) && (fl & 4)) {
       const uint8_t* dm = dmask + rm * ld_dmask + n0;
-      if (full && (((uintptr_t)dm) & 15) == 0) {
+      if (row_ok && full && (((uintptr_t)dm) & 15) == 0) {
         *(uint4*)&km[0] = *(const uint4*)dm;
         *(uint4*)&km[16] = *(const uint4*)(dm + 16);
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) km[j] = (n0 + j < N) ? dm[j] : 0;
+        for (int j = 0; j < 32; ++j) km[j] = (row_ok && n0 + j < N) ? dm[j] : 0;
       }
     }
-    if (tgrad_y && row_ok) {
+    if ((F & 8) && (fl & 8)) {
       const float* ty = tgrad_y + rm * ld_tgrad + n0;
-      if (full && (((uintptr_t)ty) & 15) == 0) {
+      if (row_ok && full && (((uintptr_t)ty) & 15) == 0) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) *(float4*)&tg[4 * q] = *((const float4*)ty + q);
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) tg[j] = (n0 + j < N) ? ty[j] : 0.f;
+        for (int j = 0; j < 32; ++j) tg[j] = (row_ok && n0 + j < N) ? ty[j] : 0.f;
       }
     }
-    if (add && row_ok) {
+    if ((F & 16) && (fl & 16)) {
       const float* aa = add + rm * ld_add + n0;
-      if (full && (((uintptr_t)aa) & 15) == 0) {
+      if (row_ok && full && (((uintptr_t)aa) & 15) == 0) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) *(float4*)&ad[4 * q] = *((const float4*)aa + q);
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) ad[j] = (n0 + j < N) ? aa[j] : 0.f;
+        for (int j = 0; j < 32; ++j) ad[j] = (row_ok && n0 + j < N) ? aa[j] : 0.f;
       }
     }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      float t = alpha * v[j];
-      if (bias) t += bv[j];
-      if (act == 1) t = c_bf16 ? ptx::tanh_fast(t) : tanhf(t);
-      if (dmask && row_ok) t = km[j] ? t * dscale : 0.f * t;
-      if (tgrad_y && row_ok) t *= (1.f - tg[j] * tg[j]);
-      if (add && row_ok) t += ad[j];
+      float t = v[j];
+      if ((F & 1) && (fl & 1)) t += bv[(F & 1) ? j : 0];
+      if ((F & 2) && (fl & 2)) t = c_bf16 ? ptx::tanh_fast(t) : tanhf(t);
+      if ((F & 4) && (fl & 4)) t = km[(F & 4) ? j : 0] ? t * dscale : 0.f * t;
+      if ((F & 8) && (fl & 8)) t *= (1.f - tg[(F & 8) ? j : 0] * tg[(F & 8) ? j : 0]);
+      if ((F & 16) && (fl & 16)) t += ad[(F & 16) ? j : 0];
       x[j] = t;
+    }
+  }
+  CMT_D int flags() const {
+    return (bias ? 1 : 0) | (act == 1 ? 2 : 0) | (dmask ? 4 : 0) | (tgrad_y ? 8 : 0) | (add ? 16 : 0);
+  }
+  CMT_D void compute(int m, int n0, const float* v, int M, int N, float* x) const {
+    switch (flags()) {
+      case 0: compute_t<0>(m, n0, v, M, N, x); break;
+      case 1: compute_t<1>(m, n0, v, M, N, x); break;
+      case 2: compute_t<2>(m, n0, v, M, N, x); break;
+      case 3: compute_t<3>(m, n0, v, M, N, x); break;
+      case 4: compute_t<4>(m, n0, v, M, N, x); break;
+      case 8: compute_t<8>(m, n0, v, M, N, x); break;
+      case 12: compute_t<12>(m, n0, v, M, N, x); break;
+      case 16: compute_t<16>(m, n0, v, M, N, x); break;
+      default: compute_t<63>(m, n0, v, M, N, x);
     }
   }
 
@@ -475,7 +493,7 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
         ptx::tc_fence_after();
       }
 #pragma unroll 1
-      for (int c = c_lo; c < c_hi; ++c) {
+      for (int c = c_lo; c < ((opt & 4) ? c_lo : c_hi); ++c) {  // opt bit 2: mainloop-only timing experiment
         float v[32];
         if (num_kb > 0) {
           ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN + c * 32, v);
@@ -485,11 +503,26 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
         }
         if constexpr (ST) {
           const int nc = n0 + c * 32, mw = m0 + q * 32;
+          if ((opt & 16) && nc < N) {  // timing experiment: TMEM drain only
+            if (v[lane] == 123.456f) epi.C = nullptr;
+            continue;
+          }
           if (nc < N && mw < M) {
             float x[32];
             epi.compute(m, nc, v, M, N, x);
-            uint8_t* sb = stg_w + (sc & 1) * tc::STG_BYTES;
-            if (lane == 0) ptx::bulk_wait_read1();  // the store that used this buffer 2 chunks ago has read it
+            if (opt & 8) {  // timing experiment: no store
+              if (x[lane] == 123.456f) epi.C = nullptr;
+              continue;
+            }
+            // fp32 rows: 2 x 4 KB buffers; bf16 rows (2 KB): 4 buffers in the same space
+            uint8_t* sb;
+            if (epi.c_bf16) {
+              sb = stg_w + (sc & 3) * (tc::STG_BYTES / 2);
+              if (lane == 0) ptx::bulk_wait_read3();  // the store that used this buffer 4 chunks ago has read it
+            } else {
+              sb = stg_w + (sc & 1) * tc::STG_BYTES;
+              if (lane == 0) ptx::bulk_wait_read1();  // ... 2 chunks ago
+            }
             __syncwarp();
             if (epi.c_bf16) {  // 64 B rows, SWIZZLE_64B: 16 B chunk j of row r at j ^ ((r >> 1) & 3)
               uint4* row = (uint4*)(sb + lane * 64);

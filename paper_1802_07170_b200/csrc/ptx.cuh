@@ -283,6 +283,7 @@ CMT_D void tma_reduce_add_2d(const void* tmap, const void* smem, int c0, int c1)
 }
 CMT_D void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 CMT_D void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+CMT_D void bulk_wait_read3() { asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); }
 CMT_D void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 CMT_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 }  // namespace ptx
