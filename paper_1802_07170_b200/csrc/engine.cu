@@ -130,6 +130,7 @@ struct Mat {
 };
 
 static int g_num_sms = 148;
+constexpr int FLAG_STRIDE = 128;  // step counters per scan (per-k-block readiness flags)
 
 // ---- kernel timeline (debug option "timeline"): an event after every launch
 // on the engine stream; consecutive event deltas are the per-launch device
@@ -648,7 +649,7 @@ class Engine {
       gcomp[t] = carve<float>(cur, (NS + NT) * E * 4);
     }
     normpart = carve<double>(cur, 3 * NORM_BLOCKS * 8);
-    flags = carve<unsigned>(cur, 64 * 4);
+    flags = carve<unsigned>(cur, 64 * FLAG_STRIDE * 4);
     scal_d = carve<StepScalars>(cur, sizeof(StepScalars));
     out_d = carve<StepOut>(cur, sizeof(StepOut));
     s32_d = carve<float>(cur, 4);
@@ -907,7 +908,7 @@ class Engine {
     float* uxb;  // hoisted input projection buffer of this scan
   };
   bool use_dual_fwd() const {
-    return bf && persistent && dual && H % (64 * mc::Fwd<128>::KBOX) == 0 && B <= 128 &&
+    return bf && persistent && dual && H % (64 * mc::Fwd<128>::KBOX) == 0 && H / 64 <= 32 && B <= 128 &&
            2 * mc::Fwd<128>::ctas(H, B) <= g_num_sms &&
            mc::Fwd<128>::stages(H) >= 2;
   }
@@ -925,12 +926,12 @@ class Engine {
     make_map(tmW, wv(ly.w_off), 4LL * H, f.din + H, 4LL * H, 64, 64);
     LstmFwdP prm;
     prm.ux = f.uxb; prm.y = (bf16*)v.ybase; prm.hprev = (const bf16*)v.hprev; prm.cst = v.cbase; prm.cprev = v.cprev;
-    prm.acts = lw[f.l].acts; prm.tcache = lw[f.l].tc; prm.mask = f.mask; prm.flag = flags + (f.l & 31);
+    prm.acts = lw[f.l].acts; prm.tcache = lw[f.l].tc; prm.mask = f.mask; prm.flag = flags + (f.l & 31) * FLAG_STRIDE;
     prm.steps = f.steps; prm.B = B; prm.H = H; prm.din = f.din; prm.reverse = f.reverse ? 1 : 0;
     prm.hrow0 = f.reverse ? B : 0;
     prm.trace = (trace_layer == f.l) ? trace_d : nullptr;
     prm.stages = mc::Fwd<ROWS>::stages(H);
-    CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
+    CMT_CUDA(cudaMemsetAsync(prm.flag, 0, FLAG_STRIDE * 4, st));
     return prm;
   }
   // two independent scans in one cooperative launch (64 CTAs each at H=1024, B=128)
@@ -959,7 +960,43 @@ class Engine {
     tl_mark(st, "lstm_fwd_pair");
   }
 
+  // one scan through lstm_fwd_multi<64> (batch halves on separate CTAs, 128 CTAs at H=1024)
+  bool use_multi_single_fwd() const {
+    return use_dual_fwd() && H % (64 * mc::Fwd<64>::KBOX) == 0 && (H / 64) * ((B + 63) / 64) <= 32 &&
+           mc::Fwd<64>::ctas(H, B) <= g_num_sms && mc::Fwd<64>::stages(H) >= 2;
+  }
+  void fwd_single(const FwdScan& a) {
+    CUtensorMap tm[2];
+    LstmFwdMulti m;
+    m.c[0] = fwd_params<64>(a, &tm[0], &tm[1]);
+    m.c[1] = m.c[0];
+    const int g = mc::Fwd<64>::ctas(H, B);
+    m.split = g;
+    auto k = lstm_fwd_multi<64>;
+    const size_t smem = mc::Fwd<64>::smem(H);
+    CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3(g);
+    c.blockDim = dim3(mc::THREADS);
+    c.dynamicSmemBytes = smem;
+    c.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    c.attrs = at;
+    c.numAttrs = 1;
+    CMT_CUDA(cudaLaunchKernelEx(&c, k, tm[0], tm[1], tm[0], tm[1], m));
+    CMT_LAUNCHED();
+    tl_mark(st, "lstm_fwd_single");
+  }
+
   void scan_fwd(int l, const void* X, int din, int steps, bool reverse, const float* mask) {
+    if (use_multi_single_fwd()) {
+      FwdScan f{l, X, din, steps, reverse, mask, ux};
+      fwd_prep(f);
+      fwd_single(f);
+      return;
+    }
     const Layer& ly = layers[l];
     long long N = (long long)steps * B;
     // hoisted input projection Ux = X W_x + b   (layers.py:354-357, K3)
@@ -973,7 +1010,7 @@ class Engine {
       make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 64);
       LstmFwdP prm;
       prm.ux = ux; prm.y = (bf16*)v.ybase; prm.hprev = (const bf16*)v.hprev; prm.cst = v.cbase; prm.cprev = v.cprev;
-      prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.mask = mask; prm.flag = flags + (l & 31);
+      prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.mask = mask; prm.flag = flags + (l & 31) * FLAG_STRIDE;
       prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
       prm.hrow0 = reverse ? B : 0;
       prm.trace = (trace_layer == l) ? trace_d : nullptr;
@@ -988,7 +1025,7 @@ class Engine {
       make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 64);
       LstmFwdP prm;
       prm.ux = ux; prm.y = (bf16*)v.ybase; prm.hprev = (const bf16*)v.hprev; prm.cst = v.cbase; prm.cprev = v.cprev;
-      prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.mask = mask; prm.flag = flags + (l & 31);
+      prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.mask = mask; prm.flag = flags + (l & 31) * FLAG_STRIDE;
       prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
       prm.hrow0 = reverse ? B : 0;
       prm.trace = (trace_layer == l) ? trace_d : nullptr;
@@ -1041,11 +1078,11 @@ class Engine {
     LstmBwdP prm;
     prm.dy = f.dy; prm.acts = lw[f.l].acts; prm.tcache = lw[f.l].tc; prm.cprev = v.cprev; prm.mask = f.mask;
     prm.dU = (bf16*)f.dUb; prm.dh_final = f.dh_final; prm.dc_final = f.dc_final; prm.dh0 = f.dh0; prm.dc0 = f.dc0;
-    prm.flag = flags + 32 + (f.l & 31);
+    prm.flag = flags + (32 + (f.l & 31)) * FLAG_STRIDE;
     prm.steps = f.steps; prm.B = B; prm.H = H; prm.din = f.din; prm.reverse = f.reverse ? 1 : 0;
     prm.trace = (trace_layer == 100 + f.l) ? trace_d : nullptr;
     prm.stages = mc::bwd_stages(H);
-    CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
+    CMT_CUDA(cudaMemsetAsync(prm.flag, 0, FLAG_STRIDE * 4, st));
     return prm;
   }
   void bwd_pair(const BwdScan& a, const BwdScan& b) {
@@ -1113,7 +1150,7 @@ class Engine {
       LstmBwdP prm;
       prm.dy = dy; prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.cprev = v.cprev; prm.mask = mask;
       prm.dU = (bf16*)dU; prm.dh_final = dh_final; prm.dc_final = dc_final; prm.dh0 = dh0; prm.dc0 = dc0;
-      prm.flag = flags + 32 + (l & 31);
+      prm.flag = flags + (32 + (l & 31)) * FLAG_STRIDE;
       prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
       prm.trace = (trace_layer == 100 + l) ? trace_d : nullptr;
       prm.stages = cl::bwd_stages(H);
@@ -1126,7 +1163,7 @@ class Engine {
       LstmBwdP prm;
       prm.dy = dy; prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.cprev = v.cprev; prm.mask = mask;
       prm.dU = (bf16*)dU; prm.dh_final = dh_final; prm.dc_final = dc_final; prm.dh0 = dh0; prm.dc0 = dc0;
-      prm.flag = flags + 32 + (l & 31);
+      prm.flag = flags + (32 + (l & 31)) * FLAG_STRIDE;
       prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
       prm.trace = nullptr;
       prm.stages = pr::stages_for(H);

@@ -94,27 +94,44 @@ __global__ void __launch_bounds__(mc::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
+    // ===== producer (whole warp): h_{t-1} k-block kb is ready once its 4
+    // producer CTAs (units [64kb, 64kb+64), this batch half) have bumped
+    // flag[kb * nh + half] for the previous step; lanes poll the flags in
+    // parallel and lane 0 streams every stage whose k-blocks are ready, so
+    // the first k-blocks load while the slowest producers are still finishing.
     if (lane == 0) {
       ptx::mbar_expect_tx(wfull, KB * 8192);
       for (int kb = 0; kb < KB; ++kb) ptx::tma_load_2d(tmW, wfull, sW + kb * 8192, n0, p.din + kb * 64);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int s = 0; s < p.steps; ++s) {
-        const int t = p.reverse ? p.steps - 1 - s : s;
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    const int nst = KB / F::KBOX;
+    for (int s = 0; s < p.steps; ++s) {
+      const int t = p.reverse ? p.steps - 1 - s : s;
+      if (p.trace && bid == 0 && lane == 0) p.trace[s * 8 + 0] = gtimer();
+      const int hrow = p.hrow0 + t * p.B + r0;
+      const unsigned target = 4u * (unsigned)s;
+      int issued = 0;
+      while (issued < nst) {
+        unsigned ready = 0xffffffffu;
         if (s > 0) {
-          const unsigned target = (unsigned)(G * s);
-          while (ptx::ld_relaxed(p.flag) < target) {}
-          ptx::fence_acquire_gpu();
-          ptx::fence_proxy_async_global();
+          const bool ok = lane >= KB || ptx::ld_acquire(p.flag + lane * nh + half) >= target;
+          ready = __ballot_sync(0xffffffffu, ok);
+          __syncwarp();  // order the lanes' acquire loads before lane 0's TMA issue
         }
-        if (p.trace && bid == 0) p.trace[s * 8 + 0] = gtimer();
-        const int hrow = p.hrow0 + t * p.B + r0;
-        for (int kb = 0; kb < KB; kb += F::KBOX) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::tma_load_3d(tmH, &full[stage], sA + stage * mc::STAGE_BYTES, 0, hrow, kb);
-          ptx::mbar_expect_tx(&full[stage], mc::STAGE_BYTES);
-          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        if (lane == 0) {
+          if (s > 0) ptx::fence_proxy_async_global();
+          while (issued < nst) {
+            const unsigned need = ((1u << F::KBOX) - 1u) << (issued * F::KBOX);
+            if ((ready & need) != need) break;
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            ptx::tma_load_3d(tmH, &full[stage], sA + stage * mc::STAGE_BYTES, 0, hrow, issued * F::KBOX);
+            ptx::mbar_expect_tx(&full[stage], mc::STAGE_BYTES);
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+            ++issued;
+          }
         }
+        issued = __shfl_sync(0xffffffffu, issued, 0);
       }
     }
   } else if (warp == 1) {
@@ -212,7 +229,7 @@ __global__ void __launch_bounds__(mc::THREADS, 1)
       // publish h_t (the only value other CTAs need), then write the BPTT caches
       ptx::named_bar_sync(1, ROWS);
       if (threadIdx.x == 128) {
-        ptx::red_release_add(p.flag, 1u);
+        ptx::red_release_add(p.flag + (u0 >> 6) * nh + half, 1u);
         if (p.trace && bid == 0) p.trace[s * 8 + 3] = gtimer();
       }
       if (valid) {
