@@ -1065,7 +1065,8 @@ class Engine {
     void* dUb;
   };
   bool use_dual_bwd() const {
-    return bf && persistent && dual && H % mc::BWD_NU == 0 && (H / 64) % mc::BWD_KBOX == 0 && B <= 128 &&
+    return bf && persistent && dual && H % mc::BWD_NU == 0 && (H / 64) % mc::BWD_KBOX == 0 && H / 64 <= 32 &&
+           4 * H / 64 <= FLAG_STRIDE && B <= 128 &&
            2 * mc::bwd_ctas(H) <= g_num_sms &&
            mc::bwd_stages(H) >= 1 && (size_t)mc::bwd_stages(H) * mc::STAGE_BYTES >= (size_t)128 * mc::XROW;
   }

@@ -346,26 +346,42 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
+    // ===== producer (whole warp): k-block kb of dU (gate columns [64kb, 64kb+64)
+    // = 16 units) is written by exactly one CTA, which bumps flag[kb] once per
+    // round; lanes poll this CTA's KBL flags in parallel and lane 0 streams
+    // every stage whose k-blocks are ready (no grid-wide step barrier).
     if (lane == 0) {
       ptx::mbar_expect_tx(wfull, KBL * mc::BWD_NU * 128);
       for (int kb = 0; kb < KBL; ++kb)
         ptx::tma_load_2d(tmW, wfull, sW + kb * (mc::BWD_NU * 128), (kb_base + kb) * 64, p.din + ug);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int i = 1; i < rounds; ++i) {
-        const unsigned target = (unsigned)(G * i);
-        while (ptx::ld_relaxed(p.flag) < target) {}
-        ptx::fence_acquire_gpu();
-        ptx::fence_proxy_async_global();
-        ptx::fence_proxy_async_shared();
-        if (p.trace && bid == 0) p.trace[i * 8 + 0] = gtimer();
-        const int arow = time_of(p.steps - i) * p.B;
-        for (int kb = 0; kb < KBL; kb += mc::BWD_KBOX) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::tma_load_3d(tmA, &full[stage], sA + stage * mc::STAGE_BYTES, 0, arow, kb_base + kb);
-          ptx::mbar_expect_tx(&full[stage], mc::STAGE_BYTES);
-          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    const int nst = KBL / mc::BWD_KBOX;
+    for (int i = 1; i < rounds; ++i) {
+      if (p.trace && bid == 0 && lane == 0) p.trace[i * 8 + 0] = gtimer();
+      const int arow = time_of(p.steps - i) * p.B;
+      const unsigned target = (unsigned)i;
+      int issued = 0;
+      while (issued < nst) {
+        const bool ok = lane >= KBL || ptx::ld_acquire(p.flag + kb_base + lane) >= target;
+        const unsigned ready = __ballot_sync(0xffffffffu, ok);
+        __syncwarp();
+        if (lane == 0) {
+          ptx::fence_proxy_async_global();
+          ptx::fence_proxy_async_shared();
+          while (issued < nst) {
+            const unsigned need = ((1u << mc::BWD_KBOX) - 1u) << (issued * mc::BWD_KBOX);
+            if ((ready & need) != need) break;
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            ptx::tma_load_3d(tmA, &full[stage], sA + stage * mc::STAGE_BYTES, 0, arow,
+                             kb_base + issued * mc::BWD_KBOX);
+            ptx::mbar_expect_tx(&full[stage], mc::STAGE_BYTES);
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+            ++issued;
+          }
         }
+        issued = __shfl_sync(0xffffffffu, issued, 0);
       }
     }
   } else if (warp == 1) {
@@ -531,7 +547,7 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
       if (p.trace && bid == 0 && threadIdx.x == 128) p.trace[i * 8 + 3] = gtimer();
       ptx::named_bar_sync(1, 256);
       if (threadIdx.x == 128) {
-        ptx::red_release_add(p.flag, 1u);
+        ptx::red_release_add(p.flag + ((ug + kq * 16) >> 4), 1u);  // my k-block: gate columns 4*(ug+16kq) ..
         if (p.trace && bid == 0) p.trace[i * 8 + 4] = gtimer();
       }
     }
