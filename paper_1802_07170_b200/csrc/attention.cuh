@@ -252,4 +252,204 @@ __global__ void __launch_bounds__(att::THREADS) attn_bwd_tiled(const E* __restri
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Split attention (one sentence spread over many CTAs; the score products'
+// H reduction is split into HSPLIT slices whose partial sums are reduced in
+// a fixed order, so results stay deterministic):
+//   attn_scores_part   grid (B, H/HS): part[b][sp][t][s] = sum_{h in slice} X[t][h] Hs[s][h]
+//   attn_softmax_fwd   grid B: scores = sum of slices, masked softmax -> alpha
+//   attn_context       grid (B, H/HC): ctx[t][h] = sum_s alpha[t][s] Hs[s][h]
+//   attn_dscores       grid B: dalpha = sum of slices; dscores = alpha (dalpha - sum alpha dalpha)
+//   attn_bwd_chunk     grid (B, H/HC): dHs += alpha^T dC + dscores^T U, dU = dscores Hs
+// Same arithmetic as attn_fwd_tiled / attn_bwd_tiled, spread over 16x the CTAs.
+// ---------------------------------------------------------------------------
+namespace att {
+constexpr int HS = 128;  // h-slice of the score products per CTA
+inline int nslices(int H) { return (H + HS - 1) / HS; }
+}  // namespace att
+
+template <typename EX, typename EH>
+__global__ void __launch_bounds__(att::THREADS) attn_scores_part(const EX* __restrict__ X, long long ldx,
+                                                                 const EH* __restrict__ Hs, int S, int Tq, int B, int H,
+                                                                 float* __restrict__ part) {
+  using namespace att;
+  __shared__ __align__(16) float sX[KC * LD];
+  __shared__ __align__(16) float sH[KC * LD];
+  const int b = blockIdx.x, sp = blockIdx.y;
+  const int h0 = sp * HS, h1 = min(H, h0 + HS);
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  float acc[4][4];
+  zero44(acc);
+  for (int k0 = h0; k0 < h1; k0 += KC) {
+    load_t(sX, X, ldx, Tq, B, b, k0, h1);
+    load_t(sH, Hs, H, S, B, b, k0, h1);
+    __syncthreads();
+    mm44(acc, sX, sH, ty * 4, tx * 4, KC);
+    __syncthreads();
+  }
+  float* o = part + ((size_t)b * gridDim.y + sp) * P * P;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    *(float4*)(o + (ty * 4 + i) * P + tx * 4) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+}
+
+__global__ void __launch_bounds__(att::THREADS) attn_softmax_fwd(const float* __restrict__ part, int nsp,
+                                                                 const float* __restrict__ src_mask, int S, int Tq,
+                                                                 int B, float* __restrict__ alpha,
+                                                                 int* __restrict__ status) {
+  using namespace att;
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* pb = part + (size_t)b * nsp * P * P;
+  for (int t = warp; t < Tq; t += THREADS / 32) {
+    float v[2];
+    float mx = -INFINITY;
+    bool bad = false;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int s = lane + 32 * r;
+      float a = 0.f;
+      if (s < S) {
+        for (int k = 0; k < nsp; ++k) a += pb[((size_t)k * P + t) * P + s];
+        a += (1.f - src_mask[s * B + b]) * -1e9f;
+        bad |= !isfinite(a);
+        mx = fmaxf(mx, a);
+      }
+      v[r] = a;
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int s = lane + 32 * r;
+      v[r] = s < S ? expf(v[r] - mx) : 0.f;
+      sum += v[r];
+    }
+    sum = warp_sum(sum);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int s = lane + 32 * r;
+      if (s < S) alpha[((long long)b * Tq + t) * S + s] = v[r] / sum;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_SCORES);
+  }
+}
+
+template <typename E>
+__global__ void __launch_bounds__(att::THREADS) attn_context(const E* __restrict__ Hs, const float* __restrict__ alpha,
+                                                             int S, int Tq, int B, int H, E* __restrict__ ctx,
+                                                             long long ldctx) {
+  using namespace att;
+  __shared__ __align__(16) float aT[P * LD];  // [s][t]
+  __shared__ __align__(16) float ch[P * LD];  // [s][h]
+  const int b = blockIdx.x, h0 = blockIdx.y * HC;
+  for (int i = threadIdx.x; i < P * P; i += THREADS) {
+    const int s = i / P, t = i % P;
+    aT[s * LD + t] = (s < S && t < Tq) ? alpha[((long long)b * Tq + t) * S + s] : 0.f;
+  }
+  load_n(ch, Hs, H, S, B, b, h0, H);
+  __syncthreads();
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  float acc[4][4];
+  zero44(acc);
+  mm44(acc, aT, ch, ty * 4, tx * 4, S);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = ty * 4 + i;
+    if (t >= Tq) continue;
+    E* o = ctx + ((long long)t * B + b) * ldctx + h0 + tx * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (h0 + tx * 4 + j < H) o[j] = from_f<E>(acc[i][j]);
+  }
+}
+
+__global__ void __launch_bounds__(att::THREADS) attn_dscores(const float* __restrict__ part, int nsp,
+                                                             const float* __restrict__ alpha, int S, int Tq,
+                                                             float* __restrict__ dsc) {
+  using namespace att;
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* pb = part + (size_t)b * nsp * P * P;
+  for (int t = warp; t < Tq; t += THREADS / 32) {
+    float g[2], p[2];
+    float dot = 0.f;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int s = lane + 32 * r;
+      float a = 0.f, pv = 0.f;
+      if (s < S) {
+        for (int k = 0; k < nsp; ++k) a += pb[((size_t)k * P + t) * P + s];
+        pv = alpha[((long long)b * Tq + t) * S + s];
+      }
+      g[r] = a;
+      p[r] = pv;
+      dot += pv * a;
+    }
+    dot = warp_sum(dot);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int s = lane + 32 * r;
+      if (s < S) dsc[((long long)b * Tq + t) * S + s] = p[r] * (g[r] - dot);
+    }
+  }
+}
+
+template <typename E>
+__global__ void __launch_bounds__(att::THREADS) attn_bwd_chunk(const E* __restrict__ Hs, const E* __restrict__ U,
+                                                               const float* __restrict__ alpha,
+                                                               const float* __restrict__ dsc,
+                                                               const float* __restrict__ dC, long long lddc, int S,
+                                                               int Tq, int B, int H, float* __restrict__ dHs,
+                                                               E* __restrict__ dU) {
+  using namespace att;
+  extern __shared__ float sm[];
+  float* al = sm;             // [t][s]
+  float* ds = al + P * LD;    // [t][s]
+  float* dsT = ds + P * LD;   // [s][t]
+  float* cC = dsT + P * LD;   // [t][h]
+  float* cU = cC + P * LD;    // [t][h]
+  float* cH = cU + P * LD;    // [s][h]
+  const int b = blockIdx.x, h0 = blockIdx.y * HC;
+  for (int i = threadIdx.x; i < P * P; i += THREADS) {
+    const int t = i / P, s = i % P;
+    const bool ok = t < Tq && s < S;
+    const long long o = ((long long)b * Tq + t) * S + s;
+    al[t * LD + s] = ok ? alpha[o] : 0.f;
+    const float d = ok ? dsc[o] : 0.f;
+    ds[t * LD + s] = d;
+    dsT[s * LD + t] = d;
+  }
+  load_n(cC, dC, lddc, Tq, B, b, h0, H);
+  load_n(cU, U, H, Tq, B, b, h0, H);
+  load_n(cH, Hs, H, S, B, b, h0, H);
+  __syncthreads();
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  float acc[4][4];
+  zero44(acc);
+  mm44(acc, al, cC, ty * 4, tx * 4, Tq);
+  mm44(acc, ds, cU, ty * 4, tx * 4, Tq);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int s = ty * 4 + i;
+    if (s >= S) continue;
+    float* o = dHs + ((long long)s * B + b) * H + h0 + tx * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (h0 + tx * 4 + j < H) o[j] += acc[i][j];
+  }
+  zero44(acc);
+  mm44(acc, dsT, cH, ty * 4, tx * 4, S);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = ty * 4 + i;
+    if (t >= Tq) continue;
+    E* o = dU + ((long long)t * B + b) * H + h0 + tx * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (h0 + tx * 4 + j < H) o[j] = from_f<E>(acc[i][j]);
+  }
+}
+
 }  // namespace cmt

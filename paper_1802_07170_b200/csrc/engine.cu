@@ -337,6 +337,8 @@ class Engine {
   float *src_mask_d, *tgt_mask_d;
   void *Xs, *Xt, *top, *u_att, *cst_att, *hod, *Y, *dhpre, *du_att, *dU, *dU2;
   float* cepart = nullptr;  // per-CTA dY column sums of the fused CE kernel
+  float *att_part = nullptr, *att_dsc = nullptr;  // split attention: score slices, d scores
+  int att_split = 1;  // option: split attention kernels (many CTAs per sentence)
   float *ux, *ux2, *alpha, *ho, *losstok, *dcst, *dXemb, *dtop, *dhc, *dcc, *colpart;
   std::vector<void*> drop_enc, drop_dec;
   std::vector<uint8_t*> keep_enc, keep_dec;
@@ -621,6 +623,8 @@ class Engine {
     }
     u_att = carve<char>(cur, NT * H * asz);
     alpha = carve<float>(cur, (long long)B * T * S * 4);
+    att_dsc = carve<float>(cur, (long long)B * T * S * 4);
+    att_part = carve<float>(cur, (long long)B * att::nslices(H) * att::P * att::P * 4);
     cst_att = carve<char>(cur, NT * 2 * H * asz);
     ho = carve<float>(cur, NT * H * 4);
     hod = carve<char>(cur, NT * H * asz);
@@ -1323,7 +1327,21 @@ class Engine {
     // attention (attention.py:146-173)
     copy_act(Ht, H, (char*)cst_att + (size_t)H * asz, 2LL * H, (int)NT, H);
     gemm((int)NT, H, H, Mat{Ht, H, 0}, Mat{wv(off_wa), H, 1}, store(u_att, H, true));
-    if (S <= att::P && T <= att::P) {
+    if (S <= att::P && T <= att::P && att_split) {
+      const int nsp = att::nslices(H);
+      dim3 gs(B, nsp), gc(B, ceil_div(H, att::HC));
+      if (bf) attn_scores_part<bf16, bf16><<<gs, att::THREADS, 0, st>>>((const bf16*)u_att, H, (const bf16*)Hs, S, T, B, H,
+                                                                       att_part);
+      else attn_scores_part<float, float><<<gs, att::THREADS, 0, st>>>((const float*)u_att, H, (const float*)Hs, S, T, B,
+                                                                       H, att_part);
+      CMT_LAUNCHED(); tl_mark(st, "attn_scores_part");
+      attn_softmax_fwd<<<B, att::THREADS, 0, st>>>(att_part, nsp, src_mask_d, S, T, B, alpha, status_d);
+      CMT_LAUNCHED(); tl_mark(st, "attn_softmax_fwd");
+      if (bf) attn_context<bf16><<<gc, att::THREADS, 0, st>>>((const bf16*)Hs, alpha, S, T, B, H, (bf16*)cst_att, 2LL * H);
+      else attn_context<float><<<gc, att::THREADS, 0, st>>>((const float*)Hs, alpha, S, T, B, H, (float*)cst_att, 2LL * H);
+      CMT_LAUNCHED(); tl_mark(st, "attn_context");
+      CMT_CUDA(cudaGetLastError());
+    } else if (S <= att::P && T <= att::P) {
       const size_t smem = att::fwd_smem();
       if (bf) {
         CMT_CUDA(cudaFuncSetAttribute(attn_fwd_tiled<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1423,7 +1441,27 @@ class Engine {
     // attention core backward
     float* dHs = (L == 1) ? dtop : lw[L].dy;
     CMT_CUDA(cudaMemsetAsync(dHs, 0, NS * H * 4, st));
-    if (S <= att::P && T <= att::P) {
+    if (S <= att::P && T <= att::P && att_split) {
+      const int nsp = att::nslices(H);
+      dim3 gs(B, nsp), gc(B, ceil_div(H, att::HC));
+      if (bf) attn_scores_part<float, bf16><<<gs, att::THREADS, 0, st>>>(dcst, 2LL * H, (const bf16*)Hs, S, T, B, H, att_part);
+      else attn_scores_part<float, float><<<gs, att::THREADS, 0, st>>>(dcst, 2LL * H, (const float*)Hs, S, T, B, H, att_part);
+      CMT_LAUNCHED(); tl_mark(st, "attn_scores_part");
+      attn_dscores<<<B, att::THREADS, 0, st>>>(att_part, nsp, alpha, S, T, att_dsc);
+      CMT_LAUNCHED(); tl_mark(st, "attn_dscores");
+      const size_t smem = sizeof(float) * 6 * att::P * att::LD;
+      if (bf) {
+        CMT_CUDA(cudaFuncSetAttribute(attn_bwd_chunk<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attn_bwd_chunk<bf16><<<gc, att::THREADS, smem, st>>>((const bf16*)Hs, (const bf16*)u_att, alpha, att_dsc, dcst,
+                                                             2LL * H, S, T, B, H, dHs, (bf16*)du_att);
+      } else {
+        CMT_CUDA(cudaFuncSetAttribute(attn_bwd_chunk<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attn_bwd_chunk<float><<<gc, att::THREADS, smem, st>>>((const float*)Hs, (const float*)u_att, alpha, att_dsc, dcst,
+                                                              2LL * H, S, T, B, H, dHs, (float*)du_att);
+      }
+      CMT_LAUNCHED(); tl_mark(st, "attn_bwd_chunk");
+      CMT_CUDA(cudaGetLastError());
+    } else if (S <= att::P && T <= att::P) {
       const size_t smem = att::bwd_smem();
       if (bf) {
         CMT_CUDA(cudaFuncSetAttribute(attn_bwd_tiled<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1810,6 +1848,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "cg2") e->eng->cg2 = (int)value;
     else if (k == "dual") e->eng->dual = (int)value;
     else if (k == "jump") e->eng->use_jump = (int)value;
+    else if (k == "att_split") e->eng->att_split = (int)value;
     else if (k == "ce2") {
       if (e->eng->staged && (value != 0) != (e->eng->ce2 != 0)) throw Error(cmt::CMT_ERR_CONFIG, "set ce2 before staging");
       e->eng->ce2 = (int)value;

@@ -153,7 +153,7 @@ CMT_D u128 pcg_jump(const PcgJump* __restrict__ t, u128 s, unsigned long long de
 
 // Same contract as dropout_fwd_kernel2 with the table jump and 64 draws per
 // thread (the jump is amortised over twice as many draws).
-constexpr int DROP_DPT = 64;
+constexpr int DROP_DPT = 16;
 // keep  <=>  (r >> 11) * 2^-53 >= p  <=>  (r >> 11) >= ceil(p * 2^53): the
 // reference's double comparison done exactly in integers (p * 2^53 is exact).
 inline unsigned long long dropout_threshold(double p) { return (unsigned long long)std::ceil(p * 9007199254740992.0); }

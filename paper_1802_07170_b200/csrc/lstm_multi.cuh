@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(mc::THREADS, 1)
             const unsigned need = ((1u << F::KBOX) - 1u) << (issued * F::KBOX);
             if ((ready & need) != need) break;
             ptx::mbar_wait(&empty[stage], phase ^ 1);
+            if (p.trace && bid == 0 && (issued == 0 || issued == nst - 1)) p.trace[s * 8 + (issued ? 5 : 4)] = gtimer();
             ptx::tma_load_3d(tmH, &full[stage], sA + stage * mc::STAGE_BYTES, 0, hrow, issued * F::KBOX);
             ptx::mbar_expect_tx(&full[stage], mc::STAGE_BYTES);
             if (++stage == p.stages) { stage = 0; phase ^= 1; }
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(mc::THREADS, 1)
         for (int kb0 = 0; kb0 < KB; kb0 += F::KBOX) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (p.trace && bid == 0 && (kb0 == 0 || kb0 + F::KBOX >= KB)) p.trace[s * 8 + (kb0 ? 7 : 6)] = gtimer();
           const uint32_t a0 = ptx::smem_u32(sA + stage * mc::STAGE_BYTES);
 #pragma unroll
           for (int j = 0; j < F::KBOX; ++j) {

@@ -27,6 +27,18 @@ eng.run(1.0, 5.0, 0.1, rng)
 X = np.array([eng.stat(f"trace:{i}")[0] for i in range(51 * 8)]).reshape(51, 8).astype(np.float64)
 names = ["t0", "t1", "t2", "t3", "t4", "t5", "t6", "t7"]
 rows = slice(3, 40)
+if layer < 100:
+    # fwd multi: 4 first stage issued, 5 last stage issued, 6 first stage landed (MMA),
+    # 7 last stage landed, 1 tfull (epilogue), 2 cell done, 3 published
+    seq = [(3, "published(prev)"), (4, "first issue"), (5, "last issue"), (6, "first landed"), (7, "last landed"),
+           (1, "tfull"), (2, "cell done"), (3, "published")]
+    R = X[1:][rows]
+    P = X[:-1][rows]
+    prev = P[:, 3]
+    for col, nm in seq[1:]:
+        cur = R[:, col]
+        print(f"  {nm:14s} +{np.median(cur - prev) / 1e3:6.2f} us")
+        prev = cur
 per = np.diff(X[:, 0])[rows]
 print(f"layer {layer}: step period us median {np.median(per) / 1e3:.2f}")
 for a, b in [(0, 1), (1, 2), (2, 3), (3, 4)]:

@@ -265,3 +265,28 @@ def test_dp_path_single_rank_nccl_matches_plain(mode):
     assert abs(out[0][1] - out[1][1]) <= 1e-5 * out[0][1]
     for n in out[0][2]:
         assert O.norm_rel_err(out[1][2][n], out[0][2][n]) < 1e-6, n
+
+
+@pytest.mark.parametrize("case", [(304, 64, 128, 2, 24, 17, 13, True), (256, 128, 256, 1, 8, 64, 64, False)])
+def test_attention_variants_agree(case):
+    """Split attention kernels (many CTAs per sentence, default) against the
+    one-CTA-per-sentence tiled kernels and the oracle (bf16 step)."""
+    from paper_1802_07170_b200.engine import Engine
+    from paper_1802_07170_b200.model import Batch
+    from tests.gpu_helpers import cfg_of
+    V, E, H, L, B, S, T, ragged = case
+    d = O.Dims(V, E, H, L, 0.0)
+    params = scaled_params(d, 13, 0.1)
+    src, sm, tgt, tm = O.synthetic_batch(V, S, T, B, seed=8, ragged=ragged)
+    _, _, og, _, _ = oracle_step(d, params, (src, sm, tgt, tm), 0.1, 1.0, 5.0, 3, update=False)
+    out = {}
+    for split in (0, 1):
+        eng = Engine(cfg_of(d), mode="bf16")
+        eng.set_option("att_split", split)
+        eng.upload(params)
+        eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, np.random.Generator(np.random.PCG64(3)), update=False)
+        out[split] = eng.grads()
+        eng.close()
+    for n in og:
+        assert O.norm_rel_err(out[1][n], out[0][n]) < 1e-3, n
+        assert O.norm_rel_err(out[1][n], og[n]) < BF16_TOL, n
