@@ -49,11 +49,42 @@ __global__ void scatter_compact_kernel(const float* __restrict__ dX, int E, cons
                                        const int* __restrict__ seg_pos, int nseg, float* __restrict__ gout) {
   int u = blockIdx.x;
   if (u >= nseg) return;
-  int b = seg_off[u], e_ = seg_off[u + 1];
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    float acc = 0.f;
-    for (int p = b; p < e_; ++p) acc += dX[(long long)seg_pos[p] * E + e];
-    gout[(long long)u * E + e] = acc;
+  const int b = seg_off[u], e_ = seg_off[u + 1];
+  // up to 8 columns per thread and 4 positions per iteration in flight (long
+  // segments such as BOS span every sentence); fixed summation order, so the
+  // result is deterministic (4 interleaved partial sums, combined in order)
+  for (int e0 = threadIdx.x; e0 < E; e0 += 8 * blockDim.x) {
+    float acc[4][8];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[r][j] = 0.f;
+    int p = b;
+    for (; p + 4 <= e_; p += 4) {
+      long long rowp[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) rowp[r] = (long long)seg_pos[p + r] * E;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int e = e0 + j * blockDim.x;
+          if (e < E) acc[r][j] += dX[rowp[r] + e];
+        }
+    }
+    for (; p < e_; ++p) {
+      const long long rp = (long long)seg_pos[p] * E;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = e0 + j * blockDim.x;
+        if (e < E) acc[0][j] += dX[rp + e];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = e0 + j * blockDim.x;
+      if (e < E) gout[(long long)u * E + e] = (acc[0][j] + acc[1][j]) + (acc[2][j] + acc[3][j]);
+    }
   }
 }
 
@@ -611,9 +642,15 @@ __global__ void colsum_partial_kernel(const T* __restrict__ D, long long ld, int
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   int r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
-  float a = 0.f;
-  for (int r = r0; r < r1; ++r) a += to_f<T>(D[(long long)r * ld + c]);
-  part[(long long)blockIdx.y * cols + c] = a;
+  // 8 rows in flight per iteration (independent partial sums, fixed order)
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  int r = r0;
+  for (; r + 8 <= r1; r += 8) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] += to_f<T>(D[(long long)(r + k) * ld + c]);
+  }
+  for (; r < r1; ++r) a[0] += to_f<T>(D[(long long)r * ld + c]);
+  part[(long long)blockIdx.y * cols + c] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
 }
 __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, int cols, float* __restrict__ out) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
