@@ -44,7 +44,9 @@ enum cmt_mode {
 /* step flags */
 enum cmt_flags {
   CMT_FLAG_NO_UPDATE = 1, /* compute loss + grads, skip clip/SGD (grads kept for cmt_download_grad) */
-  CMT_FLAG_ASYNC = 2      /* do not wait for the step; result filled by cmt_wait() */
+  CMT_FLAG_ASYNC = 2,     /* do not wait for the step; result filled by cmt_wait() */
+  CMT_FLAG_INFER = 4      /* forward only in INFER mode (no dropout, no backward, no update):
+                             the dev_entropy pass of training.py:162-182 (use epsilon = 0) */
 };
 
 /* mirrors ModelConfig (model.py:46-62) */
@@ -70,6 +72,8 @@ typedef struct {
   double grad_norm;             /* global L2 norm before clipping (training.py:128-131) */
   unsigned long long draws;     /* PCG64 doubles consumed by dropout; caller advances its generator */
   int status;                   /* cmt_status of the step */
+  double loss_sum;              /* sum over tokens of per-token loss * mask */
+  double ntok;                  /* token count the loss is averaged over */
 } cmt_step_result;
 
 typedef struct cmt_engine cmt_engine;

@@ -439,6 +439,27 @@ def forward_backward(p, d: Dims, src_ids, src_mask, tgt_ids, tgt_mask, eps, gen=
     return loss, g, aux
 
 
+def dev_entropy(p, d: Dims, batches):
+    """Mean per-token natural-log cross entropy, inference mode, no smoothing
+    (reference training.py:162-182): sum over batches of -(lp_gold * m) in
+    fp32, divided by the token count."""
+    if not batches:
+        raise OracleError("ConfigError", "development set is empty")
+    total, tokens = 0.0, 0.0
+    nmask = 2 * (d.depth - 1) + 1
+    for src, sm, tgt, tm in batches:
+        # identity dropout masks = INFER mode (layers.py:283-290)
+        _, _, aux = forward_backward(p, d, src, sm, tgt, np.ones_like(np.asarray(tm, np.float32)), 0.0,
+                                     masks=[None] * nmask, want_grads=False)
+        lp = log_softmax_cols(aux["logits"])
+        T, B = np.asarray(tgt).shape
+        gold = lp[np.asarray(tgt, np.int64).reshape(T * B), np.arange(T * B)]
+        m = np.asarray(tm, np.float32).reshape(T * B)
+        total += float(-(gold * m).sum())
+        tokens += float(m.sum())
+    return total / tokens
+
+
 def sgd_step(p, g, names, lr, clip):
     """training.py:123-142: global L2 norm (fp32 dots summed in double), clip, update.
 

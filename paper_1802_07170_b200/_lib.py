@@ -27,6 +27,7 @@ MODE_FP32 = 0
 MODE_BF16 = 1
 FLAG_NO_UPDATE = 1
 FLAG_ASYNC = 2
+FLAG_INFER = 4
 
 # every symbol include/cytonmt_b200.h declares
 EXPORTS = [
@@ -53,7 +54,8 @@ class StepArgs(ctypes.Structure):
 
 class StepResult(ctypes.Structure):
     _fields_ = [("loss", ctypes.c_double), ("grad_norm", ctypes.c_double),
-                ("draws", ctypes.c_ulonglong), ("status", ctypes.c_int)]
+                ("draws", ctypes.c_ulonglong), ("status", ctypes.c_int),
+                ("loss_sum", ctypes.c_double), ("ntok", ctypes.c_double)]
 
 
 _lib = None

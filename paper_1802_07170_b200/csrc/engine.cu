@@ -339,6 +339,8 @@ class Engine {
   float* cepart = nullptr;  // per-CTA dY column sums of the fused CE kernel
   float *att_part = nullptr, *att_dsc = nullptr;  // split attention: score slices, d scores
   int att_split = 1;  // option: split attention kernels (many CTAs per sentence)
+  int allow_empty_targets = 0;  // option: stage batches with no unmasked target (dev_entropy)
+  bool last_infer = false;
   float *ux, *ux2, *alpha, *ho, *losstok, *dcst, *dXemb, *dtop, *dhc, *dcc, *colpart;
   std::vector<void*> drop_enc, drop_dec;
   std::vector<uint8_t*> keep_enc, keep_dec;
@@ -696,7 +698,8 @@ class Engine {
     float ntok = 0.f;  // numpy float32 sum of {0,1} masks is exact below 2^24
     for (long long i = 0; i < NT; ++i) ntok += tmask[i];
     ntok_local = ntok;
-    if (!(ntok > 0.f)) throw Error(CMT_ERR_CONFIG, "smoothed_loss needs at least one unmasked token");
+    if (!(ntok > 0.f) && !allow_empty_targets)
+      throw Error(CMT_ERR_CONFIG, "smoothed_loss needs at least one unmasked token");
     ensure_ws(S_, T_, B_);
     // pinned staging: ids (int32) + masks + segments
     size_t nbytes = (size_t)(NS + 2 * NT) * 4 + (size_t)(NS + NT) * 4 + 2 * (size_t)(3 * (NS + NT) + 2) * 4;
@@ -1232,10 +1235,11 @@ class Engine {
   void run(const cmt_step_args& a, cmt_step_result* res) {
     if (!staged) throw Error(CMT_ERR_INTERNAL, "no batch staged");
     const long long NS = (long long)S * B, NT = (long long)T * B, BH = (long long)B * H;
-    const bool drop = cfg.dropout > 0.0;
+    const bool infer = (a.flags & CMT_FLAG_INFER) != 0;  // dev_entropy pass (training.py:162-182)
+    const bool drop = cfg.dropout > 0.0 && !infer;        // INFER mode: dropout is the identity
     Pcg pcg{a.pcg_state_hi, a.pcg_state_lo, a.pcg_inc_hi, a.pcg_inc_lo};
     double ntok = a.global_ntok > 0 ? a.global_ntok : ntok_local;
-    float inv_ntok = (float)(1.0 / (double)(float)ntok);
+    float inv_ntok = ntok > 0 ? (float)(1.0 / (double)(float)ntok) : 0.f;
     CMT_CUDA(cudaMemsetAsync(out_d, 0, sizeof(StepOut), st));
     tl_mark(st, "<start>");
 
@@ -1425,6 +1429,19 @@ class Engine {
     CMT_LAUNCHED(); tl_mark(st, "sum_to_double_kernel");
 
     if (stop_after == 2) { CMT_CUDA(cudaStreamSynchronize(st)); return; }
+    last_infer = infer;
+    if (infer) {  // forward only: loss sum and token count, no backward, no update, no draws
+      CMT_CUDA(cudaGetLastError());
+      CMT_CUDA(cudaMemcpyAsync(out_h, out_d, sizeof(StepOut), cudaMemcpyDeviceToHost, st));
+      last_draws = 0;
+      last_ntok = ntok;
+      if (res) {
+        res->draws = 0;
+        res->status = CMT_OK;
+        if (!(a.flags & CMT_FLAG_ASYNC)) wait(res);
+      }
+      return;
+    }
     // ===== backward =====
     // output projection (layers.py:64-73): dW_o, db_o, dH_o (+ dropout bwd + tanh' of H_o)
     gemm(H, V, (int)NT, Mat{hin, H, 1}, Mat{Y, V, 1}, store(dg + off_wo, V, false));
@@ -1670,8 +1687,11 @@ class Engine {
     CMT_CUDA(cudaStreamSynchronize(st));
     res->draws = last_draws;
     res->loss = (double)((float)out_h->loss_sum / (float)last_ntok);
+    res->loss_sum = out_h->loss_sum;
+    res->ntok = last_ntok;
     res->grad_norm = out_h->scal[1];
     int s = out_h->status;
+    if (last_infer) s &= ~ST_LOSS;  // dev_entropy does not check the loss (training.py:174-181)
     res->status = (s & ST_SCORES) ? CMT_ERR_NUM_SCORES
                 : (s & ST_LOGITS) ? CMT_ERR_NUM_LOGITS
                 : (s & ST_LOSS)   ? CMT_ERR_NUM_LOSS
@@ -1849,6 +1869,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "dual") e->eng->dual = (int)value;
     else if (k == "jump") e->eng->use_jump = (int)value;
     else if (k == "att_split") e->eng->att_split = (int)value;
+    else if (k == "allow_empty_targets") e->eng->allow_empty_targets = (int)value;
     else if (k == "ce2") {
       if (e->eng->staged && (value != 0) != (e->eng->ce2 != 0)) throw Error(cmt::CMT_ERR_CONFIG, "set ce2 before staging");
       e->eng->ce2 = (int)value;

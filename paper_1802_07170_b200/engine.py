@@ -153,12 +153,14 @@ class Engine:
         self._check(self.lib.cmt_stage_batch(self.h, _llptr(src), _fptr(sm), S, _llptr(tgt), _fptr(tm), T, B))
         self.shape = (S, T, B)
 
-    def run(self, lr, clip, eps, rng=None, update=True, global_ntok=0.0, asynchronous=False):
-        """One step on the staged batch.  Advances ``rng`` by the draws used."""
+    def run(self, lr, clip, eps, rng=None, update=True, global_ntok=0.0, asynchronous=False, infer=False):
+        """One step on the staged batch.  Advances ``rng`` by the draws used.
+        ``infer=True``: forward only in INFER mode (no dropout/backward/update)."""
         st = pcg_state(rng) if rng is not None else (0, 0, 0, 1)
         a = _lib.StepArgs(float(lr), float(clip) if clip is not None else -1.0, float(eps),
                           st[0], st[1], st[2], st[3], float(global_ntok),
-                          (0 if update else _lib.FLAG_NO_UPDATE) | (_lib.FLAG_ASYNC if asynchronous else 0))
+                          (0 if update else _lib.FLAG_NO_UPDATE) | (_lib.FLAG_ASYNC if asynchronous else 0)
+                          | (_lib.FLAG_INFER if infer else 0))
         r = _lib.StepResult()
         rc = self.lib.cmt_run_step(self.h, ctypes.byref(a), ctypes.byref(r))
         self.last_draws = r.draws
@@ -189,6 +191,24 @@ class Engine:
             raise
         r = self.run(lr, clip, eps, rng, update)
         return r.loss, r.grad_norm
+
+    def dev_entropy(self, batches):
+        """Mean per-token cross entropy over ``batches`` in INFER mode, no label
+        smoothing (reference training.py:162-182); every batch runs the device
+        forward, only the per-batch loss sum and token count come back."""
+        if not batches:
+            raise ConfigError("development set is empty")
+        total, tokens = 0.0, 0.0
+        self.set_option("allow_empty_targets", 1)
+        try:
+            for batch in batches:
+                self.stage(batch.src_ids, batch.src_mask, batch.tgt_ids, batch.tgt_mask)
+                r = self.run(0.0, None, 0.0, None, update=False, infer=True)
+                total += float(r.loss_sum)
+                tokens += float(r.ntok)
+        finally:
+            self.set_option("allow_empty_targets", 0)
+        return total / tokens
 
     def debug_buffer(self, name, cap=1 << 28):
         out = np.empty(cap, dtype=np.float32)

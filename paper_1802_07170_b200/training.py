@@ -57,6 +57,14 @@ def train_step(model, batch, cfg, lr, rng, *, mode=None, sync=None):
     return loss
 
 
+def dev_entropy(model, dev_batches, *, mode=None):
+    """Drop-in for ``minmt.training.dev_entropy`` (training.py:162-182): mean
+    per-token cross entropy (natural log), INFER mode, no label smoothing,
+    computed by the device forward on the engine bound to ``model`` (device
+    parameters are authoritative, so no host sync is needed)."""
+    return engine_for(model, mode).dev_entropy(dev_batches)
+
+
 def install(training_module=None, sync="lazy"):
     """Patch a reference ``minmt.training`` module to use this engine.
 
@@ -70,19 +78,14 @@ def install(training_module=None, sync="lazy"):
         import minmt.training as training_module  # type: ignore
     DEFAULTS["sync"] = sync
     training_module.train_step = train_step
+    training_module.dev_entropy = dev_entropy  # device forward
     if sync == "lazy":
-        orig_dev = training_module.dev_entropy
         orig_save = training_module.save_checkpoint
-
-        def dev_entropy(model, dev_batches):
-            sync_to_host(model)
-            return orig_dev(model, dev_batches)
 
         def save_checkpoint(path, model, vocab_tokens):
             sync_to_host(model)
             return orig_save(path, model, vocab_tokens)
 
-        training_module.dev_entropy = dev_entropy
         training_module.save_checkpoint = save_checkpoint
         params_cls = None
         try:

@@ -290,3 +290,53 @@ def test_attention_variants_agree(case):
     for n in og:
         assert O.norm_rel_err(out[1][n], out[0][n]) < 1e-3, n
         assert O.norm_rel_err(out[1][n], og[n]) < BF16_TOL, n
+
+
+@pytest.mark.parametrize("mode,tol", [("fp32", FP32_TOL), ("bf16", BF16_TOL)])
+@pytest.mark.parametrize("case", GOLDEN)
+def test_dev_entropy_matches_reference_golden(golden, case, mode, tol):
+    """INFER-mode device forward (dev_entropy, training.py:162-182) against the
+    reference's own value (tests/golden/make_dev_golden.py); dropout draws none."""
+    from paper_1802_07170_b200.engine import Engine
+    from paper_1802_07170_b200.model import Batch
+    from tests.gpu_helpers import cfg_of
+    g = golden(case)
+    dv = golden("dev_entropy")
+    d = dims_of(g)
+    if mode == "bf16" and any(x % 8 for x in (d.vocab, d.emb, d.hidden)):
+        pytest.skip("bf16 mode needs dims that are multiples of 8")
+    names = [str(n) for n in g["names"]]
+    eng = Engine(cfg_of(d), mode=mode)
+    eng.upload({n: g[f"init:{n}"] for n in names})
+    batches = [Batch(g["src"], g["tgt"], g["src_mask"], g["tgt_mask"]),
+               Batch(dv[f"{case}:src2"], dv[f"{case}:tgt2"], dv[f"{case}:sm2"], dv[f"{case}:tm2"])]
+    val = eng.dev_entropy(batches)
+    ref = float(dv[f"{case}:value"])
+    assert abs(val - ref) <= tol * abs(ref), (val, ref)
+    # the pass left the weights alone
+    newp = eng.params()
+    for n in names:
+        assert np.array_equal(newp[n], g[f"init:{n}"].astype(np.float32)), n
+    eng.close()
+
+
+def test_dev_entropy_drop_in_and_empty_batch():
+    """training.dev_entropy (drop-in signature) = oracle on a c-tiny-like model;
+    a batch with no unmasked target contributes nothing; empty list raises."""
+    from paper_1802_07170_b200 import training
+    from paper_1802_07170_b200.errors import ConfigError
+    from paper_1802_07170_b200.model import Batch, Model, ModelConfig, Rng
+    cfg = ModelConfig(256, 64, 256, 2, 0.2)
+    model = Model.new(cfg, Rng(4))
+    d = O.Dims(256, 64, 256, 2, 0.2)
+    b1 = O.synthetic_batch(256, 9, 7, 16, seed=2, ragged=True)
+    b2 = O.synthetic_batch(256, 5, 11, 16, seed=3, ragged=False)
+    params = {b.name: b.var.data.copy() for b in model.params.blocks()}
+    ref = O.dev_entropy(params, d, [b1, b2])
+    src, sm, tgt, tm = b2
+    empty = Batch(src, tgt, sm, np.zeros_like(tm))
+    batches = [Batch(b1[0], b1[2], b1[1], b1[3]), Batch(src, tgt, sm, tm), empty]
+    val = training.dev_entropy(model, batches, mode="bf16")
+    assert abs(val - ref) <= BF16_TOL * ref, (val, ref)
+    with pytest.raises(ConfigError):
+        training.dev_entropy(model, [], mode="bf16")

@@ -144,3 +144,17 @@ def test_sgd_nonfinite_aborts_without_update():
     with pytest.raises(O.OracleError):
         O.sgd_step(p, g, ["w"], 1.0, None)
     assert p["w"][0, 0] == 1.0
+
+
+@pytest.mark.parametrize("case", SMALL)
+def test_oracle_dev_entropy_matches_reference(golden, case):
+    """dev_entropy (training.py:162-182) against values produced by the real
+    reference (tests/golden/make_dev_golden.py)."""
+    g = golden(case)
+    dv = golden("dev_entropy")
+    names = [str(n) for n in g["names"]]
+    params = {n: g[f"init:{n}"].copy() for n in names}
+    batches = [(g["src"], g["src_mask"], g["tgt"], g["tgt_mask"]),
+               (dv[f"{case}:src2"], dv[f"{case}:sm2"], dv[f"{case}:tgt2"], dv[f"{case}:tm2"])]
+    val = O.dev_entropy(params, dims_of(g), batches)
+    assert abs(val - float(dv[f"{case}:value"])) <= 1e-6 * abs(float(dv[f"{case}:value"]))
