@@ -172,8 +172,8 @@ static void launch_tc_impl(cudaStream_t st, int M, int N, int K, Mat A, Mat B, c
   else make_map(&tb, B.p, Kx, N, B.ld, tc::BK, C::BNC);
   if constexpr (ST) make_map_c(&tcm, e.C, N, M, e.ldc, e.c_bf16 != 0);
   else tcm = ta;
-  int tiles = ceil_div(M, C::TILE_M) * ceil_div(N, BN) * ks;
-  int grid = CG * std::min(tiles, g_num_sms / CG);
+  int tiles = ceil_div(M, C::TILE_M) * ceil_div(N, BN) * (ks > 0 ? ks : 1);
+  int grid = ks > 0 ? CG * std::min(tiles, g_num_sms / CG) : CG * (g_num_sms / CG);
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3(grid);
   c.blockDim = dim3(tc::NUM_THREADS);
@@ -195,17 +195,28 @@ static int g_tma_store = 1;  // option: TMA-store epilogue for EpiStore GEMMs
 static int g_splitk = 1;  // option: split-K (TMA reduce-add) for linear fp32 epilogues
 // K slices for a linear fp32 EpiStore GEMM whose tile count leaves CTA pairs
 // idle in the last wave: minimise waves(tiles * ks) / ks (+ a per-slice cost).
+// Returns 1 (no split), 2 (two K slices per tile) or -1 (stream-K).  At most
+// two pieces of a tile ever meet in C (zeroed first), and fp32 addition is
+// commutative, so the result does not depend on which piece lands first.
 static int pick_ks(int M, int N, int K, int BN, int CG) {
   if (!g_splitk) return 1;
   const long long tiles = (long long)ceil_div(M, 128 * CG) * ceil_div(N, BN);
   const long long units = g_num_sms / CG;
   const int nkb = ceil_div(K, 64);
+  double t1 = (double)((tiles + units - 1) / units);  // in whole-tile times
   int best = 1;
-  double best_t = (double)((tiles + units - 1) / units);
-  for (int ks = 2; ks <= 4; ++ks) {
-    if (nkb / ks < 16) break;
-    double t = (double)((tiles * ks + units - 1) / units) / ks + 0.04 * (ks - 1);
-    if (t < best_t * 0.95) { best = ks; best_t = t; }
+  double best_t = t1;
+  if (nkb >= 32) {
+    double t2 = (double)((tiles * 2 + units - 1) / units) / 2 + 0.04;
+    if (t2 < best_t * 0.95) { best = 2; best_t = t2; }
+  }
+  // owner/helper stream-K (GemmWork): tiles < units, every tile in two pieces.
+  // Off by default (g_splitk & 2): each helper piece pays a full-tile epilogue
+  // (TMEM drain + reduce-add), which made the c3 dW GEMMs slower (68 vs 48 us).
+  if ((g_splitk & 2) && tiles < units && nkb >= 32) {
+    const long long nh = units - tiles, tph = (tiles + nh - 1) / nh;
+    double ts = (double)tph / (tph + 1) + 0.04;
+    if (ts < best_t * 0.95) { best = -1; best_t = ts; }
   }
   return best;
 }
@@ -215,8 +226,10 @@ static void launch_tc(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const 
   if constexpr (std::is_same<Epi, EpiStore>::value) {
     if (g_tma_store && c_map_ok(e.C, e.ldc, e.c_bf16 != 0) && !(e.beta && e.c_bf16)) {
       int ks = 1;
-      if (!e.c_bf16 && !e.bias && e.act == 0 && !e.add) ks = pick_ks(M, N, K, BN, CG);
-      if (ks > 1 && !e.beta) {  // slices reduce-add into a zeroed C
+      // split / stream-K only into a zeroed C (accumulating epilogues would add
+      // 2 pieces onto existing values in a timing-dependent order)
+      if (!e.c_bf16 && !e.bias && e.act == 0 && !e.add && !e.beta) ks = pick_ks(M, N, K, BN, CG);
+      if (ks != 1) {  // pieces reduce-add into a zeroed C
         if (e.ldc == N) CMT_CUDA(cudaMemsetAsync(e.C, 0, (size_t)M * N * 4, st));
         else CMT_CUDA(cudaMemset2DAsync(e.C, (size_t)e.ldc * 4, 0, (size_t)N * 4, M, st));
       }

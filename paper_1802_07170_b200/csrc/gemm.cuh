@@ -317,6 +317,58 @@ struct Cfg {
 };
 }  // namespace tc
 
+// Work distribution of the persistent GEMM.  ks >= 1: unit u takes work items
+// u, u+nunits, ... where item w = (tile w / ks, K slice w % ks).  ks == -1
+// (owner/helper stream-K, for tiles < units): unit t < tiles owns k-blocks
+// [0, a) of tile t; the nunits - tiles helper units each take the tails
+// [a, num_kb) of tph consecutive tiles, with a chosen so owners and helpers
+// carry equal k-block loads.  Every tile then has exactly two pieces, both
+// TMA-reduce-added into a zeroed C (order-independent: fp32 + commutes).
+// Each role (TMA, MMA, epilogue) walks the same sequence.
+struct GemmWork {
+  int tile, kb0, nk;
+  int w, step, end, ks, num_kb, a;
+  bool helper;
+  CMT_D GemmWork(int unit, int nunits, int num_tiles, int ks_, int num_kb_) {
+    ks = ks_;
+    num_kb = num_kb_;
+    helper = false;
+    if (ks_ < 0) {
+      const int nh = nunits - num_tiles;  // > 0 (host guarantees tiles < units)
+      const int tph = (num_tiles + nh - 1) / nh;
+      a = num_kb_ * tph / (tph + 1);
+      if (unit < num_tiles) {
+        w = unit; end = unit + 1; step = 1;
+      } else {
+        helper = true;
+        w = (unit - num_tiles) * tph;
+        end = min(num_tiles, w + tph);
+        step = 1;
+      }
+    } else {
+      w = unit;
+      step = nunits;
+      end = num_tiles * ks_;
+      a = 0;
+    }
+  }
+  CMT_D bool next() {
+    if (w >= end) return false;
+    if (ks < 0) {
+      tile = w;
+      kb0 = helper ? a : 0;
+      nk = helper ? num_kb - a : a;
+    } else {
+      tile = w / ks;
+      const int sp = w % ks;
+      kb0 = sp * num_kb / ks;
+      nk = (sp + 1) * num_kb / ks - kb0;
+    }
+    w += step;
+    return true;
+  }
+};
+
 // ST = 1 (EpiStore only): the epilogue stages each warp's 32x32 result block
 // in 128B/64B-swizzled smem and writes it with a TMA store (or a TMA
 // reduce-add for beta) instead of per-row global stores.
@@ -348,8 +400,6 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
   const int num_kb = (K + tc::BK - 1) / tc::BK;
   // split-K (ST only, linear epilogues): work unit w -> tile w / ks, K slice w % ks;
   // every slice reduce-adds its partial tile into C
-  const int num_work = num_tiles * ks;
-  auto kb_lo = [&](int sp) { return sp * num_kb / ks; };
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -380,13 +430,14 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
       // ===== TMA producer (both CTAs of a pair load their own halves) =====
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = unit; w < num_work; w += nunits) {
-        const int tile = w / ks, sp = w % ks;
+      GemmWork wk(unit, nunits, num_tiles, ks, num_kb);
+      while (wk.next()) {
+        const int tile = wk.tile;
         const int tm_ = (opt & 2) ? tile / tiles_n : tile % tiles_m;
         const int tn_ = (opt & 2) ? tile % tiles_n : tile / tiles_m;
         const int m0 = tm_ * C::TILE_M + (int)rank * tc::BM;
         const int n0 = tn_ * BN + (int)rank * C::BNC;
-        const int kbl = kb_lo(sp), nk = kb_lo(sp + 1) - kbl;
+        const int kbl = wk.kb0, nk = wk.nk;
         for (int kk_ = 0; kk_ < nk; ++kk_) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * C::A_BYTES;
@@ -437,8 +488,9 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int iter = 0;
-      for (int w = unit; w < num_work; w += nunits, ++iter) {
-        const int nk = kb_lo(w % ks + 1) - kb_lo(w % ks);
+      GemmWork wk(unit, nunits, num_tiles, ks, num_kb);
+      for (; wk.next(); ++iter) {
+        const int nk = wk.nk;
         const int buf = iter & 1;
         const uint32_t aphase = (iter >> 1) & 1;
         ptx::mbar_wait(&tempty[buf], aphase ^ 1);
@@ -479,8 +531,9 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
     uint8_t* stg_w = stg + (warp - 4) * 2 * tc::STG_BYTES;
     uint32_t sc = 0;  // staged chunks (buffer parity)
     int iter = 0;
-    for (int w = unit; w < num_work; w += nunits, ++iter) {
-      const int tile = w / ks;
+    GemmWork wk(unit, nunits, num_tiles, ks, num_kb);
+    for (; wk.next(); ++iter) {
+      const int tile = wk.tile;
       const int tm_ = (opt & 2) ? tile / tiles_n : tile % tiles_m;
       const int tn_ = (opt & 2) ? tile % tiles_n : tile / tiles_m;
       const int m0 = tm_ * C::TILE_M + (int)rank * tc::BM;
@@ -541,7 +594,7 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              if (epi.beta || ks > 1) ptx::tma_reduce_add_2d(&tmC, sb, nc, mw);
+              if (epi.beta || ks != 1) ptx::tma_reduce_add_2d(&tmC, sb, nc, mw);
               else ptx::tma_store_2d(&tmC, sb, nc, mw);
               ptx::bulk_commit();
             }

@@ -518,7 +518,7 @@ __global__ void sum_to_double_kernel(const float* __restrict__ x, int n, double*
 // logits are in [-1, 1] and the sum of exponentials needs no max shift.
 // Same math as ce_kernel (training.py:96-120, tensor.py:146-151).
 // ---------------------------------------------------------------------------
-constexpr int CE2_THREADS = 512;
+constexpr int CE2_THREADS = 1024;
 constexpr int CE2_MAXV = 55 * 1024;  // smem column sums (fp32)
 constexpr int CE2_UNROLL = 4;        // 16-byte loads in flight per thread
 __global__ void __launch_bounds__(CE2_THREADS, 1)

@@ -102,3 +102,18 @@ def test_tcgen05_gemm_split_k(beta, bn):
     slices TMA-reduce-add into C (zeroed first unless accumulating)."""
     C, ref = _gemm(_lib.MODE_BF16, 6400, 1024, 4096, 0, 0, bn, beta=beta, seed=5)
     assert (C - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+
+
+def test_tcgen05_gemm_stream_k_deterministic():
+    """dW-shaped GEMM (M=1024, N=4096, K=6400: 64 pair tiles < 74 pairs) with
+    owner/helper stream-K enabled (two pieces per tile reduce-added into zeroed
+    C): correct and bit-identical across runs."""
+    lib = _lib.load()
+    assert lib.cmt_set_option(None, b"splitk", 3) == 0
+    try:
+        C1, ref = _gemm(_lib.MODE_BF16, 1024, 4096, 6400, 1, 1, 257, seed=9)
+        assert (C1 - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+        C2, _ = _gemm(_lib.MODE_BF16, 1024, 4096, 6400, 1, 1, 257, seed=9)
+        assert torch.equal(C1, C2)
+    finally:
+        assert lib.cmt_set_option(None, b"splitk", 1) == 0
