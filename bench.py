@@ -73,10 +73,19 @@ class ClockSampler:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+
+    def mark(self):
+        """Start of the timed region: samples before this point are dropped."""
+        self.f.flush()
+        try:
+            with open(self.f.name) as fh:
+                self.skip = sum(1 for _ in fh)
+        except OSError:
+            self.skip = 0
 
     def stop(self):
         if self.p is None:
@@ -85,6 +94,7 @@ class ClockSampler:
         self.p.wait()
         self.f.seek(0)
         rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        rows = rows[getattr(self, "skip", 0):]
         os.unlink(self.f.name)
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -147,7 +157,7 @@ def run_reference(args, cfg_t):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=list(CONFIGS))
@@ -198,6 +208,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize(local)
     clocks = ClockSampler(local)
+    time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
+    clocks.mark()
     eng.set_option("time_dominant", 1)
     l0 = launch_count()
     eng.record(0)
