@@ -350,6 +350,7 @@ class Engine {
   float *src_mask_d, *tgt_mask_d;
   void *Xs, *Xt, *top, *u_att, *cst_att, *hod, *Y, *dhpre, *du_att, *dU, *dU2;
   float* cepart = nullptr;  // per-CTA dY column sums of the fused CE kernel
+  float* dho32 = nullptr;   // fp32 split-K scratch of dH_o (bf16 mode)
   float *att_part = nullptr, *att_dsc = nullptr;  // split attention: score slices, d scores
   int att_split = 1;  // option: split attention kernels (many CTAs per sentence)
   int allow_empty_targets = 0;  // option: stage batches with no unmasked target (dev_entropy)
@@ -647,6 +648,7 @@ class Engine {
     Y = carve<char>(cur, NT * (long long)V * asz);
     losstok = carve<float>(cur, NT * 4);
     dhpre = carve<char>(cur, NT * H * asz);
+    dho32 = bf ? carve<float>(cur, NT * H * 4) : nullptr;
     dcst = carve<float>(cur, NT * 2 * H * 4);
     du_att = carve<char>(cur, NT * H * asz);
     dXemb = carve<float>(cur, (NS + NT) * E * 4);
@@ -1460,10 +1462,19 @@ class Engine {
     gemm(H, V, (int)NT, Mat{hin, H, 1}, Mat{Y, V, 1}, store(dg + off_wo, V, false));
     if (!fused_ce) colsum(Y, true, NT, V, dg + off_bo);
     {
-      EpiStore e = store(dhpre, H, true);
+      // dH_o = dY W_o^T with the dropout mask and tanh' of H_o applied (linear, so
+      // they may act per K slice).  bf16 mode: K = V is long and the 100 output
+      // tiles leave pairs idle, so the product is split-K into an fp32 scratch
+      // and converted to the bf16 activation afterwards.
+      const bool via32 = bf && dho32 && pick_ks((int)NT, H, V, 256, 2) != 1;
+      EpiStore e = via32 ? store(dho32, H, false) : store(dhpre, H, true);
       if (drop) { e.dmask = keep_o; e.ld_dmask = H; e.dscale = 1.0f / (float)(1.0 - cfg.dropout); }
       e.tgrad_y = ho; e.ld_tgrad = H;
       gemm((int)NT, H, V, Mat{Y, V, 0}, Mat{wv(off_wo), V, 0}, e);
+      if (via32) {
+        copy2d_kernel<float, bf16><<<grid_for(NT * H), 256, 0, st>>>(dho32, H, (bf16*)dhpre, H, (int)NT, H);
+        CMT_LAUNCHED(); tl_mark(st, "copy2d_kernel");
+      }
     }
     // W_c (attention.py:171)
     gemm(2 * H, H, (int)NT, Mat{cst_att, 2LL * H, 1}, Mat{dhpre, H, 1}, store(dg + off_wc, H, false));
