@@ -668,12 +668,27 @@ __global__ void sumsq_partial_kernel(const float* __restrict__ g, long long n, d
   __shared__ double red[32];
   float a = 0.f;
   double ad = 0.0;
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int cnt = 0;
-  for (; i < n; i += (long long)gridDim.x * blockDim.x) {
-    float v = g[i];
-    a = fmaf(v, v, a);
-    if (++cnt == 256) { ad += a; a = 0.f; cnt = 0; }
+  if ((((uintptr_t)g) & 15) == 0) {
+    const long long n4 = n >> 2;
+    const float4* g4 = (const float4*)g;
+    for (long long i = tid; i < n4; i += stride) {
+      const float4 v = g4[i];
+      a = fmaf(v.x, v.x, a);
+      a = fmaf(v.y, v.y, a);
+      a = fmaf(v.z, v.z, a);
+      a = fmaf(v.w, v.w, a);
+      if (++cnt == 64) { ad += a; a = 0.f; cnt = 0; }
+    }
+    for (long long i = 4 * n4 + tid; i < n; i += stride) a = fmaf(g[i], g[i], a);
+  } else {
+    for (long long i = tid; i < n; i += stride) {
+      float v = g[i];
+      a = fmaf(v, v, a);
+      if (++cnt == 256) { ad += a; a = 0.f; cnt = 0; }
+    }
   }
   ad += a;
   ad = warp_sumd(ad);
@@ -707,7 +722,27 @@ __global__ void sgd_dense_kernel(float* __restrict__ w, const float* __restrict_
                                  long long n, const float* __restrict__ s32, const int* __restrict__ status) {
   if (*status & ST_ABORT) return;
   const float s = *s32;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // 16-byte vectors over the (256-byte aligned) arena, scalar tail
+  const long long n4 = n >> 2;
+  float4* w4 = (float4*)w;
+  const float4* g4 = (const float4*)g;
+  for (long long i = tid; i < n4; i += stride) {
+    const float4 wv = w4[i], gv = __ldcs(g4 + i);
+    float4 nw;
+    nw.x = __fsub_rn(wv.x, __fmul_rn(s, gv.x));
+    nw.y = __fsub_rn(wv.y, __fmul_rn(s, gv.y));
+    nw.z = __fsub_rn(wv.z, __fmul_rn(s, gv.z));
+    nw.w = __fsub_rn(wv.w, __fmul_rn(s, gv.w));
+    w4[i] = nw;
+    if (shadow) {
+      __align__(8) bf16 b4[4] = {__float2bfloat16_rn(nw.x), __float2bfloat16_rn(nw.y), __float2bfloat16_rn(nw.z),
+                                 __float2bfloat16_rn(nw.w)};
+      *(uint2*)(shadow + 4 * i) = *(uint2*)b4;
+    }
+  }
+  for (long long i = 4 * n4 + tid; i < n; i += stride) {
     float nw = __fsub_rn(w[i], __fmul_rn(s, g[i]));
     w[i] = nw;
     if (shadow) shadow[i] = __float2bfloat16_rn(nw);
