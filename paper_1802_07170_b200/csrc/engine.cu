@@ -1086,17 +1086,22 @@ class Engine {
     const uint8_t* dx_keep;
     void* dUb;
   };
-  bool use_dual_bwd() const {
+  template <int ROWS>
+  bool bwd_multi_ok() const {
+    using F = mc::Bwd<ROWS>;
     return bf && persistent && dual && H % mc::BWD_NU == 0 && (H / 64) % mc::BWD_KBOX == 0 && H / 64 <= 32 &&
-           4 * H / 64 <= FLAG_STRIDE && B <= 128 &&
-           2 * mc::bwd_ctas(H) <= g_num_sms &&
-           mc::bwd_stages(H) >= 1 && (size_t)mc::bwd_stages(H) * mc::STAGE_BYTES >= (size_t)128 * mc::XROW;
+           (4 * H / 64) * ((B + ROWS - 1) / ROWS) <= FLAG_STRIDE && B <= 128 && F::stages(H) >= 2 &&
+           (size_t)F::stages(H) * F::STAGE >= F::xbuf_bytes();
   }
+  bool use_dual_bwd() const { return bwd_multi_ok<128>() && 2 * mc::Bwd<128>::ctas(H, B) <= g_num_sms; }
+  // one scan over two batch halves through lstm_bwd_multi<64> (128 CTAs at H=1024)
+  bool use_multi_single_bwd() const { return bwd_multi_ok<64>() && mc::Bwd<64>::ctas(H, B) <= g_num_sms; }
+  template <int ROWS>
   LstmBwdP bwd_params(const BwdScan& f, CUtensorMap* tmA, CUtensorMap* tmW) {
     const Layer& ly = layers[f.l];
     ScanViews v = views(f.l, f.reverse);
     long long N = (long long)f.steps * B;
-    make_map_kblocks(tmA, f.dUb, N, 4LL * H, 4LL * H, 128, mc::BWD_KBOX);
+    make_map_kblocks(tmA, f.dUb, N, 4LL * H, 4LL * H, ROWS, mc::BWD_KBOX);
     make_map(tmW, wv(ly.w_off), 4LL * H, f.din + H, 4LL * H, 64, mc::BWD_NU);
     LstmBwdP prm;
     prm.dy = f.dy; prm.acts = lw[f.l].acts; prm.tcache = lw[f.l].tc; prm.cprev = v.cprev; prm.mask = f.mask;
@@ -1104,22 +1109,24 @@ class Engine {
     prm.flag = flags + (32 + (f.l & 31)) * FLAG_STRIDE;
     prm.steps = f.steps; prm.B = B; prm.H = H; prm.din = f.din; prm.reverse = f.reverse ? 1 : 0;
     prm.trace = (trace_layer == 100 + f.l) ? trace_d : nullptr;
-    prm.stages = mc::bwd_stages(H);
+    prm.stages = mc::Bwd<ROWS>::stages(H);
     CMT_CUDA(cudaMemsetAsync(prm.flag, 0, FLAG_STRIDE * 4, st));
     return prm;
   }
-  void bwd_pair(const BwdScan& a, const BwdScan& b) {
+  template <int ROWS>
+  void bwd_launch(const BwdScan& a, const BwdScan* b) {
     CUtensorMap tm[4];
     LstmBwdMulti m;
-    m.c[0] = bwd_params(a, &tm[0], &tm[1]);
-    m.c[1] = bwd_params(b, &tm[2], &tm[3]);
-    const int g = mc::bwd_ctas(H);
+    m.c[0] = bwd_params<ROWS>(a, &tm[0], &tm[1]);
+    if (b) m.c[1] = bwd_params<ROWS>(*b, &tm[2], &tm[3]);
+    else { m.c[1] = m.c[0]; tm[2] = tm[0]; tm[3] = tm[1]; }
+    const int g = mc::Bwd<ROWS>::ctas(H, B);
     m.split = g;
-    auto k = lstm_bwd_multi;
-    const size_t smem = mc::bwd_smem(H);
+    auto k = lstm_bwd_multi<ROWS>;
+    const size_t smem = mc::Bwd<ROWS>::smem(H);
     CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t c = {};
-    c.gridDim = dim3(2 * g);
+    c.gridDim = dim3(b ? 2 * g : g);
     c.blockDim = dim3(mc::BWD_THREADS);
     c.dynamicSmemBytes = smem;
     c.stream = st;
@@ -1134,8 +1141,9 @@ class Engine {
     c.numAttrs = 2;
     CMT_CUDA(cudaLaunchKernelEx(&c, k, tm[0], tm[1], tm[2], tm[3], m));
     CMT_LAUNCHED();
-    tl_mark(st, "lstm_bwd_pair");
+    tl_mark(st, b ? "lstm_bwd_pair" : "lstm_bwd_single");
   }
+  void bwd_pair(const BwdScan& a, const BwdScan& b) { bwd_launch<128>(a, &b); }
   // weight grads, bias grads and input grads of a finished BPTT scan
   void bwd_post(const BwdScan& f) {
     const Layer& ly = layers[f.l];
@@ -1567,7 +1575,13 @@ class Engine {
     };
     if (use_dual_bwd()) {
       // pairs of independent scans: dL alone, then (d(k), e(k+1)) for k = L-1..1, then (e1 bwd, e1 fwd)
-      single(dec_scan(L, dU));
+      if (use_multi_single_bwd()) {
+        BwdScan dL = dec_scan(L, dU);
+        bwd_launch<64>(dL, nullptr);
+        bwd_post(dL);
+      } else {
+        single(dec_scan(L, dU));
+      }
       for (int k = L - 1; k >= 1; --k) {
         BwdScan d = dec_scan(k, dU), e = enc_scan(k + 1, dU2);
         bwd_pair(d, e);

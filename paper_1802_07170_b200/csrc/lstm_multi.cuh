@@ -276,19 +276,24 @@ constexpr int BWD_THREADS = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-
 constexpr int BWD_KS = 4;         // cluster size = K quarters of the 4H gate columns
 constexpr int BWD_NU = 64;        // units per cluster
 constexpr int BWD_UPT = 8;        // units per epilogue thread
-constexpr int BWD_KBLK = 128 * 128;  // [128 rows][64] bf16
-constexpr int BWD_KBOX = STAGE_BYTES / BWD_KBLK;
-constexpr int XROW = BWD_NU * 4;     // bytes of one row of parked partials
+constexpr int BWD_KBOX = 2;       // k-blocks per TMA / stage
 inline size_t bwd_w_bytes(int H) { return (size_t)(H / 64) * BWD_NU * 128; }
-inline int bwd_stages(int H) {
-  long long room = (long long)SMEM_LIMIT - 1024 - 512 - (long long)bwd_w_bytes(H);
-  long long s = room / STAGE_BYTES;
-  return (int)(s > MAX_STAGES ? MAX_STAGES : s);
-}
-inline size_t bwd_smem(int H) { return 1024 + bwd_w_bytes(H) + (size_t)bwd_stages(H) * STAGE_BYTES + 512; }
-inline int bwd_ctas(int H) { return (H / BWD_NU) * BWD_KS; }
-// parked partial of (row b, 16-byte chunk c) at a swizzled offset (conflict-free 16 B stores)
-CMT_D uint32_t xoff(int b, int c) { return (uint32_t)(b * XROW + ((c ^ (b & 15)) << 4)); }
+// ROWS = batch rows per CTA: 128 (paired scans) or 64 (one scan split over two
+// batch halves, 128 CTAs; the M=128 MMA reads a padding tile past the stage).
+template <int ROWS>
+struct Bwd {
+  static constexpr int KBLK = ROWS * 128;  // [ROWS rows][64] bf16
+  static constexpr int STAGE = BWD_KBOX * KBLK;
+  static constexpr int PAD = ROWS < 128 ? KBLK : 0;
+  static int stages(int H) {
+    long long room = (long long)SMEM_LIMIT - 1024 - 512 - PAD - (long long)bwd_w_bytes(H);
+    long long s = room / STAGE;
+    return (int)(s > MAX_STAGES ? MAX_STAGES : s);
+  }
+  static size_t smem(int H) { return 1024 + bwd_w_bytes(H) + (size_t)stages(H) * STAGE + PAD + 512; }
+  static int ctas(int H, int B) { return (H / BWD_NU) * BWD_KS * ((B + ROWS - 1) / ROWS); }
+  static size_t xbuf_bytes() { return (size_t)BWD_KS * 2 * ROWS * 32; }
+};
 }  // namespace mc
 
 struct LstmBwdMulti {
@@ -296,10 +301,12 @@ struct LstmBwdMulti {
   int split;  // multiple of BWD_KS
 };
 
+template <int ROWS>
 __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
     lstm_bwd_multi(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmW0,
                    const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmW1,
                    const LstmBwdMulti m) {
+  using F = mc::Bwd<ROWS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int ch = (int)blockIdx.x >= m.split ? 1 : 0;
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
   const int KBL = p.H / 64;  // k-blocks of this CTA's gate-column quarter
   uint8_t* sW = smem;                                    // KBL x [64 units][64] (K-major)
   uint8_t* sA = smem + (size_t)KBL * (mc::BWD_NU * 128);  // stage ring; also the parked partials
-  uint64_t* full = (uint64_t*)(sA + (size_t)p.stages * mc::STAGE_BYTES);
+  uint64_t* full = (uint64_t*)(sA + (size_t)p.stages * F::STAGE + F::PAD);
   uint64_t* empty = full + mc::MAX_STAGES;
   uint64_t* wfull = empty + mc::MAX_STAGES;
   uint64_t* tfull = wfull + 1;
@@ -323,7 +330,10 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kq = (int)ptx::cluster_rank();
-  const int ug = (bid / mc::BWD_KS) * mc::BWD_NU;  // cluster's first unit
+  const int nh = (p.B + ROWS - 1) / ROWS;
+  const int half = (bid / mc::BWD_KS) % nh;                  // batch half of this cluster
+  const int ug = (bid / mc::BWD_KS / nh) * mc::BWD_NU;       // cluster's first unit
+  const int r0 = half * ROWS;
   const int kb_base = kq * KBL;
   const int rounds = p.steps + (p.dh0 ? 1 : 0);
   auto time_of = [&](int pos) { return p.reverse ? p.steps - 1 - pos : pos; };
@@ -362,11 +372,11 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
     const int nst = KBL / mc::BWD_KBOX;
     for (int i = 1; i < rounds; ++i) {
       if (p.trace && bid == 0 && lane == 0) p.trace[i * 8 + 0] = gtimer();
-      const int arow = time_of(p.steps - i) * p.B;
+      const int arow = time_of(p.steps - i) * p.B + r0;
       const unsigned target = (unsigned)i;
       int issued = 0;
       while (issued < nst) {
-        const bool ok = lane >= KBL || ptx::ld_acquire(p.flag + kb_base + lane) >= target;
+        const bool ok = lane >= KBL || ptx::ld_acquire(p.flag + (kb_base + lane) * nh + half) >= target;
         const unsigned ready = __ballot_sync(0xffffffffu, ok);
         __syncwarp();
         if (lane == 0) {
@@ -376,9 +386,8 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
             const unsigned need = ((1u << mc::BWD_KBOX) - 1u) << (issued * mc::BWD_KBOX);
             if ((ready & need) != need) break;
             ptx::mbar_wait(&empty[stage], phase ^ 1);
-            ptx::tma_load_3d(tmA, &full[stage], sA + stage * mc::STAGE_BYTES, 0, arow,
-                             kb_base + issued * mc::BWD_KBOX);
-            ptx::mbar_expect_tx(&full[stage], mc::STAGE_BYTES);
+            ptx::tma_load_3d(tmA, &full[stage], sA + stage * F::STAGE, 0, arow, kb_base + issued * mc::BWD_KBOX);
+            ptx::mbar_expect_tx(&full[stage], F::STAGE);
             if (++stage == p.stages) { stage = 0; phase ^= 1; }
             ++issued;
           }
@@ -399,12 +408,12 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
         for (int kb0 = 0; kb0 < KBL; kb0 += mc::BWD_KBOX) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a0 = ptx::smem_u32(sA + stage * mc::STAGE_BYTES);
+          const uint32_t a0 = ptx::smem_u32(sA + stage * F::STAGE);
 #pragma unroll
           for (int j = 0; j < mc::BWD_KBOX; ++j) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-              uint64_t ad = ptx::smem_desc_sw128(a0 + j * mc::BWD_KBLK + kk * 32, 16, 1024);
+              uint64_t ad = ptx::smem_desc_sw128(a0 + j * F::KBLK + kk * 32, 16, 1024);
               uint64_t bd = ptx::smem_desc_sw128(wbase + (kb0 + j) * (mc::BWD_NU * 128) + kk * 32, 16, 1024);
               ptx::umma_bf16(tmem, ad, bd, idesc, (kb0 | j | kk) ? 1u : 0u);
             }
@@ -418,12 +427,14 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
   } else if (warp >= 4) {
     const int q = warp & 3;
     const int uh = (warp - 4) >> 2;  // unit half of this CTA's 16 units
-    const int b = q * 32 + lane;
-    const bool valid = b < p.B;
+    const int b = q * 32 + lane;               // row within this CTA's batch slice
+    const bool inrow = b < ROWS;
+    const bool valid = inrow && r0 + b < p.B;
+    const long long gb = r0 + b;                // batch column
     const long long H = p.H;
     const int u0 = ug + kq * 16 + uh * 8;  // my 8 units
     // partials parked in the receiver's stage ring: xbuf[sender][uh][row][8] floats
-    const uint32_t xslot = ptx::smem_u32(sA) + (uint32_t)((kq * 2 + uh) * 128 + b) * 32;  // my slot in a receiver
+    const uint32_t xslot = ptx::smem_u32(sA) + (uint32_t)((kq * 2 + uh) * ROWS + (inrow ? b : 0)) * 32;
     uint32_t rx[mc::BWD_KS], rxf[mc::BWD_KS], rrf[mc::BWD_KS];
 #pragma unroll
     for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
@@ -434,13 +445,13 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
     float dhc[mc::BWD_UPT], dc[mc::BWD_UPT];
 #pragma unroll
     for (int u = 0; u < mc::BWD_UPT; ++u) {
-      dhc[u] = (valid && p.dh_final) ? p.dh_final[(long long)b * H + u0 + u] : 0.f;
-      dc[u] = (valid && p.dc_final) ? p.dc_final[(long long)b * H + u0 + u] : 0.f;
+      dhc[u] = (valid && p.dh_final) ? p.dh_final[gb * H + u0 + u] : 0.f;
+      dc[u] = (valid && p.dc_final) ? p.dc_final[gb * H + u0 + u] : 0.f;
     }
     for (int i = 0; i < rounds; ++i) {
       const bool cell = i < p.steps;
       const int t = cell ? time_of(p.steps - 1 - i) : 0;
-      const long long row = (long long)t * p.B + b;
+      const long long row = (long long)t * p.B + gb;
       float4 dy4[2], tc4[2], cp4[2], a4[mc::BWD_UPT];
       float mk = 1.f;
       if (valid && cell) {
@@ -474,7 +485,7 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
         if (lane == 0) ptx::mbar_arrive(tempty);
         // my MMA is done: my ring may now receive the partners' partials
         if (threadIdx.x == 128) {
-          ptx::mbar_expect_tx(xfull, (mc::BWD_KS - 1) * 2 * 128 * 32);
+          ptx::mbar_expect_tx(xfull, (mc::BWD_KS - 1) * 2 * ROWS * 32);
 #pragma unroll
           for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_)
             if (pr_ != kq) ptx::mbar_arrive_remote_relaxed(rrf[pr_]);
@@ -489,15 +500,15 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
         ptx::mbar_wait_cluster(rfree, (i - 1) & 1);
 #pragma unroll
         for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
-          if (pr_ == kq) continue;
+          if (pr_ == kq || !inrow) continue;
           ptx::st_async_v4(rx[pr_], v[pr_][0], v[pr_][1], v[pr_][2], v[pr_][3], rxf[pr_]);
           ptx::st_async_v4(rx[pr_] + 16, v[pr_][4], v[pr_][5], v[pr_][6], v[pr_][7], rxf[pr_]);
         }
         ptx::mbar_wait_cluster(xfull, (i - 1) & 1);
 #pragma unroll
         for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
-          if (pr_ == kq) continue;
-          const float4* xr = (const float4*)(sA + ((pr_ * 2 + uh) * 128 + b) * 32);
+          if (pr_ == kq || !inrow) continue;
+          const float4* xr = (const float4*)(sA + ((pr_ * 2 + uh) * ROWS + b) * 32);
           const float4 z0 = xr[0], z1 = xr[1];
           acc[0] += z0.x; acc[1] += z0.y; acc[2] += z0.z; acc[3] += z0.w;
           acc[4] += z1.x; acc[5] += z1.y; acc[6] += z1.z; acc[7] += z1.w;
@@ -541,15 +552,16 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
         } else {
 #pragma unroll
           for (int u = 0; u < mc::BWD_UPT; ++u) {
-            p.dh0[(long long)b * H + u0 + u] = acc[u] + dhc[u];
-            p.dc0[(long long)b * H + u0 + u] = dc[u];
+            p.dh0[gb * H + u0 + u] = acc[u] + dhc[u];
+            p.dc0[gb * H + u0 + u] = dc[u];
           }
         }
       }
       if (p.trace && bid == 0 && threadIdx.x == 128) p.trace[i * 8 + 3] = gtimer();
       ptx::named_bar_sync(1, 256);
       if (threadIdx.x == 128) {
-        ptx::red_release_add(p.flag + ((ug + kq * 16) >> 4), 1u);  // my k-block: gate columns 4*(ug+16kq) ..
+        // my k-block (gate columns 4*(ug+16kq) ..) of this batch half
+        ptx::red_release_add(p.flag + ((ug + kq * 16) >> 4) * nh + half, 1u);
         if (p.trace && bid == 0) p.trace[i * 8 + 4] = gtimer();
       }
     }
