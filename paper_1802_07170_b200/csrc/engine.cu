@@ -366,6 +366,7 @@ class Engine {
   int* uniq_d[2];
   float* gcomp[2];
   int nuniq[2] = {0, 0};
+  std::vector<unsigned long long> sort_tmp;  // radix-sort scratch of the segment builder
   int nseg_pos[2] = {0, 0};
   double* normpart;
   unsigned* flags;
@@ -738,15 +739,28 @@ class Engine {
     CMT_CUDA(cudaMemcpyAsync(tgt_mask_d, h_tm, NT * 4, cudaMemcpyHostToDevice, st));
     // embedding segments: unique ids (ascending) with their positions in order
     int* q = (int*)(h_tm + NT);
-    auto build = [&](int t, const std::vector<std::pair<int, int>>& idpos) {
-      std::vector<std::pair<int, int>> v = idpos;
-      std::stable_sort(v.begin(), v.end(), [](auto& a, auto& b) { return a.first < b.first; });
-      int n = (int)v.size();
+    // (id, position) pairs grouped by id, positions ascending within an id
+    // (= np.add.at order): one 64-bit key per pair, keys are unique, so an
+    // LSD radix sort (11-bit digits) gives the stable order in O(n)
+    auto build = [&](int t, std::vector<unsigned long long>& keys) {
+      const int n = (int)keys.size();
+      sort_tmp.resize(n);
+      unsigned long long* src_k = keys.data();
+      unsigned long long* dst_k = sort_tmp.data();
+      const unsigned long long maxkey = ((unsigned long long)(V - 1) << 32) | 0xffffffffull;
+      for (int shift = 0; shift < 64 && (maxkey >> shift); shift += 11) {
+        unsigned cnt[2049] = {0};
+        for (int i = 0; i < n; ++i) ++cnt[((src_k[i] >> shift) & 2047) + 1];
+        for (int d = 0; d < 2048; ++d) cnt[d + 1] += cnt[d];
+        for (int i = 0; i < n; ++i) dst_k[cnt[(src_k[i] >> shift) & 2047]++] = src_k[i];
+        std::swap(src_k, dst_k);
+      }
       int* off = q; int* pos = q + n + 1; int* uq = pos + n;
       int nu = 0;
       for (int i = 0; i < n; ++i) {
-        if (i == 0 || v[i].first != v[i - 1].first) { off[nu] = i; uq[nu] = v[i].first; ++nu; }
-        pos[i] = v[i].second;
+        const int id = (int)(src_k[i] >> 32);
+        if (i == 0 || id != (int)(src_k[i - 1] >> 32)) { off[nu] = i; uq[nu] = id; ++nu; }
+        pos[i] = (int)(src_k[i] & 0xffffffffull);
       }
       off[nu] = n;
       nuniq[t] = nu;
@@ -757,16 +771,18 @@ class Engine {
       CMT_CUDA(cudaMemcpyAsync(uniq_d[t], uq, nu * 4, cudaMemcpyHostToDevice, st));
       q = uq + nu;
     };
-    std::vector<std::pair<int, int>> a, b;
-    for (long long i = 0; i < NS; ++i) a.push_back({h_src[i], (int)i});
-    for (long long i = 0; i < NT; ++i) b.push_back({h_tin[i], (int)(NS + i)});
+    std::vector<unsigned long long> ka, kb;
+    ka.reserve(NS + NT);
+    kb.reserve(NT);
+    for (long long i = 0; i < NS; ++i) ka.push_back(((unsigned long long)h_src[i] << 32) | (unsigned)i);
+    for (long long i = 0; i < NT; ++i) kb.push_back(((unsigned long long)h_tin[i] << 32) | (unsigned)(NS + i));
     if (cfg.shared_embeddings) {
-      a.insert(a.end(), b.begin(), b.end());
-      build(0, a);
+      ka.insert(ka.end(), kb.begin(), kb.end());
+      build(0, ka);
       nuniq[1] = 0;
     } else {
-      build(0, a);
-      build(1, b);
+      build(0, ka);
+      build(1, kb);
     }
     staged = true;
   }
