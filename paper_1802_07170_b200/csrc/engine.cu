@@ -945,11 +945,14 @@ class Engine {
     const float* mask;
     float* uxb;  // hoisted input projection buffer of this scan
   };
-  bool use_dual_fwd() const {
-    return bf && persistent && dual && H % (64 * mc::Fwd<128>::KBOX) == 0 && H / 64 <= 32 && B <= 128 &&
-           2 * mc::Fwd<128>::ctas(H, B) <= g_num_sms &&
-           mc::Fwd<128>::stages(H) >= 2;
+  template <int ROWS>
+  bool fwd_multi_ok() const {
+    using F = mc::Fwd<ROWS>;
+    const int nh = (B + ROWS - 1) / ROWS;
+    return bf && persistent && dual && H % (64 * F::KBOX) == 0 && H / 64 <= 32 && (H / 64) * nh <= FLAG_STRIDE &&
+           F::ctas(H, B) <= g_num_sms && F::stages(H) >= 2;
   }
+  bool use_dual_fwd() const { return fwd_multi_ok<128>() && 2 * mc::Fwd<128>::ctas(H, B) <= g_num_sms; }
   void fwd_prep(const FwdScan& f) {  // Ux = X W_x + b (layers.py:354-357, K3)
     const Layer& ly = layers[f.l];
     EpiStore e = store(f.uxb, 4LL * H, false);
@@ -998,20 +1001,19 @@ class Engine {
     tl_mark(st, "lstm_fwd_pair");
   }
 
-  // one scan through lstm_fwd_multi<64> (batch halves on separate CTAs, 128 CTAs at H=1024)
-  bool use_multi_single_fwd() const {
-    return use_dual_fwd() && H % (64 * mc::Fwd<64>::KBOX) == 0 && (H / 64) * ((B + 63) / 64) <= 32 &&
-           mc::Fwd<64>::ctas(H, B) <= g_num_sms && mc::Fwd<64>::stages(H) >= 2;
-  }
+  // one scan through lstm_fwd_multi<ROWS>: batch slices of ROWS rows on separate
+  // CTAs (ROWS=64: 128 CTAs at H=1024, B<=128; ROWS=128: B<=256)
+  int single_fwd_rows() const { return fwd_multi_ok<64>() ? 64 : fwd_multi_ok<128>() ? 128 : 0; }
+  template <int ROWS>
   void fwd_single(const FwdScan& a) {
     CUtensorMap tm[2];
     LstmFwdMulti m;
-    m.c[0] = fwd_params<64>(a, &tm[0], &tm[1]);
+    m.c[0] = fwd_params<ROWS>(a, &tm[0], &tm[1]);
     m.c[1] = m.c[0];
-    const int g = mc::Fwd<64>::ctas(H, B);
+    const int g = mc::Fwd<ROWS>::ctas(H, B);
     m.split = g;
-    auto k = lstm_fwd_multi<64>;
-    const size_t smem = mc::Fwd<64>::smem(H);
+    auto k = lstm_fwd_multi<ROWS>;
+    const size_t smem = mc::Fwd<ROWS>::smem(H);
     CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t c = {};
     c.gridDim = dim3(g);
@@ -1029,10 +1031,11 @@ class Engine {
   }
 
   void scan_fwd(int l, const void* X, int din, int steps, bool reverse, const float* mask) {
-    if (use_multi_single_fwd()) {
+    if (const int rows = single_fwd_rows()) {
       FwdScan f{l, X, din, steps, reverse, mask, ux};
       fwd_prep(f);
-      fwd_single(f);
+      if (rows == 64) fwd_single<64>(f);
+      else fwd_single<128>(f);
       return;
     }
     const Layer& ly = layers[l];
@@ -1106,12 +1109,17 @@ class Engine {
   bool bwd_multi_ok() const {
     using F = mc::Bwd<ROWS>;
     return bf && persistent && dual && H % mc::BWD_NU == 0 && (H / 64) % mc::BWD_KBOX == 0 && H / 64 <= 32 &&
-           (4 * H / 64) * ((B + ROWS - 1) / ROWS) <= FLAG_STRIDE && B <= 128 && F::stages(H) >= 2 &&
-           (size_t)F::stages(H) * F::STAGE >= F::xbuf_bytes();
+           (4 * H / 64) * ((B + ROWS - 1) / ROWS) <= FLAG_STRIDE && F::ctas(H, B) <= g_num_sms &&
+           F::stages(H) >= 2 && (size_t)F::stages(H) * F::STAGE >= F::xbuf_bytes();
   }
   bool use_dual_bwd() const { return bwd_multi_ok<128>() && 2 * mc::Bwd<128>::ctas(H, B) <= g_num_sms; }
-  // one scan over two batch halves through lstm_bwd_multi<64> (128 CTAs at H=1024)
-  bool use_multi_single_bwd() const { return bwd_multi_ok<64>() && mc::Bwd<64>::ctas(H, B) <= g_num_sms; }
+  // one scan over batch slices of ROWS rows (64: two halves of B<=128; 128: B<=256)
+  int single_bwd_rows() const { return bwd_multi_ok<64>() ? 64 : bwd_multi_ok<128>() ? 128 : 0; }
+  void bwd_single(const BwdScan& f) {
+    if (single_bwd_rows() == 64) bwd_launch<64>(f, nullptr);
+    else bwd_launch<128>(f, nullptr);
+    bwd_post(f);
+  }
   template <int ROWS>
   LstmBwdP bwd_params(const BwdScan& f, CUtensorMap* tmA, CUtensorMap* tmW) {
     const Layer& ly = layers[f.l];
@@ -1586,18 +1594,13 @@ class Engine {
       return f;
     };
     auto single = [&](const BwdScan& f) {
+      if (single_bwd_rows()) { bwd_single(f); return; }
       scan_bwd(f.l, f.X, f.din, f.steps, f.reverse, f.mask, f.dy, f.dh_final, f.dc_final, f.dh0, f.dc0, f.dX,
                f.dx_beta, f.dx_keep);
     };
     if (use_dual_bwd()) {
       // pairs of independent scans: dL alone, then (d(k), e(k+1)) for k = L-1..1, then (e1 bwd, e1 fwd)
-      if (use_multi_single_bwd()) {
-        BwdScan dL = dec_scan(L, dU);
-        bwd_launch<64>(dL, nullptr);
-        bwd_post(dL);
-      } else {
-        single(dec_scan(L, dU));
-      }
+      single(dec_scan(L, dU));
       for (int k = L - 1; k >= 1; --k) {
         BwdScan d = dec_scan(k, dU), e = enc_scan(k + 1, dU2);
         bwd_pair(d, e);

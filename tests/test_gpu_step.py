@@ -207,7 +207,8 @@ def test_drop_in_train_step_and_determinism(mode):
 
 
 @pytest.mark.parametrize("case", [(256, 128, 256, 2, 32, 11, 9, True), (512, 64, 256, 3, 128, 7, 12, True),
-                                  (304, 64, 512, 1, 5, 13, 4, False), (256, 256, 256, 2, 96, 6, 5, True)])
+                                  (304, 64, 512, 1, 5, 13, 4, False), (256, 256, 256, 2, 96, 6, 5, True),
+                                  (256, 64, 1024, 1, 256, 5, 4, True)])  # B=256: 128-row slices, two per scan
 def test_persistent_recurrence_matches_per_step_and_oracle(case):
     """The persistent recurrent kernels (default in bf16) against the per-step
     tcgen05 path and the oracle, masked + unmasked, forward + reverse scans."""
