@@ -316,6 +316,12 @@ class Engine {
   bool bf;  // bf16 mode
   int asz;  // activation element size
   cudaStream_t st = nullptr;
+  // side stream for independent work of the two scans of a level (their input
+  // projections / weight-gradient GEMMs overlap and pack each other's waves)
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int overlap = 1;      // option
+  bool on_side = false;
   cudaEvent_t ev[16];
   std::string err;
 
@@ -350,6 +356,7 @@ class Engine {
   float *src_mask_d, *tgt_mask_d;
   void *Xs, *Xt, *top, *u_att, *cst_att, *hod, *Y, *dhpre, *du_att, *dU, *dU2;
   float* cepart = nullptr;  // per-CTA dY column sums of the fused CE kernel
+  float* colpart2 = nullptr;  // column-sum scratch of the side stream
   float* dho32 = nullptr;   // fp32 split-K scratch of dH_o (bf16 mode)
   float *att_part = nullptr, *att_dsc = nullptr;  // split attention: score slices, d scores
   int att_split = 1;  // option: split attention kernels (many CTAs per sentence)
@@ -430,6 +437,9 @@ class Engine {
       throw Error(CMT_ERR_SHAPE, "bf16 mode needs vocab/embedding/hidden sizes that are multiples of 8");
     asz = bf ? 2 : 4;
     CMT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CMT_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+    CMT_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CMT_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     for (auto& e : ev) CMT_CUDA(cudaEventCreate(&e));
     build_registry();
     alloc_params();
@@ -447,6 +457,9 @@ class Engine {
     if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
     for (auto& e : ev) cudaEventDestroy(e);
     cudaStreamDestroy(st);
+    cudaStreamDestroy(st2);
+    cudaEventDestroy(ev_fork);
+    cudaEventDestroy(ev_join);
   }
 
   static size_t al(size_t x) { return (x + 63) & ~(size_t)63; }
@@ -663,6 +676,7 @@ class Engine {
     }
     long long colmax = std::max<long long>(V, 4LL * H);
     colpart = carve<float>(cur, 64 * colmax * 4);
+    colpart2 = carve<float>(cur, 64 * colmax * 4);
     cepart = use_ce2() ? carve<float>(cur, (long long)g_num_sms * V * 4) : nullptr;
     for (int t = 0; t < 2; ++t) {
       seg_off_d[t] = carve<int>(cur, (NS + NT + 1) * 4);
@@ -1256,7 +1270,33 @@ class Engine {
     gemm((int)N, din, 4 * H, Mat{dU, 4LL * H, 0}, Mat{wv(ly.w_off), 4LL * H, 0}, e);
   }
 
+  // ---- fork / join of the side stream ----
+  bool use_overlap() const { return overlap && !g_tl.on; }  // the timeline measures one stream
+  void fork() {
+    CMT_CUDA(cudaEventRecord(ev_fork, st));
+    CMT_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
+  }
+  template <class F>
+  void on_side_stream(F&& f) {  // issue f's launches on the side stream
+    std::swap(st, st2);
+    on_side = true;
+    try {
+      f();
+    } catch (...) {
+      std::swap(st, st2);
+      on_side = false;
+      throw;
+    }
+    std::swap(st, st2);
+    on_side = false;
+  }
+  void join() {
+    CMT_CUDA(cudaEventRecord(ev_join, st2));
+    CMT_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+  }
+
   void colsum(const void* D, bool is_act, long long rows, int cols, float* out) {
+    float* colpart = on_side ? colpart2 : this->colpart;
     int chunks = (int)std::min<long long>(64, std::max<long long>(1, rows / 64));
     int rows_per = ceil_div(rows, chunks);
     chunks = ceil_div(rows, rows_per);
@@ -1285,6 +1325,7 @@ class Engine {
     const bool infer = (a.flags & CMT_FLAG_INFER) != 0;  // dev_entropy pass (training.py:162-182)
     const bool drop = cfg.dropout > 0.0 && !infer;        // INFER mode: dropout is the identity
     Pcg pcg{a.pcg_state_hi, a.pcg_state_lo, a.pcg_inc_hi, a.pcg_inc_lo};
+    if (drop && use_jump) ensure_jump(pcg);  // before any side-stream dropout reads the table
     double ntok = a.global_ntok > 0 ? a.global_ntok : ntok_local;
     float inv_ntok = ntok > 0 ? (float)(1.0 / (double)(float)ntok) : 0.f;
     CMT_CUDA(cudaMemsetAsync(out_d, 0, sizeof(StepOut), st));
@@ -1341,16 +1382,42 @@ class Engine {
     if (use_dual_fwd()) {
       // two independent scans per launch: (e1f, e1b), (e2, d1), ..., (eL, d(L-1)), then dL
       FwdScan a{0, Xs, E, S, false, src_mask_d, ux}, b{1, Xs, E, S, true, src_mask_d, ux2};
-      fwd_prep(a); fwd_prep(b); fwd_pair(a, b);
+      if (use_overlap()) {
+        fork();
+        fwd_prep(a);
+        on_side_stream([&]() { fwd_prep(b); });
+        join();
+      } else {
+        fwd_prep(a);
+        fwd_prep(b);
+      }
+      fwd_pair(a, b);
       add_top();
       const void* cur = top;
       for (int k = 2; k <= L; ++k) {
+        // the two scans' inputs (dropout, initial state, input projection) are
+        // independent: the decoder side is issued on the side stream
+        const bool ov = use_overlap();
+        if (ov) fork();
         const void* in = enc_input(k, cur);
         zero_enc_state(k);
-        const void* xd = dec_input(k - 1);
-        dec_init(k - 1);
-        FwdScan e{k, in, H, S, false, src_mask_d, ux}, d{L + k - 1, xd, k - 1 == 1 ? E : H, T, false, nullptr, ux2};
-        fwd_prep(e); fwd_prep(d); fwd_pair(e, d);
+        FwdScan e{k, in, H, S, false, src_mask_d, ux};
+        fwd_prep(e);
+        const void* xd = nullptr;
+        auto dec_side = [&]() {
+          xd = dec_input(k - 1);
+          dec_init(k - 1);
+        };
+        if (ov) on_side_stream(dec_side);
+        else dec_side();
+        FwdScan d{L + k - 1, xd, k - 1 == 1 ? E : H, T, false, nullptr, ux2};
+        if (ov) {
+          on_side_stream([&]() { fwd_prep(d); });
+          join();
+        } else {
+          fwd_prep(d);
+        }
+        fwd_pair(e, d);
         cur = views(k, false).ybase;
       }
       const void* xd = dec_input(L);
@@ -1604,8 +1671,15 @@ class Engine {
       for (int k = L - 1; k >= 1; --k) {
         BwdScan d = dec_scan(k, dU), e = enc_scan(k + 1, dU2);
         bwd_pair(d, e);
-        bwd_post(d);
-        bwd_post(e);
+        if (use_overlap()) {  // disjoint outputs: the encoder scan's GEMMs on the side stream
+          fork();
+          bwd_post(d);
+          on_side_stream([&]() { bwd_post(e); });
+          join();
+        } else {
+          bwd_post(d);
+          bwd_post(e);
+        }
       }
       BwdScan b1 = l1_scan(true, dU), f1 = l1_scan(false, dU2);
       bwd_pair(b1, f1);
@@ -1927,6 +2001,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "jump") e->eng->use_jump = (int)value;
     else if (k == "att_split") e->eng->att_split = (int)value;
     else if (k == "allow_empty_targets") e->eng->allow_empty_targets = (int)value;
+    else if (k == "overlap") e->eng->overlap = (int)value;
     else if (k == "ce2") {
       if (e->eng->staged && (value != 0) != (e->eng->ce2 != 0)) throw Error(cmt::CMT_ERR_CONFIG, "set ce2 before staging");
       e->eng->ce2 = (int)value;
