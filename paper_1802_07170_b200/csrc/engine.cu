@@ -1192,7 +1192,12 @@ class Engine {
     gemm(H, 4 * H, (int)N, Mat{v.hprev, H, 1}, Mat{f.dUb, 4LL * H, 1},
          store(dg + ly.w_off + (size_t)f.din * 4 * H, 4LL * H, false));
     colsum(f.dUb, true, N, 4 * H, dg + ly.b_off);
-    // dX = dU W_x^T (layers.py:392; K7), dropout backward fused (layers.py:292-296)
+    if (f.dX) bwd_post_dx(f);
+  }
+  // dX = dU W_x^T (layers.py:392; K7), dropout backward fused (layers.py:292-296)
+  void bwd_post_dx(const BwdScan& f) {
+    const Layer& ly = layers[f.l];
+    long long N = (long long)f.steps * B;
     EpiStore e = store(f.dX, f.din, false);
     e.beta = f.dx_beta;
     if (f.dx_keep) { e.dmask = f.dx_keep; e.ld_dmask = f.din; e.dscale = 1.0f / (float)(1.0 - cfg.dropout); }
@@ -1558,8 +1563,19 @@ class Engine {
     }
     // ===== backward =====
     // output projection (layers.py:64-73): dW_o, db_o, dH_o (+ dropout bwd + tanh' of H_o)
-    gemm(H, V, (int)NT, Mat{hin, H, 1}, Mat{Y, V, 1}, store(dg + off_wo, V, false));
-    if (!fused_ce) colsum(Y, true, NT, V, dg + off_bo);
+    // dW_o only feeds the update: on the side stream it overlaps dH_o and the
+    // attention backward (joined before the BPTT scans)
+    const bool ov_wo = use_overlap();
+    if (ov_wo) {
+      fork();
+      on_side_stream([&]() {
+        gemm(H, V, (int)NT, Mat{hin, H, 1}, Mat{Y, V, 1}, store(dg + off_wo, V, false));
+        if (!fused_ce) colsum(Y, true, NT, V, dg + off_bo);
+      });
+    } else {
+      gemm(H, V, (int)NT, Mat{hin, H, 1}, Mat{Y, V, 1}, store(dg + off_wo, V, false));
+      if (!fused_ce) colsum(Y, true, NT, V, dg + off_bo);
+    }
     {
       // dH_o = dY W_o^T with the dropout mask and tanh' of H_o applied (linear, so
       // they may act per K slice).  bf16 mode: K = V is long and the 100 output
@@ -1635,6 +1651,7 @@ class Engine {
       e.add = dcst + H; e.ld_add = 2LL * H;
       gemm((int)NT, H, H, Mat{du_att, H, 0}, Mat{wv(off_wa), H, 0}, e);
     }
+    if (ov_wo) join();
     // decoder BPTT, top layer first (graph.py:112-115); init-state grads -> encoder finals
     auto dec_scan = [&](int k, void* dub) {
       BwdScan f;
@@ -1683,8 +1700,20 @@ class Engine {
       }
       BwdScan b1 = l1_scan(true, dU), f1 = l1_scan(false, dU2);
       bwd_pair(b1, f1);
-      bwd_post(b1);
-      bwd_post(f1);
+      if (use_overlap()) {
+        // weight grads of both directions overlap; the two dX GEMMs stay ordered
+        // (enc.l1.fwd accumulates into enc.l1.bwd's embedding grads)
+        fork();
+        bwd_post(b1);
+        BwdScan f1w = f1;
+        f1w.dX = nullptr;
+        on_side_stream([&]() { bwd_post(f1w); });
+        join();
+        bwd_post_dx(f1);
+      } else {
+        bwd_post(b1);
+        bwd_post(f1);
+      }
     } else {
       for (int k = L; k >= 1; --k) single(dec_scan(k, dU));
       for (int k = L; k >= 2; --k) single(enc_scan(k, dU));
