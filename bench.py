@@ -188,6 +188,9 @@ def main():
     cfg = ModelConfig(V, E, H, L, 0.2)
     model = Model.new(cfg, Rng(1))
     eng = Engine(cfg, mode="bf16", device=local)
+    for kv in filter(None, os.environ.get("CMT_OPTIONS", "").split(",")):  # experiments: k=v engine options
+        k, v = kv.split("=")
+        eng.set_option(k.strip(), int(v))
     eng.upload(model.params)
     if world > 1:
         eng.set_dp(dist, rank, world)

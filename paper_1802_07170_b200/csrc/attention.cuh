@@ -452,4 +452,231 @@ __global__ void __launch_bounds__(att::THREADS) attn_bwd_chunk(const E* __restri
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Tiled split attention for S, T <= 128 (used for every length <= 128): the
+// (t, s) plane is cut into 64 x 64 tiles and every product gets its own grid
+// axis over tiles, so longer sentences (c5: S = T = 80) stay on the same
+// register-tiled path.  The dHs and dU products are separate kernels.
+// ---------------------------------------------------------------------------
+namespace att2 {
+using att::HC;
+using att::KC;
+using att::LD;
+using att::THREADS;
+constexpr int P = 64;       // tile edge
+constexpr int MAXL = 128;   // longest S / T handled
+CMT_HD int tiles(int n) { return (n + P - 1) / P; }
+
+// dst[k][r] = src row r0 + r (r < 64), columns k0..k0+KC-1, zero padded
+template <typename E>
+CMT_D void load_t_tile(float* dst, const E* src, long long ld, int r0, int rows, int B, int b, int k0, int K) {
+  constexpr int VEC = 16 / sizeof(E);
+  constexpr int SEGS = KC / VEC;
+  for (int i = threadIdx.x; i < P * SEGS; i += THREADS) {
+    const int r = i / SEGS, sg = i % SEGS;
+    const int k = k0 + sg * VEC;
+    const int gr = r0 + r;
+    float v[VEC];
+    const E* p = src + ((long long)gr * B + b) * ld + k;
+    if (gr < rows && k + VEC <= K && (((uintptr_t)p) & 15) == 0) {
+      const uint4 q = *(const uint4*)p;
+      const E* e = (const E*)&q;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[j] = to_f<E>(e[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[j] = (gr < rows && k + j < K) ? to_f<E>(p[j]) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) dst[(sg * VEC + j) * LD + r] = v[j];
+  }
+}
+// dst[r][c] = src row r (r < npad), columns h0..h0+HC-1, zero padded
+template <typename E>
+CMT_D void load_n_rows(float* dst, const E* src, long long ld, int npad, int rows, int B, int b, int h0, int K) {
+  constexpr int VEC = 16 / sizeof(E);
+  constexpr int SEGS = HC / VEC;
+  for (int i = threadIdx.x; i < npad * SEGS; i += THREADS) {
+    const int r = i / SEGS, sg = i % SEGS;
+    const int k = h0 + sg * VEC;
+    float v[VEC];
+    const E* p = src + ((long long)r * B + b) * ld + k;
+    if (r < rows && k + VEC <= K && (((uintptr_t)p) & 15) == 0) {
+      const uint4 q = *(const uint4*)p;
+      const E* e = (const E*)&q;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[j] = to_f<E>(e[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[j] = (r < rows && k + j < K) ? to_f<E>(p[j]) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) dst[r * LD + sg * VEC + j] = v[j];
+  }
+}
+}  // namespace att2
+
+// part[b][sp][t][s] (t < Tp, s < Sp padded to 64) = sum_{h in slice sp} X[t][h] Hs[s][h]
+template <typename EX, typename EH>
+__global__ void __launch_bounds__(att::THREADS) attn2_scores_part(const EX* __restrict__ X, long long ldx,
+                                                                  const EH* __restrict__ Hs, int S, int Tq, int B,
+                                                                  int H, float* __restrict__ part) {
+  using namespace att2;
+  __shared__ __align__(16) float sX[KC * LD];
+  __shared__ __align__(16) float sH[KC * LD];
+  const int b = blockIdx.x, sp = blockIdx.y, nsp = gridDim.y;
+  const int ts = tiles(S), Tp = tiles(Tq) * P, Sp = ts * P;
+  const int t0 = (blockIdx.z / ts) * P, s0 = (blockIdx.z % ts) * P;
+  const int h0 = sp * att::HS, h1 = min(H, h0 + att::HS);
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  float acc[4][4];
+  att::zero44(acc);
+  for (int k0 = h0; k0 < h1; k0 += KC) {
+    load_t_tile(sX, X, ldx, t0, Tq, B, b, k0, h1);
+    load_t_tile(sH, Hs, H, s0, S, B, b, k0, h1);
+    __syncthreads();
+    att::mm44(acc, sX, sH, ty * 4, tx * 4, KC);
+    __syncthreads();
+  }
+  float* o = part + ((size_t)b * nsp + sp) * Tp * Sp;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    *(float4*)(o + (size_t)(t0 + ty * 4 + i) * Sp + s0 + tx * 4) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+}
+
+// mode 0: alpha = masked softmax of the summed scores; mode 1: dscores = alpha (g - sum alpha g)
+__global__ void __launch_bounds__(att::THREADS) attn2_rows(const float* __restrict__ part, int nsp,
+                                                           const float* __restrict__ src_mask, int S, int Tq, int B,
+                                                           float* __restrict__ alpha, float* __restrict__ dsc,
+                                                           int mode, int* __restrict__ status) {
+  using namespace att2;
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Tp = tiles(Tq) * P, Sp = tiles(S) * P;
+  const float* pb = part + (size_t)b * nsp * Tp * Sp;
+  for (int t = warp; t < Tq; t += THREADS / 32) {
+    float v[MAXL / 32], pv[MAXL / 32];
+#pragma unroll
+    for (int r = 0; r < MAXL / 32; ++r) {
+      const int s = lane + 32 * r;
+      float a = 0.f;
+      if (s < S)
+        for (int k = 0; k < nsp; ++k) a += pb[((size_t)k * Tp + t) * Sp + s];
+      v[r] = a;
+      pv[r] = (mode == 1 && s < S) ? alpha[((long long)b * Tq + t) * S + s] : 0.f;
+    }
+    if (mode == 0) {
+      float mx = -INFINITY;
+      bool bad = false;
+#pragma unroll
+      for (int r = 0; r < MAXL / 32; ++r) {
+        const int s = lane + 32 * r;
+        if (s < S) {
+          v[r] += (1.f - src_mask[s * B + b]) * -1e9f;
+          bad |= !isfinite(v[r]);
+          mx = fmaxf(mx, v[r]);
+        }
+      }
+      mx = warp_max(mx);
+      float sum = 0.f;
+#pragma unroll
+      for (int r = 0; r < MAXL / 32; ++r) {
+        const int s = lane + 32 * r;
+        v[r] = s < S ? expf(v[r] - mx) : 0.f;
+        sum += v[r];
+      }
+      sum = warp_sum(sum);
+#pragma unroll
+      for (int r = 0; r < MAXL / 32; ++r) {
+        const int s = lane + 32 * r;
+        if (s < S) alpha[((long long)b * Tq + t) * S + s] = v[r] / sum;
+      }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_SCORES);
+    } else {
+      float dot = 0.f;
+#pragma unroll
+      for (int r = 0; r < MAXL / 32; ++r) dot += pv[r] * v[r];
+      dot = warp_sum(dot);
+#pragma unroll
+      for (int r = 0; r < MAXL / 32; ++r) {
+        const int s = lane + 32 * r;
+        if (s < S) dsc[((long long)b * Tq + t) * S + s] = pv[r] * (v[r] - dot);
+      }
+    }
+  }
+}
+
+// out[t][h] (t-tile blockIdx.z) = sum_s W[t][s] Hs[s][h]; W = alpha (ctx) or dscores (dU)
+template <typename E>
+__global__ void __launch_bounds__(att::THREADS) attn2_ws_hs(const E* __restrict__ Hs, const float* __restrict__ W,
+                                                            int S, int Tq, int B, int H, E* __restrict__ out,
+                                                            long long ldo) {
+  using namespace att2;
+  extern __shared__ float sm[];
+  const int Sp = tiles(S) * P;
+  float* wT = sm;            // [s][t-local]
+  float* ch = sm + Sp * LD;  // [s][h]
+  const int b = blockIdx.x, h0 = blockIdx.y * HC, t0 = blockIdx.z * P;
+  for (int i = threadIdx.x; i < Sp * P; i += THREADS) {
+    const int s = i / P, t = i % P;
+    wT[s * LD + t] = (s < S && t0 + t < Tq) ? W[((long long)b * Tq + t0 + t) * S + s] : 0.f;
+  }
+  load_n_rows(ch, Hs, H, Sp, S, B, b, h0, H);
+  __syncthreads();
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  float acc[4][4];
+  att::zero44(acc);
+  att::mm44(acc, wT, ch, ty * 4, tx * 4, S);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = t0 + ty * 4 + i;
+    if (t >= Tq) continue;
+    E* o = out + ((long long)t * B + b) * ldo + h0 + tx * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (h0 + tx * 4 + j < H) o[j] = from_f<E>(acc[i][j]);
+  }
+}
+
+// dHs[s][h] (s-tile blockIdx.z) += sum_t alpha[t][s] dC[t][h] + dscores[t][s] U[t][h]
+template <typename E>
+__global__ void __launch_bounds__(att::THREADS) attn2_dhs(const E* __restrict__ U, const float* __restrict__ alpha,
+                                                          const float* __restrict__ dsc, const float* __restrict__ dC,
+                                                          long long lddc, int S, int Tq, int B, int H,
+                                                          float* __restrict__ dHs) {
+  using namespace att2;
+  extern __shared__ float sm[];
+  const int Tp = tiles(Tq) * P;
+  float* al = sm;             // [t][s-local]
+  float* ds = al + Tp * LD;   // [t][s-local]
+  float* cC = ds + Tp * LD;   // [t][h]
+  float* cU = cC + Tp * LD;   // [t][h]
+  const int b = blockIdx.x, h0 = blockIdx.y * HC, s0 = blockIdx.z * P;
+  for (int i = threadIdx.x; i < Tp * P; i += THREADS) {
+    const int t = i / P, s = i % P;
+    const bool ok = t < Tq && s0 + s < S;
+    const long long o = ((long long)b * Tq + t) * S + s0 + s;
+    al[t * LD + s] = ok ? alpha[o] : 0.f;
+    ds[t * LD + s] = ok ? dsc[o] : 0.f;
+  }
+  load_n_rows(cC, dC, lddc, Tp, Tq, B, b, h0, H);
+  load_n_rows(cU, U, H, Tp, Tq, B, b, h0, H);
+  __syncthreads();
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  float acc[4][4];
+  att::zero44(acc);
+  att::mm44(acc, al, cC, ty * 4, tx * 4, Tq);
+  att::mm44(acc, ds, cU, ty * 4, tx * 4, Tq);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int s = s0 + ty * 4 + i;
+    if (s >= S) continue;
+    float* o = dHs + ((long long)s * B + b) * H + h0 + tx * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (h0 + tx * 4 + j < H) o[j] += acc[i][j];
+  }
+}
+
 }  // namespace cmt

@@ -359,7 +359,7 @@ class Engine {
   float* colpart2 = nullptr;  // column-sum scratch of the side stream
   float* dho32 = nullptr;   // fp32 split-K scratch of dH_o (bf16 mode)
   float *att_part = nullptr, *att_dsc = nullptr;  // split attention: score slices, d scores
-  int att_split = 1;  // option: split attention kernels (many CTAs per sentence)
+  int att_split = 2;  // option: 2 tiled split attention (S,T <= 128), 1 split (<= 64), 0 per-sentence
   int allow_empty_targets = 0;  // option: stage batches with no unmasked target (dev_entropy)
   bool last_infer = false;
   float *ux, *ux2, *alpha, *ho, *losstok, *dcst, *dXemb, *dtop, *dhc, *dcc, *colpart;
@@ -654,7 +654,7 @@ class Engine {
     u_att = carve<char>(cur, NT * H * asz);
     alpha = carve<float>(cur, (long long)B * T * S * 4);
     att_dsc = carve<float>(cur, (long long)B * T * S * 4);
-    att_part = carve<float>(cur, (long long)B * att::nslices(H) * att::P * att::P * 4);
+    att_part = carve<float>(cur, (long long)B * att::nslices(H) * att2::tiles(T) * att2::tiles(S) * att2::P * att2::P * 4);
     cst_att = carve<char>(cur, NT * 2 * H * asz);
     ho = carve<float>(cur, NT * H * 4);
     hod = carve<char>(cur, NT * H * asz);
@@ -1450,7 +1450,27 @@ class Engine {
     // attention (attention.py:146-173)
     copy_act(Ht, H, (char*)cst_att + (size_t)H * asz, 2LL * H, (int)NT, H);
     gemm((int)NT, H, H, Mat{Ht, H, 0}, Mat{wv(off_wa), H, 1}, store(u_att, H, true));
-    if (S <= att::P && T <= att::P && att_split) {
+    if (S <= att2::MAXL && T <= att2::MAXL && att_split == 2) {
+      const int nsp = att::nslices(H), tt = att2::tiles(T), ts = att2::tiles(S);
+      dim3 gs(B, nsp, tt * ts), gc(B, ceil_div(H, att::HC), tt);
+      if (bf) attn2_scores_part<bf16, bf16><<<gs, att::THREADS, 0, st>>>((const bf16*)u_att, H, (const bf16*)Hs, S, T, B,
+                                                                        H, att_part);
+      else attn2_scores_part<float, float><<<gs, att::THREADS, 0, st>>>((const float*)u_att, H, (const float*)Hs, S, T, B,
+                                                                        H, att_part);
+      CMT_LAUNCHED(); tl_mark(st, "attn2_scores_part");
+      attn2_rows<<<B, att::THREADS, 0, st>>>(att_part, nsp, src_mask_d, S, T, B, alpha, nullptr, 0, status_d);
+      CMT_LAUNCHED(); tl_mark(st, "attn2_rows");
+      const size_t smem = sizeof(float) * 2 * ts * att2::P * att::LD;
+      if (bf) {
+        CMT_CUDA(cudaFuncSetAttribute(attn2_ws_hs<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attn2_ws_hs<bf16><<<gc, att::THREADS, smem, st>>>((const bf16*)Hs, alpha, S, T, B, H, (bf16*)cst_att, 2LL * H);
+      } else {
+        CMT_CUDA(cudaFuncSetAttribute(attn2_ws_hs<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attn2_ws_hs<float><<<gc, att::THREADS, smem, st>>>((const float*)Hs, alpha, S, T, B, H, (float*)cst_att, 2LL * H);
+      }
+      CMT_LAUNCHED(); tl_mark(st, "attn2_context");
+      CMT_CUDA(cudaGetLastError());
+    } else if (S <= att::P && T <= att::P && att_split) {
       const int nsp = att::nslices(H);
       dim3 gs(B, nsp), gc(B, ceil_div(H, att::HC));
       if (bf) attn_scores_part<bf16, bf16><<<gs, att::THREADS, 0, st>>>((const bf16*)u_att, H, (const bf16*)Hs, S, T, B, H,
@@ -1597,7 +1617,36 @@ class Engine {
     // attention core backward
     float* dHs = (L == 1) ? dtop : lw[L].dy;
     CMT_CUDA(cudaMemsetAsync(dHs, 0, NS * H * 4, st));
-    if (S <= att::P && T <= att::P && att_split) {
+    if (S <= att2::MAXL && T <= att2::MAXL && att_split == 2) {
+      const int nsp = att::nslices(H), tt = att2::tiles(T), ts = att2::tiles(S);
+      dim3 gs(B, nsp, tt * ts), gt(B, ceil_div(H, att::HC), tt), gsd(B, ceil_div(H, att::HC), ts);
+      if (bf) attn2_scores_part<float, bf16><<<gs, att::THREADS, 0, st>>>(dcst, 2LL * H, (const bf16*)Hs, S, T, B, H,
+                                                                         att_part);
+      else attn2_scores_part<float, float><<<gs, att::THREADS, 0, st>>>(dcst, 2LL * H, (const float*)Hs, S, T, B, H,
+                                                                         att_part);
+      CMT_LAUNCHED(); tl_mark(st, "attn2_scores_part");
+      attn2_rows<<<B, att::THREADS, 0, st>>>(att_part, nsp, src_mask_d, S, T, B, alpha, att_dsc, 1, status_d);
+      CMT_LAUNCHED(); tl_mark(st, "attn2_rows");
+      const size_t smem_h = sizeof(float) * 4 * tt * att2::P * att::LD;
+      const size_t smem_u = sizeof(float) * 2 * ts * att2::P * att::LD;
+      if (bf) {
+        CMT_CUDA(cudaFuncSetAttribute(attn2_dhs<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_h));
+        attn2_dhs<bf16><<<gsd, att::THREADS, smem_h, st>>>((const bf16*)u_att, alpha, att_dsc, dcst, 2LL * H, S, T, B, H,
+                                                           dHs);
+        CMT_LAUNCHED(); tl_mark(st, "attn2_dhs");
+        CMT_CUDA(cudaFuncSetAttribute(attn2_ws_hs<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u));
+        attn2_ws_hs<bf16><<<gt, att::THREADS, smem_u, st>>>((const bf16*)Hs, att_dsc, S, T, B, H, (bf16*)du_att, H);
+      } else {
+        CMT_CUDA(cudaFuncSetAttribute(attn2_dhs<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_h));
+        attn2_dhs<float><<<gsd, att::THREADS, smem_h, st>>>((const float*)u_att, alpha, att_dsc, dcst, 2LL * H, S, T, B,
+                                                            H, dHs);
+        CMT_LAUNCHED(); tl_mark(st, "attn2_dhs");
+        CMT_CUDA(cudaFuncSetAttribute(attn2_ws_hs<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u));
+        attn2_ws_hs<float><<<gt, att::THREADS, smem_u, st>>>((const float*)Hs, att_dsc, S, T, B, H, (float*)du_att, H);
+      }
+      CMT_LAUNCHED(); tl_mark(st, "attn2_du");
+      CMT_CUDA(cudaGetLastError());
+    } else if (S <= att::P && T <= att::P && att_split) {
       const int nsp = att::nslices(H);
       dim3 gs(B, nsp), gc(B, ceil_div(H, att::HC));
       if (bf) attn_scores_part<float, bf16><<<gs, att::THREADS, 0, st>>>(dcst, 2LL * H, (const bf16*)Hs, S, T, B, H, att_part);

@@ -326,7 +326,8 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
   uint64_t* tempty = tfull + 1;
   uint64_t* rfree = tempty + 1;  // the three partners' MMAs are done: their rings may receive partials
   uint64_t* xfull = rfree + 1;   // all partials for my units have landed in my ring
-  uint32_t* tmem_slot = (uint32_t*)(xfull + 1);
+  uint64_t* xdone = xfull + 1;   // my epilogue has read this round's partials: the ring may refill
+  uint32_t* tmem_slot = (uint32_t*)(xdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kq = (int)ptx::cluster_rank();
@@ -349,6 +350,7 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
     ptx::mbar_init(tempty, 8);
     ptx::mbar_init(rfree, mc::BWD_KS - 1);
     ptx::mbar_init(xfull, 1);  // my expect_tx; the partners' st.async bytes complete it
+    ptx::mbar_init(xdone, 8);  // the 8 epilogue warps
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 64);
@@ -371,6 +373,10 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
     uint32_t phase = 0;
     const int nst = KBL / mc::BWD_KBOX;
     for (int i = 1; i < rounds; ++i) {
+      // the ring doubles as the receive buffer of round i-1's partial sums: with
+      // per-k-block flags this round's k-blocks can be ready before this CTA has
+      // read them, so wait until its epilogue is done with the partials
+      if (i >= 2) ptx::mbar_wait(xdone, (i - 2) & 1);
       if (p.trace && bid == 0 && lane == 0) p.trace[i * 8 + 0] = gtimer();
       const int arow = time_of(p.steps - i) * p.B + r0;
       const unsigned target = (unsigned)i;
@@ -513,6 +519,8 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
           acc[0] += z0.x; acc[1] += z0.y; acc[2] += z0.z; acc[3] += z0.w;
           acc[4] += z1.x; acc[5] += z1.y; acc[6] += z1.z; acc[7] += z1.w;
         }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(xdone);  // partials consumed: the producer may refill the ring
         if (p.trace && bid == 0 && threadIdx.x == 128) p.trace[i * 8 + 2] = gtimer();
       } else {
 #pragma unroll

@@ -268,7 +268,8 @@ def test_dp_path_single_rank_nccl_matches_plain(mode):
         assert O.norm_rel_err(out[1][2][n], out[0][2][n]) < 1e-6, n
 
 
-@pytest.mark.parametrize("case", [(304, 64, 128, 2, 24, 17, 13, True), (256, 128, 256, 1, 8, 64, 64, False)])
+@pytest.mark.parametrize("case", [(304, 64, 128, 2, 24, 17, 13, True), (256, 128, 256, 1, 8, 64, 64, False),
+                                  (256, 64, 128, 1, 12, 80, 72, True), (256, 64, 128, 1, 4, 128, 100, False)])
 def test_attention_variants_agree(case):
     """Split attention kernels (many CTAs per sentence, default) against the
     one-CTA-per-sentence tiled kernels and the oracle (bf16 step)."""
@@ -281,16 +282,17 @@ def test_attention_variants_agree(case):
     src, sm, tgt, tm = O.synthetic_batch(V, S, T, B, seed=8, ragged=ragged)
     _, _, og, _, _ = oracle_step(d, params, (src, sm, tgt, tm), 0.1, 1.0, 5.0, 3, update=False)
     out = {}
-    for split in (0, 1):
+    for split in (0, 1, 2):
         eng = Engine(cfg_of(d), mode="bf16")
         eng.set_option("att_split", split)
         eng.upload(params)
         eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, np.random.Generator(np.random.PCG64(3)), update=False)
         out[split] = eng.grads()
         eng.close()
-    for n in og:
-        assert O.norm_rel_err(out[1][n], out[0][n]) < 1e-3, n
-        assert O.norm_rel_err(out[1][n], og[n]) < BF16_TOL, n
+    for v in (1, 2):
+        for n in og:
+            assert O.norm_rel_err(out[v][n], out[0][n]) < 1e-3, (v, n)
+            assert O.norm_rel_err(out[v][n], og[n]) < BF16_TOL, (v, n)
 
 
 @pytest.mark.parametrize("mode,tol", [("fp32", FP32_TOL), ("bf16", BF16_TOL)])
