@@ -519,6 +519,12 @@ __global__ void sum_to_double_kernel(const float* __restrict__ x, int n, double*
 // Same math as ce_kernel (training.py:96-120, tensor.py:146-151).
 // ---------------------------------------------------------------------------
 constexpr int CE2_THREADS = 1024;
+constexpr float kLog2e = 1.4426950408889634f;
+CMT_D float ex2f(float x) {  // 2^x (MUFU.EX2)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 constexpr int CE2_MAXV = 55 * 1024;  // smem column sums (fp32)
 constexpr int CE2_UNROLL = 4;        // 16-byte loads in flight per thread
 __global__ void __launch_bounds__(CE2_THREADS, 1)
@@ -551,13 +557,16 @@ __global__ void __launch_bounds__(CE2_THREADS, 1)
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         y[j] = __bfloat162float(e[j]);
-        bad |= !isfinite(y[j]);
         sy += y[j];
       }
       if (tanh_on) {
+        // |y| <= 1: no max shift; a non-finite logit makes the row sum
+        // non-finite, which is checked once per row below
 #pragma unroll
-        for (int j = 0; j < 8; ++j) se += __expf(y[j]);
+        for (int j = 0; j < 8; ++j) se += ex2f(y[j] * kLog2e);
       } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bad |= !isfinite(y[j]);
         float lm = y[0];
 #pragma unroll
         for (int j = 1; j < 8; ++j) lm = fmaxf(lm, y[j]);
@@ -574,6 +583,7 @@ __global__ void __launch_bounds__(CE2_THREADS, 1)
     se = (mx == -INFINITY) ? 0.f : se * __expf(mx - wm);
     se = warp_sum(se);
     sy = warp_sum(sy);
+    if (tanh_on) bad = !isfinite(sy);
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_LOGITS);
     if (lane == 0) { red_m[warp] = wm; red_s[warp] = se; red_y[warp] = sy; }
     __syncthreads();
@@ -600,6 +610,7 @@ __global__ void __launch_bounds__(CE2_THREADS, 1)
     __syncthreads();
     const float lse = bc[0], w = bc[1];
     const int g = tgt[n];
+    const float lse2 = lse * kLog2e, ewv = eV * w, gw = (1.f - eps) * w;
     for (int i0 = threadIdx.x; i0 < nv; i0 += CE2_UNROLL * CE2_THREADS) {
       uint4 qv[CE2_UNROLL];
 #pragma unroll
@@ -616,15 +627,16 @@ __global__ void __launch_bounds__(CE2_THREADS, 1)
       float* cs = csum + i * 8;
       const float4 c0 = *(const float4*)cs, c1 = *(const float4*)(cs + 4);
       float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      const int gj = g - i * 8;  // the gold column falls in this vector iff 0 <= gj < 8
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float y = __bfloat162float(e[j]);
-        float d = __expf(y - lse) - eV - (i * 8 + j == g ? (1.f - eps) : 0.f);
-        d *= w;
-        if (tanh_on) d *= (1.f - y * y);
-        const bf16 db = __float2bfloat16_rn(d);
-        o[j] = db;
-        c[j] += __bfloat162float(db);  // the bias grad sums the stored (bf16) dY, as colsum did
+        // d = (p - eps/V - (1-eps)[v=gold]) * m / ntok   (* (1 - y^2) with the output tanh)
+        float d = fmaf(ex2f(fmaf(y, kLog2e, -lse2)), w, -ewv);
+        if (j == gj) d -= gw;
+        if (tanh_on) d *= fmaf(-y, y, 1.f);
+        o[j] = __float2bfloat16_rn(d);
+        c[j] += d;  // bias grad = column sum of dpre (fp32, layers.py:72-73)
       }
       row[i] = *(const uint4*)o;
       *(float4*)cs = make_float4(c[0], c[1], c[2], c[3]);
