@@ -1772,8 +1772,14 @@ class Engine {
     // embedding grads: deterministic segmented scatter (tensor.py:208-216)
     for (int t = 0; t < n_tables; ++t) {
       if (nuniq[t] == 0) continue;
-      scatter_compact_kernel<<<nuniq[t], 128, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t], gcomp[t]);
-      CMT_LAUNCHED(); tl_mark(st, "scatter_compact_kernel");
+      if (E % 4 == 0) {
+        scatter_compact_v4_kernel<<<nuniq[t], SCAT_THREADS, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t],
+                                                                       gcomp[t]);
+        CMT_LAUNCHED(); tl_mark(st, "scatter_compact_v4_kernel");
+      } else {
+        scatter_compact_kernel<<<nuniq[t], 128, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t], gcomp[t]);
+        CMT_LAUNCHED(); tl_mark(st, "scatter_compact_kernel");
+      }
     }
 
     // ===== data parallel: sum grads / loss / status over ranks (NCCL) =====
@@ -1804,7 +1810,7 @@ class Engine {
       CMT_LAUNCHED(); tl_mark(st, "sumsq_partial_kernel");
       nparts += NORM_BLOCKS;
     }
-    clip_scale_kernel<<<1, 32, 0, st>>>(normpart, nparts, a.lr, a.clip_norm, normscal_d, s32_d, status_d);
+    clip_scale_kernel<<<1, CLIP_THREADS, 0, st>>>(normpart, nparts, a.lr, a.clip_norm, normscal_d, s32_d, status_d);
     CMT_LAUNCHED(); tl_mark(st, "clip_scale_kernel");
     if (!(a.flags & CMT_FLAG_NO_UPDATE)) {
       sgd_dense_kernel<<<grid_for((long long)dense_n), 256, 0, st>>>(dw, dg, bf ? dsh : nullptr, (long long)dense_n, s32_d,

@@ -88,6 +88,45 @@ __global__ void scatter_compact_kernel(const float* __restrict__ dX, int E, cons
   }
 }
 
+// E % 4 == 0 variant: one float4 column group per thread, the segment's
+// positions staged 8 at a time, 8 rows in flight per thread.  Summation order
+// is fixed (8 interleaved partials combined as a tree), so it is deterministic.
+constexpr int SCAT_THREADS = 256;
+__global__ void __launch_bounds__(SCAT_THREADS) scatter_compact_v4_kernel(const float* __restrict__ dX, int E,
+                                                                          const int* __restrict__ seg_off,
+                                                                          const int* __restrict__ seg_pos, int nseg,
+                                                                          float* __restrict__ gout) {
+  const int u = blockIdx.x;
+  if (u >= nseg) return;
+  const int b = seg_off[u], e_ = seg_off[u + 1];
+  const int E4 = E >> 2;
+  for (int c = threadIdx.x; c < E4; c += blockDim.x) {
+    float4 acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p = b; p < e_; p += 8) {
+      int pos[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) pos[r] = p + r < e_ ? __ldg(seg_pos + p + r) : -1;
+      float4 v[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        v[r] = pos[r] >= 0 ? __ldg((const float4*)(dX + (long long)pos[r] * E) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        acc[r].x += v[r].x; acc[r].y += v[r].y; acc[r].z += v[r].z; acc[r].w += v[r].w;
+      }
+    }
+#pragma unroll
+    for (int w = 4; w; w >>= 1)
+#pragma unroll
+      for (int r = 0; r < w; ++r) {
+        acc[r].x += acc[r + w].x; acc[r].y += acc[r + w].y; acc[r].z += acc[r + w].z; acc[r].w += acc[r + w].w;
+      }
+    ((float4*)(gout + (long long)u * E))[c] = acc[0];
+  }
+}
+
 // dense[ids[u]][:] = rows[u][:]   (compact embedding grads -> dense, for DP all-reduce)
 __global__ void scatter_rows_kernel(const float* __restrict__ rows, int E, const int* __restrict__ ids, int n,
                                     float* __restrict__ dense) {
@@ -716,9 +755,18 @@ __global__ void sumsq_partial_kernel(const float* __restrict__ g, long long n, d
 // scal[0] = sum of squares, scal[1] = norm; s32 = fp32(lr * scale)
 __global__ void clip_scale_kernel(const double* __restrict__ part, int nparts, double lr, double clip,
                                   double* __restrict__ scal, float* __restrict__ s32, int* __restrict__ status) {
-  if (threadIdx.x != 0) return;
+  // fixed-shape reduction (strided per-thread sums, then a fixed tree), so the
+  // norm is deterministic; launched with CLIP_THREADS threads
+  __shared__ double red[32];
   double sq = 0.0;
-  for (int i = 0; i < nparts; ++i) sq += part[i];
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) sq += part[i];
+  sq = warp_sumd(sq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  sq = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+  sq = warp_sumd(sq);
+  if (threadIdx.x != 0) return;
   double norm = sqrt(sq);
   scal[0] = sq;
   scal[1] = norm;
@@ -727,6 +775,7 @@ __global__ void clip_scale_kernel(const double* __restrict__ part, int nparts, d
   if (clip > 0.0 && norm > clip) scale = clip / norm;
   *s32 = (float)(lr * scale);
 }
+constexpr int CLIP_THREADS = 512;
 
 constexpr int ST_ABORT = ST_SCORES | ST_LOGITS | ST_LOSS | ST_NORM;
 
