@@ -30,6 +30,7 @@
 #include "lstm_persistent.cuh"
 #include "lstm_cluster.cuh"
 #include "lstm_multi.cuh"
+#include "lstm_tm.cuh"
 #include "attention.cuh"
 
 namespace cmt {
@@ -382,6 +383,7 @@ class Engine {
   int clustered_fwd = 0;  // option: cluster K-split forward (slower than the plain persistent one at c3)
   int cg2 = 1;         // option: CTA-pair (cta_group::2) tiles for the large GEMMs
   int dual = 1;        // option: run independent scans of the layer graph two at a time
+  int fwd_tm = 1;      // option: forward scans with W_h split over smem + TMEM (lstm_tm.cuh)
   int use_jump = 1;    // option: table-driven PCG64 jump-ahead dropout kernel
   int ce2 = 1;         // option: fused CE + bias-grad column sums (persistent, 16-byte vectors)
   bool use_ce2() const { return bf && ce2 && V % 8 == 0 && V <= CE2_MAXV; }
@@ -966,7 +968,17 @@ class Engine {
     return bf && persistent && dual && H % (64 * F::KBOX) == 0 && H / 64 <= 32 && (H / 64) * nh <= FLAG_STRIDE &&
            F::ctas(H, B) <= g_num_sms && F::stages(H) >= 2;
   }
-  bool use_dual_fwd() const { return fwd_multi_ok<128>() && 2 * mc::Fwd<128>::ctas(H, B) <= g_num_sms; }
+  template <int ROWS>
+  bool fwd_tm_ok() const {
+    using F = tm::Fwd<ROWS>;
+    const int nh = (B + ROWS - 1) / ROWS;
+    return bf && persistent && fwd_tm && F::ok(H, B) && H / 64 <= 32 && (H / 64) * nh <= FLAG_STRIDE &&
+           F::ctas(H, B) <= g_num_sms;
+  }
+  bool dual_tm() const { return dual && fwd_tm_ok<64>() && 2 * tm::Fwd<64>::ctas(H, B) <= g_num_sms; }
+  bool use_dual_fwd() const {
+    return dual_tm() || (fwd_multi_ok<128>() && 2 * mc::Fwd<128>::ctas(H, B) <= g_num_sms);
+  }
   void fwd_prep(const FwdScan& f) {  // Ux = X W_x + b (layers.py:354-357, K3)
     const Layer& ly = layers[f.l];
     EpiStore e = store(f.uxb, 4LL * H, false);
@@ -989,8 +1001,43 @@ class Engine {
     CMT_CUDA(cudaMemsetAsync(prm.flag, 0, FLAG_STRIDE * 4, st));
     return prm;
   }
+  // lstm_fwd_tm<ROWS>: one or two scans per cooperative launch
+  template <int ROWS>
+  void fwd_tm_launch(const FwdScan& a, const FwdScan* b) {
+    using F = tm::Fwd<ROWS>;
+    CUtensorMap tmap[4];
+    LstmFwdMulti m;
+    auto prm = [&](const FwdScan& f, CUtensorMap* tmH, CUtensorMap* tmW) {
+      LstmFwdP r = fwd_params<128>(f, tmH, tmW);
+      make_map_kblocks(tmH, lw[f.l].yext, (long long)(f.steps + 1) * B, H, H, ROWS, F::KBOX);
+      r.stages = F::stages(H);
+      return r;
+    };
+    m.c[0] = prm(a, &tmap[0], &tmap[1]);
+    if (b) m.c[1] = prm(*b, &tmap[2], &tmap[3]);
+    else { m.c[1] = m.c[0]; tmap[2] = tmap[0]; tmap[3] = tmap[1]; }
+    const int g = F::ctas(H, B);
+    m.split = g;
+    auto k = lstm_fwd_tm<ROWS>;
+    const size_t smem = F::smem(H);
+    CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3(b ? 2 * g : g);
+    c.blockDim = dim3(tm::THREADS);
+    c.dynamicSmemBytes = smem;
+    c.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    c.attrs = at;
+    c.numAttrs = 1;
+    CMT_CUDA(cudaLaunchKernelEx(&c, k, tmap[0], tmap[1], tmap[2], tmap[3], m));
+    CMT_LAUNCHED();
+    tl_mark(st, b ? "lstm_fwd_tm_pair" : "lstm_fwd_tm_single");
+  }
   // two independent scans in one cooperative launch (64 CTAs each at H=1024, B=128)
   void fwd_pair(const FwdScan& a, const FwdScan& b) {
+    if (dual_tm()) return fwd_tm_launch<64>(a, &b);
     CUtensorMap tm[4];
     LstmFwdMulti m;
     m.c[0] = fwd_params<128>(a, &tm[0], &tm[1]);
@@ -1045,6 +1092,16 @@ class Engine {
   }
 
   void scan_fwd(int l, const void* X, int din, int steps, bool reverse, const float* mask) {
+    // single scans: lstm_fwd_multi<64> (128 CTAs, 6.4 us/step at c3) beats the
+    // TMEM-split kernel with 32-row slices (6.9 us/step); the latter is kept
+    // behind fwd_tm=2 for measurement
+    if (fwd_tm == 2 && (fwd_tm_ok<32>() || fwd_tm_ok<64>())) {
+      FwdScan f{l, X, din, steps, reverse, mask, ux};
+      fwd_prep(f);
+      if (fwd_tm_ok<32>()) fwd_tm_launch<32>(f, nullptr);
+      else fwd_tm_launch<64>(f, nullptr);
+      return;
+    }
     if (const int rows = single_fwd_rows()) {
       FwdScan f{l, X, din, steps, reverse, mask, ux};
       fwd_prep(f);
@@ -2082,6 +2139,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "cluster") e->eng->clustered = (int)value;
     else if (k == "cg2") e->eng->cg2 = (int)value;
     else if (k == "dual") e->eng->dual = (int)value;
+    else if (k == "fwd_tm") e->eng->fwd_tm = (int)value;
     else if (k == "jump") e->eng->use_jump = (int)value;
     else if (k == "att_split") e->eng->att_split = (int)value;
     else if (k == "allow_empty_targets") e->eng->allow_empty_targets = (int)value;

@@ -82,6 +82,46 @@ __global__ void probe(const bf16* A, const bf16* B, float* D, int N) {
   if (warp == 0) ptx::tmem_dealloc(tmem, 256);
 }
 
+
+// MMA issue/execute rate: R rounds of 64 MMAs (M=128, N, K=16 each) with A
+// from TMEM (mode 0) or from smem (mode 1, MN-major 128B atoms), B from smem.
+template <int N>
+__global__ void rate(int mode, int nacc, int R, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = sm;               // 16 KB
+  uint8_t* sB = sm + 16384;       // N x 128 B (N <= 256)
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (16384 + N * 128) / 4; i += blockDim.x) ((uint32_t*)sm)[i] = 0x3c003c00u;
+  if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::fence_barrier_init(); }
+  if (warp == 0) ptx::tmem_alloc(&slot, 512);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t id_t = ptx::idesc_bf16(128, N, 0, 0), id_s = ptx::idesc_bf16(128, N, 1, 0);
+    long long t0 = clock64();
+    for (int r = 0; r < R; ++r) {
+      for (int i = 0; i < 64; ++i) {
+        uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(sB) + (i & 3) * 32, 16, 1024);
+        const uint32_t d = tmem + (uint32_t)((i % nacc) * N);  // nacc independent accumulators
+        if (mode == 0) umma_ts(d, tmem + 256 + (i & 31) * 8, bd, id_t, 1u);
+        else ptx::umma_bf16(d, ptx::smem_desc_sw128(ptx::smem_u32(sA) + (i & 3) * 2048, 8192, 1024), bd, id_s, 1u);
+      }
+      ptx::umma_commit(&bar);
+      ptx::mbar_wait(&bar, r & 1);
+    }
+    cyc[0] = clock64() - t0;
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) ptx::tmem_dealloc(tmem, 512);
+}
+
 int main() {
   const int M = 128, N = 64, K = 64;
   std::vector<bf16> hA(M * K), hB(N * K);
@@ -111,5 +151,37 @@ int main() {
       maxerr = fmax(maxerr, err);
     }
   printf("TMEM-A probe: %s (max err %g, %d bad of %d)\n", bad ? "MISMATCH" : "OK", maxerr, bad, M * N);
+  long long* dc;
+  cudaMalloc(&dc, 8);
+  cudaFuncSetAttribute(rate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 60000);
+  cudaFuncSetAttribute(rate<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 60000);
+  cudaFuncSetAttribute(rate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 60000);
+  cudaFuncSetAttribute(rate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 60000);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int R = 4000;
+  auto run = [&](int n, int mode, int nacc) {
+    float ms = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0);
+      if (n == 32) rate<32><<<1, 128, 60000>>>(mode, nacc, R, dc);
+      if (n == 64) rate<64><<<1, 128, 60000>>>(mode, nacc, R, dc);
+      if (n == 128) rate<128><<<1, 128, 60000>>>(mode, nacc, R, dc);
+      if (n == 256) rate<256><<<1, 128, 60000>>>(mode, nacc, R, dc);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+    }
+    long long c = 0;
+    cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+    double ns = ms * 1e6 / (R * 64.0);
+    printf("A %s N=%3d acc=%d: %.1f ns/MMA (%.1f clk64/MMA)  %.2f TFLOP/s per SM\n", mode ? "smem" : "TMEM", n, nacc, ns,
+           c / (R * 64.0), 2.0 * 128 * n * 16 / ns / 1e3);
+  };
+  for (int n : {32, 64, 128, 256}) run(n, 1, 1);
+  for (int n : {32, 64, 128}) run(n, 0, 1);
+  run(64, 1, 4);
+  run(64, 0, 4);
+  printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return bad ? 2 : 0;
 }

@@ -211,7 +211,8 @@ def test_drop_in_train_step_and_determinism(mode):
                                   (256, 64, 1024, 1, 256, 5, 4, True)])  # B=256: 128-row slices, two per scan
 def test_persistent_recurrence_matches_per_step_and_oracle(case):
     """The persistent recurrent kernels (default in bf16) against the per-step
-    tcgen05 path and the oracle, masked + unmasked, forward + reverse scans."""
+    tcgen05 path and the oracle, masked + unmasked, forward + reverse scans,
+    partial batch slices (B not a multiple of the slice rows)."""
     from paper_1802_07170_b200.engine import Engine
     from paper_1802_07170_b200.model import Batch
     from tests.gpu_helpers import cfg_of
@@ -225,7 +226,9 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
         "per_step": dict(persistent=0, dual=0, cluster=0),
         "persistent": dict(persistent=1, dual=0, cluster=0),
         "cluster": dict(persistent=1, dual=0, cluster=1, cluster_fwd=1),
-        "dual": dict(),
+        "dual": dict(),  # paired forward scans in lstm_fwd_tm (W_h over smem + TMEM)
+        "dual_multi": dict(fwd_tm=0),  # paired forward scans in lstm_fwd_multi<128>
+        "tm_single": dict(fwd_tm=2),  # single forward scans in lstm_fwd_tm too
     }
     for variant, opts in variants.items():
         eng = Engine(cfg_of(d), mode="bf16")
@@ -235,7 +238,7 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
         eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, np.random.Generator(np.random.PCG64(3)), update=False)
         out[variant] = eng.grads()
         eng.close()
-    for v in ("persistent", "cluster", "dual"):
+    for v in ("persistent", "cluster", "dual", "dual_multi", "tm_single"):
         for n in og:
             assert O.norm_rel_err(out[v][n], out["per_step"][n]) < BF16_TOL, (v, n)
             assert O.norm_rel_err(out[v][n], og[n]) < BF16_TOL, (v, n)
