@@ -132,6 +132,48 @@ def cpu_oracle_rate(cfg_t, params, steps, warmup, sample_b=CPU_SAMPLE_B):
     return ntok / statistics.median(times), times
 
 
+def step_breakdown(tl):
+    """Group a per-launch timeline [(label, ms)] into kernel classes; keep the
+    GEMM launches (label 'gemm MxNxK tile') for the GEMM-only roofline."""
+    tot = sum(ms for _, ms in tl)
+    cls = {"recurrent scans": 0.0, "tcgen05 GEMMs": 0.0, "CE + column sums": 0.0, "SGD + norm": 0.0,
+           "attention core": 0.0, "dropout": 0.0, "other": 0.0}
+    gemms = []
+    for lab, ms in tl:
+        if lab.startswith("gemm "):
+            m, n, k = (int(x) for x in lab.split()[1].split("x"))
+            gemms.append((m, n, k, ms))
+            cls["tcgen05 GEMMs"] += ms
+        elif lab.startswith("lstm"):
+            cls["recurrent scans"] += ms
+        elif lab.startswith(("ce_", "colsum", "sum_to")):
+            cls["CE + column sums"] += ms
+        elif lab.startswith(("sgd", "sumsq", "clip")):
+            cls["SGD + norm"] += ms
+        elif lab.startswith("attn"):
+            cls["attention core"] += ms
+        elif lab.startswith("dropout"):
+            cls["dropout"] += ms
+        else:
+            cls["other"] += ms
+    shares = {k: round(v / tot, 4) for k, v in cls.items()} if tot > 0 else {}
+    shares["serialized_step_ms"] = round(tot, 4)
+    return {"shares": shares, "gemms": gemms}
+
+
+def gemm_roofline(bd, peak_tf):
+    """GEMM-only fraction: sum of 2MNK over the step's tcgen05
+    GEMM launches / their summed device time / the bf16 peak."""
+    if not bd or not bd["gemms"]:
+        return None
+    fl = sum(2.0 * m * n * k for m, n, k, _ in bd["gemms"])
+    ms = sum(x[3] for x in bd["gemms"])
+    ach = fl / (ms / 1e3) / 1e12
+    return {"achieved": ach, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf, "launches": len(bd["gemms"]),
+            "flops_per_step": fl, "ms_per_step": ms,
+            "source": "per-launch CUDA events on the engine stream (one untimed step, side stream off)"}
+
+
 def run_reference(args, cfg_t):
     """--impl reference: the reference's CPU implementation of the path, timed here."""
     from paper_1802_07170_b200.model import Model, ModelConfig, Rng
@@ -226,6 +268,16 @@ def main():
     eng.set_option("time_dominant", 0)
     ck = clocks.stop()
 
+    # ---- per-launch breakdown of one (untimed) step: CUDA events after every
+    # launch on the engine stream (the side-stream overlap is off in this mode) ----
+    breakdown = None
+    if rank == 0:
+        eng.set_option("timeline", 1)
+        eng.run(lr, clip, eps, rng, global_ntok=ntok_global)
+        tl = eng.timeline()
+        eng.set_option("timeline", 0)
+        breakdown = step_breakdown(tl)
+
     # ---- end-to-end through the public API (host buffers, H2D + D2H inside) ----
     if dist:
         dist.barrier()
@@ -279,6 +331,8 @@ def main():
                      "frac": (achieved / peak_tf) if achieved else None, "traffic": traffic,
                      "flops_per_launch": dom_flops, "launch_ms": dom_ms, "launches_timed": dom_n,
                      "peak_source": peak_src},
+        "gemm_roofline": gemm_roofline(breakdown, peak_tf),
+        "breakdown": breakdown and breakdown["shares"],
         "step_roofline": {"flops_per_step": fstep, "achieved_tflops": fstep / (ms_step / 1e3) / 1e12,
                           "frac": fstep / (ms_step / 1e3) / 1e12 / peak_tf},
         "src_tok_per_s": world * float(sm.sum()) / (ms_step / 1e3),
