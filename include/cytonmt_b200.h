@@ -89,6 +89,17 @@ int cmt_upload_param(cmt_engine* e, int idx, const float* host_rowmajor, long lo
 int cmt_download_param(cmt_engine* e, int idx, float* host_rowmajor, long long rows, long long cols);
 int cmt_download_grad(cmt_engine* e, int idx, float* host_rowmajor, long long rows, long long cols);
 
+/* device-resident parameter snapshots: replaces the host round trip of
+ * ModelParams.copy_data / load_data (model.py:104-115) that the Trainer uses
+ * to keep and restore its best parameters (training.py:205, 246-254, 269).
+ * slot in [0, 4); save/restore copy the fp32 masters device-to-device (restore
+ * also refreshes the bf16 shadows); download reads one block of a saved slot in
+ * the reference layout (like cmt_download_param); free releases the slot. */
+int cmt_snapshot_save(cmt_engine* e, int slot);
+int cmt_snapshot_restore(cmt_engine* e, int slot);
+int cmt_snapshot_download(cmt_engine* e, int slot, int idx, float* host_rowmajor, long long rows, long long cols);
+int cmt_snapshot_free(cmt_engine* e, int slot);
+
 /* batch (data.py:108-122): ids int64 (steps, batch) C order; masks float32 {0,1} */
 int cmt_stage_batch(cmt_engine* e, const long long* src_ids, const float* src_mask, int S,
                     const long long* tgt_ids, const float* tgt_mask, int T, int B);

@@ -454,6 +454,11 @@ class Engine {
       if (i == 0 || !cfg.shared_embeddings) { cudaFree(emb_w[i]); cudaFree(emb_sh[i]); }
     }
     cudaFree(ws);
+    for (auto& sn : snaps) {
+      if (sn.dense) cudaFree(sn.dense);
+      for (int t = 0; t < n_tables; ++t)
+        if (sn.emb[t]) cudaFree(sn.emb[t]);
+    }
     if (jump_d) cudaFree(jump_d);
     for (int t = 0; t < 2; ++t) if (demb[t]) cudaFree(demb[t]);
     if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
@@ -572,14 +577,16 @@ class Engine {
     CMT_LAUNCHED(); tl_mark(st, "to_bf16_kernel");
     CMT_CUDA(cudaStreamSynchronize(st));
   }
-  void download(int idx, float* h, long long rows, long long cols, bool grad) {
+  void download(int idx, float* h, long long rows, long long cols, bool grad, int snap = -1) {
     check_block(idx, rows, cols);
     CMT_CUDA(cudaStreamSynchronize(st));
     const BlockInfo& b = blocks[idx];
-    const float* base = grad ? dg : dw;
+    if (snap >= 0 && !snaps[snap].dense) throw Error(CMT_ERR_CONFIG, "snapshot slot is empty");
+    const float* base = snap >= 0 ? snaps[snap].dense : grad ? dg : dw;
     if (b.kind == BK_EMB) {
       if (!grad) {
-        copy_sync(h, emb_w[b.table], (size_t)rows * cols * 4, cudaMemcpyDeviceToHost);
+        copy_sync(h, snap >= 0 ? snaps[snap].emb[b.table] : emb_w[b.table], (size_t)rows * cols * 4,
+                  cudaMemcpyDeviceToHost);
       } else {
         std::memset(h, 0, (size_t)rows * cols * 4);
         int t = b.table;
@@ -609,6 +616,53 @@ class Engine {
       copy_sync(tmp.data(), base + ly.b_off, n4 * 4, cudaMemcpyDeviceToHost);
       for (int j = 0; j < H; ++j) h[j] = tmp[4 * j + b.gate];
     }
+  }
+
+  // ---- device-resident parameter snapshots (ModelParams.copy_data/load_data,
+  // model.py:104-115; the Trainer's restore-from-best, training.py:246-254):
+  // fp32 masters copied device-to-device, no host round trip ----
+  struct Snapshot {
+    float* dense = nullptr;
+    float* emb[2] = {nullptr, nullptr};
+  };
+  static constexpr int NSNAP = 4;
+  Snapshot snaps[NSNAP];
+  void check_slot(int slot) const {
+    if (slot < 0 || slot >= NSNAP) throw Error(CMT_ERR_CONFIG, "snapshot slot out of range");
+  }
+  void snapshot_save(int slot) {
+    check_slot(slot);
+    Snapshot& sn = snaps[slot];
+    if (!sn.dense) {
+      CMT_CUDA(cudaMalloc(&sn.dense, dense_n * 4));
+      for (int t = 0; t < n_tables; ++t) CMT_CUDA(cudaMalloc(&sn.emb[t], (size_t)V * E * 4));
+    }
+    CMT_CUDA(cudaMemcpyAsync(sn.dense, dw, dense_n * 4, cudaMemcpyDeviceToDevice, st));
+    for (int t = 0; t < n_tables; ++t)
+      CMT_CUDA(cudaMemcpyAsync(sn.emb[t], emb_w[t], (size_t)V * E * 4, cudaMemcpyDeviceToDevice, st));
+    CMT_CUDA(cudaStreamSynchronize(st));
+  }
+  void snapshot_restore(int slot) {
+    check_slot(slot);
+    const Snapshot& sn = snaps[slot];
+    if (!sn.dense) throw Error(CMT_ERR_CONFIG, "snapshot slot is empty");
+    CMT_CUDA(cudaMemcpyAsync(dw, sn.dense, dense_n * 4, cudaMemcpyDeviceToDevice, st));
+    for (int t = 0; t < n_tables; ++t)
+      CMT_CUDA(cudaMemcpyAsync(emb_w[t], sn.emb[t], (size_t)V * E * 4, cudaMemcpyDeviceToDevice, st));
+    if (bf) {
+      refresh_shadow(dw, dsh, dense_n);
+      for (int t = 0; t < n_tables; ++t) refresh_shadow(emb_w[t], emb_sh[t], (size_t)V * E);
+    }
+    CMT_CUDA(cudaStreamSynchronize(st));
+  }
+  void snapshot_free(int slot) {
+    check_slot(slot);
+    Snapshot& sn = snaps[slot];
+    CMT_CUDA(cudaStreamSynchronize(st));
+    if (sn.dense) cudaFree(sn.dense);
+    for (int t = 0; t < n_tables; ++t)
+      if (sn.emb[t]) cudaFree(sn.emb[t]);
+    sn = Snapshot();
   }
 
   // ---- workspace carving for (S, T, B) ----
@@ -2035,6 +2089,21 @@ int cmt_upload_param(cmt_engine* e, int idx, const float* h, long long rows, lon
 }
 int cmt_download_param(cmt_engine* e, int idx, float* h, long long rows, long long cols) {
   return guard(e, [&] { e->eng->download(idx, h, rows, cols, false); });
+}
+int cmt_snapshot_save(cmt_engine* e, int slot) {
+  return guard(e, [&] { e->eng->snapshot_save(slot); });
+}
+int cmt_snapshot_restore(cmt_engine* e, int slot) {
+  return guard(e, [&] { e->eng->snapshot_restore(slot); });
+}
+int cmt_snapshot_free(cmt_engine* e, int slot) {
+  return guard(e, [&] { e->eng->snapshot_free(slot); });
+}
+int cmt_snapshot_download(cmt_engine* e, int slot, int idx, float* h, long long rows, long long cols) {
+  return guard(e, [&] {
+    e->eng->check_slot(slot);
+    e->eng->download(idx, h, rows, cols, false, slot);
+  });
 }
 int cmt_download_grad(cmt_engine* e, int idx, float* h, long long rows, long long cols) {
   return guard(e, [&] { e->eng->download(idx, h, rows, cols, true); });

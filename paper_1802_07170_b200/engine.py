@@ -10,6 +10,7 @@ caller's generator is then advanced by the number of draws consumed).
 from __future__ import annotations
 
 import ctypes
+from collections.abc import Mapping
 
 import numpy as np
 
@@ -58,6 +59,49 @@ def dropout_draws(cfg, S, T, B):
         return 0
     L, H = cfg.depth, cfg.hidden_size
     return H * B * ((L - 1) * S + (L - 1) * T + T)
+
+
+NSNAP = 4  # device snapshot slots (include/cytonmt_b200.h)
+
+
+class DeviceSnapshot(Mapping):
+    """Parameters saved on the device by Engine.snapshot().  Behaves like the
+    reference's ``ModelParams.copy_data()`` dict (model.py:104-106): keys are
+    the block names in registry order and ``snap[name]`` is an fp32 array (read
+    from the device slot on first access).  ``Engine.restore`` / the installed
+    ``ModelParams.load_data`` restore it without a host round trip."""
+
+    def __init__(self, engine, slot):
+        self.engine, self.slot, self.alive = engine, slot, True
+        self._cache = {}
+
+    def __getitem__(self, name):
+        if name not in self._cache:
+            eng = self.engine
+            if not self.alive or eng.h is None:
+                raise ConfigError("device snapshot was released")
+            i = eng.index[name]
+            out = np.empty(eng.blocks[i][1], dtype=np.float32)
+            eng._check(eng.lib.cmt_snapshot_download(eng.h, self.slot, i, _fptr(out), out.shape[0], out.shape[1]))
+            self._cache[name] = out
+        return self._cache[name]
+
+    def __iter__(self):
+        return (n for n, _ in self.engine.blocks)
+
+    def __len__(self):
+        return len(self.engine.blocks)
+
+    def release(self):
+        if self.alive and getattr(self.engine, "h", None):
+            self.engine.lib.cmt_snapshot_free(self.engine.h, self.slot)
+        self.alive = False
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
 
 
 class Engine:
@@ -133,6 +177,26 @@ class Engine:
 
     def grads(self):
         return {n: self._download(self.lib.cmt_download_grad, n) for n, _ in self.blocks}
+
+    # ---- device snapshots (ModelParams.copy_data / load_data, model.py:104-115) ----
+    def snapshot(self):
+        """Save the current parameters on the device; returns a DeviceSnapshot
+        (a read-only {name: array} mapping that downloads blocks on access), or
+        None when all snapshot slots are in use."""
+        used = {sn.slot for sn in list(getattr(self, "_snaps", ())) if sn.alive}
+        free = [i for i in range(NSNAP) if i not in used]
+        if not free:
+            return None
+        sn = DeviceSnapshot(self, free[0])
+        self._check(self.lib.cmt_snapshot_save(self.h, sn.slot))
+        self._snaps = [x for x in getattr(self, "_snaps", ()) if x.alive] + [sn]
+        return sn
+
+    def restore(self, snap):
+        """Load a DeviceSnapshot of this engine back into the parameters (device to device)."""
+        if not isinstance(snap, DeviceSnapshot) or snap.engine is not self or not snap.alive:
+            raise ConfigError("restore needs a live snapshot of this engine")
+        self._check(self.lib.cmt_snapshot_restore(self.h, snap.slot))
 
     def download_into(self, params):
         for b in params.blocks():

@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import weakref
 
-from .engine import Engine
+from .engine import DeviceSnapshot, Engine
 
 _ENGINES: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 DEFAULTS = {"mode": "bf16", "sync": "eager", "device": 0}
@@ -65,14 +65,17 @@ def dev_entropy(model, dev_batches, *, mode=None):
     return engine_for(model, mode).dev_entropy(dev_batches)
 
 
-def install(training_module=None, sync="lazy"):
+def install(training_module=None, sync="lazy", params_cls=None):
     """Patch a reference ``minmt.training`` module to use this engine.
 
     ``Trainer.train`` resolves ``train_step`` as a module global at call time
     (training.py:232), so replacing it is sufficient for the step.  With
     ``sync="lazy"`` the host-side readers of parameters are wrapped so the
-    device copy is fetched first (dev_entropy, save_checkpoint) and pushed
-    after host writes (ModelParams.load_data).
+    device copy is fetched first (save_checkpoint), ``ModelParams.copy_data``
+    returns a device-resident snapshot (a read-only name -> array mapping) that
+    ``ModelParams.load_data`` restores device-to-device (the Trainer's
+    restore-from-best, training.py:205, 246-254, 269), and other host writes
+    through ``load_data`` are pushed to the device.
     """
     if training_module is None:
         import minmt.training as training_module  # type: ignore
@@ -87,20 +90,42 @@ def install(training_module=None, sync="lazy"):
             return orig_save(path, model, vocab_tokens)
 
         training_module.save_checkpoint = save_checkpoint
-        params_cls = None
-        try:
-            from minmt.model import ModelParams as params_cls  # type: ignore
-        except Exception:
-            pass
+        if params_cls is None:
+            try:
+                from minmt.model import ModelParams as params_cls  # type: ignore
+            except Exception:
+                params_cls = None
         if params_cls is not None and not getattr(params_cls, "_cmt_patched", False):
             orig_load = params_cls.load_data
+            orig_copy = params_cls.copy_data
+
+            def _engine_of(params):
+                for m, eng in list(_ENGINES.items()):
+                    if m.params is params:
+                        return eng
+                return None
+
+            def copy_data(self):
+                # the Trainer keeps the best parameters (training.py:205, 246) and
+                # hands them back to load_data: keep them on the device
+                eng = _engine_of(self)
+                if eng is not None:
+                    snap = eng.snapshot()
+                    if snap is not None:
+                        return snap
+                    eng.download_into(self)  # all slots in use: host copy of the device params
+                return orig_copy(self)
 
             def load_data(self, snapshot):
+                eng = _engine_of(self)
+                if eng is not None and isinstance(snapshot, DeviceSnapshot) and snapshot.engine is eng:
+                    eng.restore(snapshot)  # device to device (training.py:254, 269)
+                    return
                 orig_load(self, snapshot)
-                for m, eng in list(_ENGINES.items()):
-                    if m.params is self:
-                        eng.upload(self)
+                if eng is not None:
+                    eng.upload(self)
 
+            params_cls.copy_data = copy_data
             params_cls.load_data = load_data
             params_cls._cmt_patched = True
     return training_module

@@ -346,3 +346,51 @@ def test_dev_entropy_drop_in_and_empty_batch():
     assert abs(val - ref) <= BF16_TOL * ref, (val, ref)
     with pytest.raises(ConfigError):
         training.dev_entropy(model, [], mode="bf16")
+
+
+@pytest.mark.gpu
+def test_device_snapshot_and_restore_from_best():
+    """ModelParams.copy_data / load_data through install(sync="lazy"): the
+    snapshot stays on the device (a read-only name -> array mapping equal to the
+    parameters at that point), load_data restores it device-to-device exactly,
+    and a plain host dict still round-trips (model.py:104-115, training.py:246-254)."""
+    import types
+
+    from paper_1802_07170_b200 import training as TR
+    from paper_1802_07170_b200.engine import DeviceSnapshot
+    from paper_1802_07170_b200.model import Batch, Model, ModelConfig, ModelParams, Rng, TrainConfig
+    saved = (ModelParams.copy_data, ModelParams.load_data, dict(TR.DEFAULTS))
+    fake = types.SimpleNamespace(train_step=None, dev_entropy=None, save_checkpoint=lambda path, model, vocab: None)
+    try:
+        TR.install(fake, sync="lazy", params_cls=ModelParams)
+        cfg = ModelConfig(96, 32, 256, 2, 0.2)
+        model = Model.new(cfg, Rng(1))
+        src, sm, tgt, tm = O.synthetic_batch(96, 7, 6, 8, seed=2, ragged=True)
+        batch, tcfg, rng = Batch(src, tgt, sm, tm), TrainConfig(), Rng(5)
+        fake.train_step(model, batch, tcfg, 1.0, rng)
+        snap = model.params.copy_data()
+        assert isinstance(snap, DeviceSnapshot) and list(snap) == [b.name for b in model.params.blocks()]
+        TR.sync_to_host(model)
+        ref = {b.name: b.var.data.copy() for b in model.params.blocks()}
+        for n in ref:
+            assert np.array_equal(snap[n], ref[n]), n
+        for _ in range(2):
+            fake.train_step(model, batch, tcfg, 1.0, rng)
+        eng = TR.engine_for(model)
+        moved = eng.params()
+        assert any(not np.array_equal(moved[n], ref[n]) for n in ref)
+        model.params.load_data(snap)
+        back = eng.params()
+        for n in ref:
+            assert np.array_equal(back[n], ref[n]), n
+        host = {n: (0.5 * v).astype(np.float32) for n, v in ref.items()}
+        model.params.load_data(host)
+        got = eng.params()
+        for n in ref:
+            assert np.array_equal(got[n], host[n]), n
+        snap.release()
+    finally:
+        ModelParams.copy_data, ModelParams.load_data = saved[0], saved[1]
+        ModelParams._cmt_patched = False
+        TR.DEFAULTS.clear()
+        TR.DEFAULTS.update(saved[2])
