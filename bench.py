@@ -281,10 +281,14 @@ def main():
     # ---- end-to-end through the public API (host buffers, H2D + D2H inside) ----
     if dist:
         dist.barrier()
+    # Engine.pipeline: the public training-loop API; every step stages its
+    # batch from host arrays (validation, id conversion, segment sort, pinned
+    # H2D) and reads its loss back, the host work of step i+1 overlapping the
+    # device work of step i
     eng.record(2)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        loss, _ = eng.step(batch, lr, clip, eps, rng)
+    for loss, _ in eng.pipeline((batch for _ in range(args.steps)), lr, clip, eps, rng, global_ntok=ntok_global):
+        pass
     t_e2e = time.perf_counter() - t0
     eng.record(3)
     ms_e2e_dev = eng.elapsed_ms(2, 3)

@@ -420,7 +420,9 @@ class Engine {
   int* status_d;
   double* losssum_d;
   double* normscal_d;
-  Pinned pin_in, pin_out;
+  Pinned pin_in[2], pin_out;  // batch staging is double-buffered (see stage())
+  cudaEvent_t pin_ev[2] = {nullptr, nullptr};
+  int pin_cur = 0;
   StepOut* out_h = nullptr;
   // host copies of the staged segment info (for grad download)
   std::vector<int> uniq_h[2];
@@ -442,6 +444,7 @@ class Engine {
     CMT_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
     CMT_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     CMT_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    for (auto& e : pin_ev) CMT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : ev) CMT_CUDA(cudaEventCreate(&e));
     build_registry();
     alloc_params();
@@ -467,6 +470,7 @@ class Engine {
     cudaStreamDestroy(st2);
     cudaEventDestroy(ev_fork);
     cudaEventDestroy(ev_join);
+    for (auto& e : pin_ev) cudaEventDestroy(e);
   }
 
   static size_t al(size_t x) { return (x + 63) & ~(size_t)63; }
@@ -789,8 +793,12 @@ class Engine {
     ensure_ws(S_, T_, B_);
     // pinned staging: ids (int32) + masks + segments
     size_t nbytes = (size_t)(NS + 2 * NT) * 4 + (size_t)(NS + NT) * 4 + 2 * (size_t)(3 * (NS + NT) + 2) * 4;
-    char* p = (char*)pin_in.get(nbytes);
-    CMT_CUDA(cudaStreamSynchronize(st));  // previous step may still read the staging buffer
+    // two pinned buffers: this batch's host work (conversion, segment sort)
+    // overlaps the step still running on the device; only the copies issued
+    // from the same buffer two batches ago must have landed
+    const int k = pin_cur ^= 1;
+    CMT_CUDA(cudaEventSynchronize(pin_ev[k]));
+    char* p = (char*)pin_in[k].get(nbytes);
     int* h_src = (int*)p;
     int* h_tin = h_src + NS;
     int* h_tout = h_tin + NT;
@@ -854,6 +862,7 @@ class Engine {
       build(0, ka);
       build(1, kb);
     }
+    CMT_CUDA(cudaEventRecord(pin_ev[k], st));
     staged = true;
   }
 

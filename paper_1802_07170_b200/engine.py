@@ -239,8 +239,7 @@ class Engine:
         self._check(self.lib.cmt_wait(self.h, ctypes.byref(r)))
         return r
 
-    def step(self, batch, lr, clip, eps, rng=None, update=True):
-        """Stage + run: returns (loss, grad_norm)."""
+    def _stage_batch(self, batch, rng):
         src, tgt = batch.src_ids, batch.tgt_ids
         try:
             self.stage(src, batch.src_mask, tgt, batch.tgt_mask)
@@ -253,7 +252,41 @@ class Engine:
                 if n:
                     getattr(rng, "gen", rng).bit_generator.advance(n)
             raise
+
+    def step(self, batch, lr, clip, eps, rng=None, update=True):
+        """Stage + run: returns (loss, grad_norm)."""
+        self._stage_batch(batch, rng)
         r = self.run(lr, clip, eps, rng, update)
+        return r.loss, r.grad_norm
+
+    def pipeline(self, batches, lr, clip, eps, rng=None, global_ntok=0.0):
+        """Train on ``batches`` in order, yielding (loss, grad_norm) per batch.
+
+        Same results as calling ``step`` per batch (same updates, same draws),
+        but batch i+1 is validated, converted, segment-sorted and copied into
+        pinned memory on the host while step i still runs on the device (the
+        staging buffers are double-buffered); step i's result is read back
+        before step i+1 is launched.  A NumericError of step i is raised when
+        its result is collected (the device already skipped its update)."""
+        pending = False
+        for batch in batches:
+            try:
+                self._stage_batch(batch, rng)
+            except Exception:
+                if pending:
+                    pending = False
+                    yield self._finish()
+                raise
+            if pending:
+                pending = False
+                yield self._finish()
+            self.run(lr, clip, eps, rng, asynchronous=True, global_ntok=global_ntok)
+            pending = True
+        if pending:
+            yield self._finish()
+
+    def _finish(self):
+        r = self.wait()
         return r.loss, r.grad_norm
 
     def dev_entropy(self, batches):

@@ -394,3 +394,36 @@ def test_device_snapshot_and_restore_from_best():
         ModelParams._cmt_patched = False
         TR.DEFAULTS.clear()
         TR.DEFAULTS.update(saved[2])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+def test_pipeline_matches_sequential_steps(mode):
+    """Engine.pipeline (batch i+1 staged on the host while step i runs, staging
+    double-buffered, shapes changing between batches) gives exactly the losses,
+    parameters and generator state of one Engine.step per batch."""
+    from paper_1802_07170_b200.engine import Engine
+    from paper_1802_07170_b200.model import Batch
+    from tests.gpu_helpers import cfg_of
+    d = O.Dims(96, 32, 256, 2, 0.2)
+    params = scaled_params(d, 4, 0.1)
+    shapes = [(7, 6, 8), (9, 5, 8), (7, 6, 8), (5, 8, 12)]
+    batches = []
+    for i, (S, T, B) in enumerate(shapes):
+        src, sm, tgt, tm = O.synthetic_batch(96, S, T, B, seed=10 + i, ragged=True)
+        batches.append(Batch(src, tgt, sm, tm))
+    out = []
+    for piped in (False, True):
+        eng = Engine(cfg_of(d), mode=mode)
+        eng.upload(params)
+        gen = np.random.Generator(np.random.PCG64(9))
+        if piped:
+            losses = [l for l, _ in eng.pipeline(iter(batches), 1.0, 5.0, 0.1, gen)]
+        else:
+            losses = [eng.step(b, 1.0, 5.0, 0.1, gen)[0] for b in batches]
+        out.append((losses, eng.params(), gen.bit_generator.state))
+        eng.close()
+    assert out[0][0] == out[1][0]
+    assert out[0][2] == out[1][2]
+    for n in out[0][1]:
+        assert np.array_equal(out[0][1][n], out[1][1][n]), n
