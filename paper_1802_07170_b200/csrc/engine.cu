@@ -31,6 +31,7 @@
 #include "lstm_cluster.cuh"
 #include "lstm_multi.cuh"
 #include "lstm_tm.cuh"
+#include "lstm_tm_bwd.cuh"
 #include "attention.cuh"
 
 namespace cmt {
@@ -384,6 +385,10 @@ class Engine {
   int cg2 = 1;         // option: CTA-pair (cta_group::2) tiles for the large GEMMs
   int dual = 1;        // option: run independent scans of the layer graph two at a time
   int fwd_tm = 1;      // option: forward scans with W_h split over smem + TMEM (lstm_tm.cuh)
+  // option: BPTT scans with W_h split over smem + TMEM (lstm_tm_bwd.cuh; 1: paired scans, 2: also single).
+  // Off by default: at c3 it runs 12.3 us/step paired vs 11.5 for lstm_bwd_multi<128>
+  // (halving the dU stream does not pay for the slower MMA drain; profiles/r01/s3/trace_bwd.txt)
+  int bwd_tm = 0;
   int use_jump = 1;    // option: table-driven PCG64 jump-ahead dropout kernel
   int ce2 = 1;         // option: fused CE + bias-grad column sums (persistent, 16-byte vectors)
   bool use_ce2() const { return bf && ce2 && V % 8 == 0 && V <= CE2_MAXV; }
@@ -1246,11 +1251,61 @@ class Engine {
            (4 * H / 64) * ((B + ROWS - 1) / ROWS) <= FLAG_STRIDE && F::ctas(H, B) <= g_num_sms &&
            F::stages(H) >= 2 && (size_t)F::stages(H) * F::STAGE >= F::xbuf_bytes();
   }
-  bool use_dual_bwd() const { return bwd_multi_ok<128>() && 2 * mc::Bwd<128>::ctas(H, B) <= g_num_sms; }
+  template <int ROWS>
+  bool bwd_tm_ok() const {
+    using F = tmb::Bwd<ROWS>;
+    const int nh = (B + ROWS - 1) / ROWS;
+    return bf && persistent && bwd_tm && F::ok(H, B) && (H / 32) * nh <= FLAG_STRIDE && F::ctas(H, B) <= g_num_sms;
+  }
+  bool dual_bwd_tm() const { return dual && bwd_tm_ok<64>() && 2 * tmb::Bwd<64>::ctas(H, B) <= g_num_sms; }
+  bool use_dual_bwd() const {
+    return dual_bwd_tm() || (bwd_multi_ok<128>() && 2 * mc::Bwd<128>::ctas(H, B) <= g_num_sms);
+  }
+  template <int ROWS>
+  void bwd_tm_launch(const BwdScan& a, const BwdScan* b) {
+    using F = tmb::Bwd<ROWS>;
+    CUtensorMap tmap[4];
+    LstmBwdMulti m;
+    auto prm = [&](const BwdScan& f, CUtensorMap* tA, CUtensorMap* tW) {
+      LstmBwdP r = bwd_params<128>(f, tA, tW);
+      const Layer& ly = layers[f.l];
+      make_map_kblocks(tA, f.dUb, (long long)f.steps * B, 4LL * H, 4LL * H, ROWS, tmb::KBOX);
+      make_map(tW, wv(ly.w_off), 4LL * H, f.din + H, 4LL * H, 64, tmb::NU);
+      r.stages = F::stages(H);
+      return r;
+    };
+    m.c[0] = prm(a, &tmap[0], &tmap[1]);
+    if (b) m.c[1] = prm(*b, &tmap[2], &tmap[3]);
+    else { m.c[1] = m.c[0]; tmap[2] = tmap[0]; tmap[3] = tmap[1]; }
+    const int g = F::ctas(H, B);
+    m.split = g;
+    auto k = lstm_bwd_tm<ROWS>;
+    const size_t smem = F::smem(H);
+    CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3(b ? 2 * g : g);
+    c.blockDim = dim3(tmb::THREADS);
+    c.dynamicSmemBytes = smem;
+    c.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = tmb::KS_CL;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    c.attrs = at;
+    c.numAttrs = 2;
+    CMT_CUDA(cudaLaunchKernelEx(&c, k, tmap[0], tmap[1], tmap[2], tmap[3], m));
+    CMT_LAUNCHED();
+    tl_mark(st, b ? "lstm_bwd_tm_pair" : "lstm_bwd_tm_single");
+  }
   // one scan over batch slices of ROWS rows (64: two halves of B<=128; 128: B<=256)
   int single_bwd_rows() const { return bwd_multi_ok<64>() ? 64 : bwd_multi_ok<128>() ? 128 : 0; }
   void bwd_single(const BwdScan& f) {
-    if (single_bwd_rows() == 64) bwd_launch<64>(f, nullptr);
+    if (bwd_tm == 2 && bwd_tm_ok<32>()) bwd_tm_launch<32>(f, nullptr);
+    else if (bwd_tm == 2 && bwd_tm_ok<64>()) bwd_tm_launch<64>(f, nullptr);
+    else if (single_bwd_rows() == 64) bwd_launch<64>(f, nullptr);
     else bwd_launch<128>(f, nullptr);
     bwd_post(f);
   }
@@ -1301,7 +1356,10 @@ class Engine {
     CMT_LAUNCHED();
     tl_mark(st, b ? "lstm_bwd_pair" : "lstm_bwd_single");
   }
-  void bwd_pair(const BwdScan& a, const BwdScan& b) { bwd_launch<128>(a, &b); }
+  void bwd_pair(const BwdScan& a, const BwdScan& b) {
+    if (dual_bwd_tm()) bwd_tm_launch<64>(a, &b);
+    else bwd_launch<128>(a, &b);
+  }
   // weight grads, bias grads and input grads of a finished BPTT scan
   void bwd_post(const BwdScan& f) {
     const Layer& ly = layers[f.l];
@@ -2218,6 +2276,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "cg2") e->eng->cg2 = (int)value;
     else if (k == "dual") e->eng->dual = (int)value;
     else if (k == "fwd_tm") e->eng->fwd_tm = (int)value;
+    else if (k == "bwd_tm") e->eng->bwd_tm = (int)value;
     else if (k == "jump") e->eng->use_jump = (int)value;
     else if (k == "att_split") e->eng->att_split = (int)value;
     else if (k == "allow_empty_targets") e->eng->allow_empty_targets = (int)value;

@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
             const unsigned need = ((1u << mc::BWD_KBOX) - 1u) << (issued * mc::BWD_KBOX);
             if ((ready & need) != need) break;
             ptx::mbar_wait(&empty[stage], phase ^ 1);
+            if (p.trace && bid == 0 && (issued == 0 || issued == nst - 1)) p.trace[i * 8 + (issued ? 6 : 5)] = gtimer();
             ptx::tma_load_3d(tmA, &full[stage], sA + stage * F::STAGE, 0, arow, kb_base + issued * mc::BWD_KBOX);
             ptx::mbar_expect_tx(&full[stage], F::STAGE);
             if (++stage == p.stages) { stage = 0; phase ^= 1; }
@@ -414,6 +415,7 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
         for (int kb0 = 0; kb0 < KBL; kb0 += mc::BWD_KBOX) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (p.trace && bid == 0 && kb0 + mc::BWD_KBOX >= KBL) p.trace[i * 8 + 7] = gtimer();
           const uint32_t a0 = ptx::smem_u32(sA + stage * F::STAGE);
 #pragma unroll
           for (int j = 0; j < mc::BWD_KBOX; ++j) {

@@ -226,9 +226,9 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
         "per_step": dict(persistent=0, dual=0, cluster=0),
         "persistent": dict(persistent=1, dual=0, cluster=0),
         "cluster": dict(persistent=1, dual=0, cluster=1, cluster_fwd=1),
-        "dual": dict(),  # paired forward scans in lstm_fwd_tm (W_h over smem + TMEM)
-        "dual_multi": dict(fwd_tm=0),  # paired forward scans in lstm_fwd_multi<128>
-        "tm_single": dict(fwd_tm=2),  # single forward scans in lstm_fwd_tm too
+        "dual": dict(),  # default: paired forward scans in lstm_fwd_tm, paired BPTT in lstm_bwd_multi<128>
+        "dual_multi": dict(fwd_tm=0, bwd_tm=1),  # lstm_fwd_multi<128> / lstm_bwd_tm (W_h over smem + TMEM)
+        "tm_single": dict(fwd_tm=2, bwd_tm=2),  # single scans in the TMEM-split kernels too
     }
     for variant, opts in variants.items():
         eng = Engine(cfg_of(d), mode="bf16")
