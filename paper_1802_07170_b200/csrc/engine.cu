@@ -321,6 +321,12 @@ class Engine {
   // side stream for independent work of the two scans of a level (their input
   // projections / weight-gradient GEMMs overlap and pack each other's waves)
   cudaStream_t st2 = nullptr;
+  // data parallel: gradient buckets are all-reduced on stc as soon as the
+  // backward has produced them; the clip waits for stc
+  cudaStream_t stc = nullptr;
+  cudaEvent_t ev_ar[64] = {};
+  int n_ev_ar = 0;
+  int ar_overlap = 1;  // option: bucketed all-reduce overlapped with the backward (0: one all-reduce at the end)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int overlap = 1;      // option
   bool on_side = false;
@@ -413,8 +419,46 @@ class Engine {
     rank = rank_;
     world = world_;
     for (int t = 0; t < n_tables; ++t) CMT_CUDA(cudaMalloc(&demb[t], (size_t)V * E * 4));
+    CMT_CUDA(cudaStreamCreateWithFlags(&stc, cudaStreamNonBlocking));
+    for (auto& e : ev_ar) CMT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
+  // all-reduce (sum) of a finished gradient bucket on the comm stream, ordered
+  // after the work issued so far on the current stream.  Every rank issues the
+  // same buckets in the same (host program) order.
+  bool ar_buckets = false;    // this step all-reduces gradient buckets during the backward
+  std::vector<char> ar_done;  // per bucket: layers 0..2L, attention 2L+1, output 2L+2
+  void allreduce_region(int id) {
+    if (!ar_buckets || ar_done[id]) return;
+    ar_done[id] = 1;
+    if (id < (int)layers.size()) {
+      const Layer& ly = layers[id];
+      allreduce_bucket(dg + ly.w_off, ly.b_off + 4 * (size_t)H - ly.w_off);  // [W; b] of the layer
+    } else if (id == (int)layers.size()) {
+      allreduce_bucket(dg + off_wa, off_wo - off_wa);  // att.w_a, att.w_c
+    } else {
+      allreduce_bucket(dg + off_wo, dense_n - off_wo);  // out.w, out.b
+    }
+  }
+  void allreduce_bucket(void* buf, size_t n, int dtype = NCCL_FLOAT32) {
+    const int slot = n_ev_ar < 63 ? n_ev_ar++ : 63;  // events are reusable once waited on
+    CMT_CUDA(cudaEventRecord(ev_ar[slot], st));
+    CMT_CUDA(cudaStreamWaitEvent(stc, ev_ar[slot], 0));
+    nccl_check(g_nccl.all_reduce(buf, buf, n, dtype, NCCL_SUM, comm, stc), "ncclAllReduce");
+  }
+  void allreduce_join() {
+    if (!n_ev_ar) return;
+    CMT_CUDA(cudaEventRecord(ev_ar[0], stc));
+    CMT_CUDA(cudaStreamWaitEvent(st, ev_ar[0], 0));
+    n_ev_ar = 0;
+  }
+  // Every collective of a step is issued on ONE stream (stc while buckets are
+  // in flight, else the engine stream), so all ranks execute the shared
+  // communicator's operations in the same order.
   void allreduce(void* buf, size_t n, int dtype) {
+    if (ar_buckets) {
+      allreduce_bucket(buf, n, dtype);
+      return;
+    }
     nccl_check(g_nccl.all_reduce(buf, buf, n, dtype, NCCL_SUM, comm, st), "ncclAllReduce");
   }
   int trace_layer = -1;  // debug: record per-step phase timestamps of this layer's forward scan
@@ -470,6 +514,10 @@ class Engine {
     if (jump_d) cudaFree(jump_d);
     for (int t = 0; t < 2; ++t) if (demb[t]) cudaFree(demb[t]);
     if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
+    if (stc) {
+      cudaStreamDestroy(stc);
+      for (auto& e : ev_ar) cudaEventDestroy(e);
+    }
     for (auto& e : ev) cudaEventDestroy(e);
     cudaStreamDestroy(st);
     cudaStreamDestroy(st2);
@@ -1370,6 +1418,7 @@ class Engine {
     gemm(H, 4 * H, (int)N, Mat{v.hprev, H, 1}, Mat{f.dUb, 4LL * H, 1},
          store(dg + ly.w_off + (size_t)f.din * 4 * H, 4LL * H, false));
     colsum(f.dUb, true, N, 4 * H, dg + ly.b_off);
+    allreduce_region(f.l);
     if (f.dX) bwd_post_dx(f);
   }
   // dX = dU W_x^T (layers.py:392; K7), dropout backward fused (layers.py:292-296)
@@ -1764,11 +1813,15 @@ class Engine {
     // dW_o only feeds the update: on the side stream it overlaps dH_o and the
     // attention backward (joined before the BPTT scans)
     const bool ov_wo = use_overlap();
+    ar_buckets = comm != nullptr && ar_overlap && ov_wo;
+    ar_done.assign(layers.size() + 2, 0);
+    n_ev_ar = 0;
     if (ov_wo) {
       fork();
       on_side_stream([&]() {
         gemm(H, V, (int)NT, Mat{hin, H, 1}, Mat{Y, V, 1}, store(dg + off_wo, V, false));
         if (!fused_ce) colsum(Y, true, NT, V, dg + off_bo);
+        allreduce_region((int)layers.size() + 1);
       });
     } else {
       gemm(H, V, (int)NT, Mat{hin, H, 1}, Mat{Y, V, 1}, store(dg + off_wo, V, false));
@@ -1878,6 +1931,7 @@ class Engine {
       e.add = dcst + H; e.ld_add = 2LL * H;
       gemm((int)NT, H, H, Mat{du_att, H, 0}, Mat{wv(off_wa), H, 0}, e);
     }
+    allreduce_region((int)layers.size());
     if (ov_wo) join();
     // decoder BPTT, top layer first (graph.py:112-115); init-state grads -> encoder finals
     auto dec_scan = [&](int k, void* dub) {
@@ -1963,7 +2017,11 @@ class Engine {
     // ===== data parallel: sum grads / loss / status over ranks (NCCL) =====
     const bool dp = comm != nullptr;  // (a 1-rank communicator exercises the same path)
     if (dp) {
-      allreduce(dg, dense_n, NCCL_FLOAT32);
+      if (ar_buckets) {
+        for (int id = 0; id < (int)layers.size() + 2; ++id) allreduce_region(id);  // any not yet issued
+      } else {
+        allreduce(dg, dense_n, NCCL_FLOAT32);
+      }
       for (int t = 0; t < n_tables; ++t) {
         CMT_CUDA(cudaMemsetAsync(demb[t], 0, (size_t)V * E * 4, st));
         if (nuniq[t]) {
@@ -1974,6 +2032,7 @@ class Engine {
       }
       allreduce(losssum_d, 1, NCCL_FLOAT64);
       allreduce(status_d, 1, NCCL_INT32);
+      allreduce_join();
     }
     // ===== global-norm clip + SGD (training.py:123-142) =====
     int nparts = 0;
@@ -2277,6 +2336,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "dual") e->eng->dual = (int)value;
     else if (k == "fwd_tm") e->eng->fwd_tm = (int)value;
     else if (k == "bwd_tm") e->eng->bwd_tm = (int)value;
+    else if (k == "ar_overlap") e->eng->ar_overlap = (int)value;
     else if (k == "jump") e->eng->use_jump = (int)value;
     else if (k == "att_split") e->eng->att_split = (int)value;
     else if (k == "allow_empty_targets") e->eng->allow_empty_targets = (int)value;

@@ -257,18 +257,20 @@ def test_dp_path_single_rank_nccl_matches_plain(mode):
     params = scaled_params(d, 2, 0.1)
     src, sm, tgt, tm = O.synthetic_batch(96, 7, 6, 8, seed=2, ragged=True)
     out = []
-    for use_dp in (False, True):
+    for use_dp, ar_overlap in ((False, 1), (True, 1), (True, 0)):
         eng = Engine(cfg_of(d), mode=mode)
+        eng.set_option("ar_overlap", ar_overlap)  # bucketed all-reduce on the comm stream during the backward
         eng.upload(params)
         if use_dp:
             dp.attach(eng, None, 0, 1)
         loss, norm = eng.step(Batch(src, tgt, sm, tm), 1.0, 0.05, 0.1, None)
         out.append((loss, norm, eng.params()))
         eng.close()
-    assert abs(out[0][0] - out[1][0]) <= 1e-6 * abs(out[0][0])
-    assert abs(out[0][1] - out[1][1]) <= 1e-5 * out[0][1]
-    for n in out[0][2]:
-        assert O.norm_rel_err(out[1][2][n], out[0][2][n]) < 1e-6, n
+    for k in (1, 2):
+        assert abs(out[0][0] - out[k][0]) <= 1e-6 * abs(out[0][0])
+        assert abs(out[0][1] - out[k][1]) <= 1e-5 * out[0][1]
+        for n in out[0][2]:
+            assert O.norm_rel_err(out[k][2][n], out[0][2][n]) < 1e-6, n
 
 
 @pytest.mark.parametrize("case", [(304, 64, 128, 2, 24, 17, 13, True), (256, 128, 256, 1, 8, 64, 64, False),
