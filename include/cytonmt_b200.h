@@ -89,6 +89,19 @@ int cmt_upload_param(cmt_engine* e, int idx, const float* host_rowmajor, long lo
 int cmt_download_param(cmt_engine* e, int idx, float* host_rowmajor, long long rows, long long cols);
 int cmt_download_grad(cmt_engine* e, int idx, float* host_rowmajor, long long rows, long long cols);
 
+/* GPU translation.  decode_begin encodes one source
+ * sentence (ids int64, length S) with the INFER-mode forward and sets the
+ * decoder states to the encoder finals (model.py:180-208).  decode_step runs
+ * model.decode_step (model.py:211-236) for n <= 64 live hypotheses: row i
+ * feeds token prev_tokens[i] to the state row parent[i] of the previous call's
+ * output (parent = NULL: the encoder finals), and returns the k <= 32 best
+ * log-probabilities of each row with their token ids, ordered by log-prob
+ * descending then token ascending (the tie order of decoding.py:120-121).
+ * The host drives beam search / greedy decoding (decoding.py:89-184). */
+int cmt_decode_begin(cmt_engine* e, const long long* src_ids, int S);
+int cmt_decode_step(cmt_engine* e, int n, const long long* prev_tokens, const int* parent, int k,
+                    float* top_logprob, int* top_token);
+
 /* device-resident parameter snapshots: replaces the host round trip of
  * ModelParams.copy_data / load_data (model.py:104-115) that the Trainer uses
  * to keep and restore its best parameters (training.py:205, 246-254, 269).

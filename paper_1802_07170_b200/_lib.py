@@ -36,6 +36,7 @@ EXPORTS = [
     "cmt_run_step", "cmt_train_step", "cmt_wait", "cmt_set_comm", "cmt_nccl_unique_id", "cmt_event_record",
     "cmt_event_elapsed", "cmt_launch_count", "cmt_set_option", "cmt_get_stat", "cmt_debug_buffer", "cmt_test_gemm", "cmt_test_dropout", "cmt_timeline",
     "cmt_snapshot_save", "cmt_snapshot_restore", "cmt_snapshot_download", "cmt_snapshot_free",
+    "cmt_decode_begin", "cmt_decode_step",
 ]
 
 
@@ -86,6 +87,8 @@ def load(path=LIB_PATH):
     for f in (lib.cmt_snapshot_save, lib.cmt_snapshot_restore, lib.cmt_snapshot_free):
         f.argtypes = [VP, I]
     lib.cmt_snapshot_download.argtypes = [VP, I, I, fp, LL, LL]
+    lib.cmt_decode_begin.argtypes = [VP, llp, I]
+    lib.cmt_decode_step.argtypes = [VP, I, llp, P(I), I, fp, P(I)]
     lib.cmt_stage_batch.argtypes = [VP, llp, fp, I, llp, fp, I, I]
     lib.cmt_run_step.argtypes = [VP, P(StepArgs), P(StepResult)]
     lib.cmt_train_step.argtypes = [VP, llp, fp, I, llp, fp, I, I, P(StepArgs), P(StepResult)]

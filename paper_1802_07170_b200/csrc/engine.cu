@@ -33,6 +33,7 @@
 #include "lstm_tm.cuh"
 #include "lstm_tm_bwd.cuh"
 #include "attention.cuh"
+#include "decode.cuh"
 
 namespace cmt {
 unsigned long long g_launches = 0;
@@ -511,6 +512,7 @@ class Engine {
       for (int t = 0; t < n_tables; ++t)
         if (sn.emb[t]) cudaFree(sn.emb[t]);
     }
+    dec_free();
     if (jump_d) cudaFree(jump_d);
     for (int t = 0; t < 2; ++t) if (demb[t]) cudaFree(demb[t]);
     if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
@@ -720,6 +722,162 @@ class Engine {
     for (int t = 0; t < n_tables; ++t)
       if (sn.emb[t]) cudaFree(sn.emb[t]);
     sn = Snapshot();
+  }
+
+  // ---- GPU translation: encode one sentence with the
+  // training forward in INFER mode, then decode_step for n live hypotheses
+  // (model.py:180-236, driven by decoding.py:89-184) ----
+  static constexpr int DEC_NMAX = 64;
+  float *dec_hs = nullptr, *dec_fin = nullptr, *dec_st = nullptr, *dec_z = nullptr, *dec_u = nullptr;
+  float *dec_ho = nullptr, *dec_y = nullptr, *dec_part = nullptr, *dec_topv = nullptr;
+  int *dec_ids = nullptr, *dec_par = nullptr, *dec_topi = nullptr;
+  int dec_S = 0, dec_Smax = 0, dec_cur = 0;
+  bool dec_ready = false, dec_par_set = false;
+  size_t dec_part_n = 0;
+  long long dec_lstride() const { return (long long)DEC_NMAX * H; }
+  float* dec_h(int buf) { return dec_st + (size_t)buf * 2 * L * dec_lstride(); }
+  float* dec_c(int buf) { return dec_h(buf) + (size_t)L * dec_lstride(); }
+  void dec_alloc(int S_) {
+    if (!dec_z) {
+      const int zc = std::max(E + H, 2 * H);
+      CMT_CUDA(cudaMalloc(&dec_fin, (size_t)2 * L * H * 4));
+      CMT_CUDA(cudaMalloc(&dec_st, (size_t)2 * 2 * L * DEC_NMAX * H * 4));
+      CMT_CUDA(cudaMalloc(&dec_z, (size_t)DEC_NMAX * zc * 4));
+      CMT_CUDA(cudaMalloc(&dec_u, (size_t)DEC_NMAX * 4 * H * 4));
+      CMT_CUDA(cudaMalloc(&dec_ho, (size_t)DEC_NMAX * H * 4));
+      CMT_CUDA(cudaMalloc(&dec_y, (size_t)DEC_NMAX * V * 4));
+      const int kmax = std::max({E + H, 2 * H, H});
+      dec_part_n = (size_t)ceil_div(kmax, dec::KCH) * DEC_NMAX * std::max(4 * H, V);
+      CMT_CUDA(cudaMalloc(&dec_part, dec_part_n * 4));
+      CMT_CUDA(cudaMalloc(&dec_topv, (size_t)DEC_NMAX * dec::MAXK * 4));
+      CMT_CUDA(cudaMalloc(&dec_topi, (size_t)DEC_NMAX * dec::MAXK * 4));
+      CMT_CUDA(cudaMalloc(&dec_ids, DEC_NMAX * 4));
+      CMT_CUDA(cudaMalloc(&dec_par, DEC_NMAX * 4));
+    }
+    if (S_ > dec_Smax) {
+      if (dec_hs) cudaFree(dec_hs);
+      CMT_CUDA(cudaMalloc(&dec_hs, (size_t)S_ * H * 4));
+      dec_Smax = S_;
+    }
+  }
+  void dec_free() {
+    for (float* p : {dec_hs, dec_fin, dec_st, dec_z, dec_u, dec_ho, dec_y, dec_part, dec_topv})
+      if (p) cudaFree(p);
+    for (int* p : {dec_ids, dec_par, dec_topi})
+      if (p) cudaFree(p);
+  }
+  template <typename T>
+  void dec_cvt(const void* src, float* dst, long long n) {
+    copy2d_kernel<T, float><<<grid_for(n), 256, 0, st>>>((const T*)src, n, dst, n, 1, (int)n);
+    CMT_LAUNCHED();
+  }
+  void decode_begin(const long long* src, int S_) {
+    if (S_ < 1) throw Error(CMT_ERR_CONFIG, "cannot translate an empty source sentence");
+    std::vector<float> ones((size_t)S_, 1.f);
+    const long long eos = 3;
+    const float one = 1.f;
+    stage(src, ones.data(), S_, &eos, &one, 1, 1);
+    cmt_step_args a = {};
+    a.flags = CMT_FLAG_INFER;
+    a.pcg_inc_lo = 1;
+    cmt_step_result r = {};
+    run(a, &r);  // the training forward in INFER mode: encoder states for B = 1
+    if (r.status != CMT_OK) throw Error(r.status, "non-finite values while encoding the source");
+    dec_alloc(S_);
+    const void* Hs = (L == 1) ? top : views(L, false).ybase;
+    if (bf) dec_cvt<bf16>(Hs, dec_hs, (long long)S_ * H);
+    else CMT_CUDA(cudaMemcpyAsync(dec_hs, Hs, (size_t)S_ * H * 4, cudaMemcpyDeviceToDevice, st));
+    for (int k = 1; k <= L; ++k) {  // init_decoder_states (model.py:207-208): l1.bwd final, then enc.lk finals
+      const int el = (k == 1) ? 1 : k;
+      const size_t slot = (k == 1) ? 0 : (size_t)S_;  // B = 1
+      const void* hsrc = (const char*)lw[el].yext + slot * H * asz;
+      if (bf) dec_cvt<bf16>(hsrc, dec_fin + (size_t)(k - 1) * H, H);
+      else CMT_CUDA(cudaMemcpyAsync(dec_fin + (size_t)(k - 1) * H, hsrc, H * 4, cudaMemcpyDeviceToDevice, st));
+      CMT_CUDA(cudaMemcpyAsync(dec_fin + (size_t)(L + k - 1) * H, lw[el].cext + slot * H, H * 4,
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    CMT_CUDA(cudaStreamSynchronize(st));
+    dec_S = S_;
+    dec_cur = 0;
+    dec_ready = true;
+  }
+  template <typename T>
+  void dec_gemv(const float* Z, int ldz, int n, int K, const T* W, long long ldw, int N, const float* bias, int act,
+                float* Y, int ldy) {
+    const int ks = ceil_div(K, dec::KCH);
+    if ((size_t)ks * n * N > dec_part_n) throw Error(CMT_ERR_INTERNAL, "decode partials too small");
+    dim3 g(ceil_div(N, dec::GV_COLS), ks, ceil_div(n, dec::ROWS));
+    dec_gemv_partial<T><<<g, dec::GV_THREADS, 0, st>>>(Z, ldz, n, K, W, ldw, N, dec_part);
+    CMT_LAUNCHED();
+    dec_gemv_final<<<(int)ceil_div((long long)n * N, 256), 256, 0, st>>>(dec_part, ks, n, N, bias, act, Y, ldy);
+    CMT_LAUNCHED();
+  }
+  template <typename T>
+  void decode_step_t(int n, int k) {
+    const int zc = std::max(E + H, 2 * H);
+    const T* wts = bf ? (const T*)(const void*)dsh : (const T*)(const void*)dw;
+    const long long ls = dec_lstride();
+    const int in = dec_cur ^ 1, outb = dec_cur;  // gather the inputs into `in`, write new states to `outb`
+    // input states: the parents' new states of the previous step (or the encoder finals)
+    dim3 gg(n, L);
+    dec_gather_states<<<gg, 256, 0, st>>>(dec_h(dec_cur), dec_c(dec_cur), dec_fin, dec_fin + (size_t)L * H,
+                                          dec_par_set ? dec_par : nullptr, n, H, ls, dec_h(in), dec_c(in));
+    CMT_LAUNCHED();
+    const T* table = bf ? (const T*)(const void*)emb_sh[tgt_table()] : (const T*)(const void*)emb_w[tgt_table()];
+    dec_embed<T><<<n, 256, 0, st>>>(table, dec_ids, E, dec_z, zc);
+    CMT_LAUNCHED();
+    for (int k1 = 1; k1 <= L; ++k1) {  // decoder layers (lstm_cell_forward, layers.py:344-363)
+      const Layer& ly = layers[L + k1];
+      const int din = ly.din;
+      dec_copy_rows<<<n, 256, 0, st>>>(dec_h(in) + (k1 - 1) * ls, H, dec_z + din, zc, H);
+      CMT_LAUNCHED();
+      dec_gemv<T>(dec_z, zc, n, din + H, wts + ly.w_off, 4LL * H, 4 * H, dw + ly.b_off, 0, dec_u, 4 * H);
+      // the next layer's input (the x rows of z) is this layer's h
+      dec_lstm_cell<<<n, 256, 0, st>>>(dec_u, dec_c(in) + (k1 - 1) * ls, H, dec_h(outb) + (k1 - 1) * ls,
+                                       dec_c(outb) + (k1 - 1) * ls, k1 < L ? dec_z : nullptr, zc);
+      CMT_LAUNCHED();
+    }
+    const float* x = dec_h(outb) + (L - 1) * ls;  // top decoder h [n][H]
+    // attention (attend_values): u = W_a^T x; context; H_o = tanh(W_c^T [ctx; x])
+    dec_gemv<T>(x, H, n, H, wts + off_wa, H, H, nullptr, 0, dec_u, H);
+    dec_attention<<<n, 256, (size_t)dec_S * 4, st>>>(dec_hs, dec_S, H, dec_u, dec_z, zc);
+    CMT_LAUNCHED();
+    dec_copy_rows<<<n, 256, 0, st>>>(x, H, dec_z + H, zc, H);
+    CMT_LAUNCHED();
+    dec_gemv<T>(dec_z, zc, n, 2 * H, wts + off_wc, H, H, nullptr, 1, dec_ho, H);
+    // output layer (model.py:232-235), log-softmax and the k best entries per row
+    dec_gemv<T>(dec_ho, H, n, H, wts + off_wo, V, V, dw + off_bo, cfg.output_tanh ? 1 : 0, dec_y, V);
+    dec_logsoftmax_topk<<<n, dec::TOPK_THREADS, 0, st>>>(dec_y, V, k, dec_topv, dec_topi, status_d);
+    CMT_LAUNCHED();
+    dec_cur = outb;
+  }
+  void decode_step(int n, const long long* prev, const int* parent, int k, float* top_val, int* top_tok) {
+    if (!dec_ready) throw Error(CMT_ERR_CONFIG, "decode_step before decode_begin");
+    if (n < 1 || n > DEC_NMAX) throw Error(CMT_ERR_SHAPE, "decode_step: 1 <= n <= 64 hypotheses");
+    if (k < 1 || k > dec::MAXK || k > V) throw Error(CMT_ERR_SHAPE, "decode_step: 1 <= k <= min(32, V)");
+    std::vector<int> ids(n), par(n);
+    for (int i = 0; i < n; ++i) {
+      if (prev[i] < 0 || prev[i] >= V)
+        throw Error(CMT_ERR_CONFIG, "token id " + std::to_string(prev[i]) + " outside vocabulary of size " +
+                                        std::to_string(V));
+      ids[i] = (int)prev[i];
+      if (parent) {
+        if (parent[i] < 0 || parent[i] >= DEC_NMAX) throw Error(CMT_ERR_SHAPE, "decode_step: bad parent index");
+        par[i] = parent[i];
+      }
+    }
+    CMT_CUDA(cudaMemcpyAsync(dec_ids, ids.data(), n * 4, cudaMemcpyHostToDevice, st));
+    if (parent) CMT_CUDA(cudaMemcpyAsync(dec_par, par.data(), n * 4, cudaMemcpyHostToDevice, st));
+    dec_par_set = parent != nullptr;
+    CMT_CUDA(cudaMemsetAsync(status_d, 0, 4, st));
+    if (bf) decode_step_t<bf16>(n, k);
+    else decode_step_t<float>(n, k);
+    CMT_CUDA(cudaMemcpyAsync(top_val, dec_topv, (size_t)n * k * 4, cudaMemcpyDeviceToHost, st));
+    CMT_CUDA(cudaMemcpyAsync(top_tok, dec_topi, (size_t)n * k * 4, cudaMemcpyDeviceToHost, st));
+    int stt = 0;
+    CMT_CUDA(cudaMemcpyAsync(&stt, status_d, 4, cudaMemcpyDeviceToHost, st));
+    CMT_CUDA(cudaStreamSynchronize(st));
+    if (stt & ST_LOGITS) throw Error(CMT_ERR_NUM_LOGITS, "log_softmax_columns received non-finite input");
   }
 
   // ---- workspace carving for (S, T, B) ----
@@ -2230,6 +2388,13 @@ int cmt_snapshot_download(cmt_engine* e, int slot, int idx, float* h, long long 
     e->eng->check_slot(slot);
     e->eng->download(idx, h, rows, cols, false, slot);
   });
+}
+int cmt_decode_begin(cmt_engine* e, const long long* src_ids, int S) {
+  return guard(e, [&] { e->eng->decode_begin(src_ids, S); });
+}
+int cmt_decode_step(cmt_engine* e, int n, const long long* prev_tokens, const int* parent, int k, float* top_logprob,
+                    int* top_token) {
+  return guard(e, [&] { e->eng->decode_step(n, prev_tokens, parent, k, top_logprob, top_token); });
 }
 int cmt_download_grad(cmt_engine* e, int idx, float* h, long long rows, long long cols) {
   return guard(e, [&] { e->eng->download(idx, h, rows, cols, true); });

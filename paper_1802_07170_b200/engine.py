@@ -285,6 +285,30 @@ class Engine:
         if pending:
             yield self._finish()
 
+    # ---- translation (decode_begin / decode_step, include/cytonmt_b200.h) ----
+    def decode_begin(self, src_tokens):
+        """Encode one source sentence (INFER) and reset the decoder states to its finals."""
+        src = np.ascontiguousarray(np.asarray(src_tokens, dtype=np.int64).reshape(-1))
+        if src.size == 0:
+            raise ConfigError("cannot translate an empty source sentence")
+        self._check(self.lib.cmt_decode_begin(self.h, _llptr(src), int(src.size)))
+
+    def decode_step(self, prev_tokens, parent, k):
+        """One decoder step for the rows ``prev_tokens`` (parent: state row of the
+        previous step per row, or None for the encoder finals).  Returns the k
+        best (log-prob, token) of every row as arrays of shape (n, k)."""
+        prev = np.ascontiguousarray(np.asarray(prev_tokens, dtype=np.int64).reshape(-1))
+        n = int(prev.size)
+        vals = np.empty((n, k), dtype=np.float32)
+        toks = np.empty((n, k), dtype=np.int32)
+        par_p = None
+        if parent is not None:
+            par = np.ascontiguousarray(np.asarray(parent, dtype=np.int32).reshape(-1))
+            par_p = par.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+        self._check(self.lib.cmt_decode_step(self.h, n, _llptr(prev), par_p, int(k), _fptr(vals),
+                                             toks.ctypes.data_as(ctypes.POINTER(ctypes.c_int))))
+        return vals, toks
+
     def _finish(self):
         r = self.wait()
         return r.loss, r.grad_norm
