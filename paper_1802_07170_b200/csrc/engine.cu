@@ -365,6 +365,7 @@ class Engine {
   float *src_mask_d, *tgt_mask_d;
   void *Xs, *Xt, *top, *u_att, *cst_att, *hod, *Y, *dhpre, *du_att, *dU, *dU2;
   float* cepart = nullptr;  // per-CTA dY column sums of the fused CE kernel
+  float2* cerow = nullptr;  // per-token (lse * log2e, mask / ntok) between the two CE passes
   float* colpart2 = nullptr;  // column-sum scratch of the side stream
   float* dho32 = nullptr;   // fp32 split-K scratch of dH_o (bf16 mode)
   float *att_part = nullptr, *att_dsc = nullptr;  // split attention: score slices, d scores
@@ -397,7 +398,7 @@ class Engine {
   // (halving the dU stream does not pay for the slower MMA drain; profiles/r01/s3/trace_bwd.txt)
   int bwd_tm = 0;
   int use_jump = 1;    // option: table-driven PCG64 jump-ahead dropout kernel
-  int ce2 = 1;         // option: fused CE + bias-grad column sums (persistent, 16-byte vectors)
+  int ce2 = 2;         // option: fused CE + bias-grad column sums: 2 two-pass (stats, gradient), 1 persistent one-pass
   bool use_ce2() const { return bf && ce2 && V % 8 == 0 && V <= CE2_MAXV; }
   // data parallel (NCCL): dense all-reduce of grads, loss and status
   void* comm = nullptr;
@@ -948,7 +949,8 @@ class Engine {
     long long colmax = std::max<long long>(V, 4LL * H);
     colpart = carve<float>(cur, 64 * colmax * 4);
     colpart2 = carve<float>(cur, 64 * colmax * 4);
-    cepart = use_ce2() ? carve<float>(cur, (long long)g_num_sms * V * 4) : nullptr;
+    cepart = use_ce2() ? carve<float>(cur, std::max<long long>(g_num_sms, ceil_div(NT, CEG_ROWS)) * V * 4) : nullptr;
+    cerow = carve<float2>(cur, (size_t)NT * 8);
     for (int t = 0; t < 2; ++t) {
       seg_off_d[t] = carve<int>(cur, (NS + NT + 1) * 4);
       seg_pos_d[t] = carve<int>(cur, (NS + NT) * 4);
@@ -1935,7 +1937,18 @@ class Engine {
     if (stop_after == 1) { CMT_CUDA(cudaStreamSynchronize(st)); return; }
     // fused log-softmax + smoothed CE + grad (training.py:96-120, tensor.py:146-151)
     const bool fused_ce = use_ce2() && cepart;
-    if (fused_ce) {
+    if (fused_ce && ce2 == 2) {
+      ce_stats_kernel<<<(int)NT, CES_THREADS, 0, st>>>((const bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon,
+                                                       inv_ntok, cfg.output_tanh, losstok, status_d, cerow);
+      CMT_LAUNCHED(); tl_mark(st, "ce_stats_kernel");
+      const int chunks = (int)ceil_div(NT, CEG_ROWS);
+      ce_grad_kernel<<<dim3(ceil_div(V, CEG_COLS), chunks), CEG_THREADS, 0, st>>>((bf16*)Y, V, (int)NT, tgt_out_d,
+                                                                                  cerow, (float)a.epsilon,
+                                                                                  cfg.output_tanh, cepart);
+      CMT_LAUNCHED(); tl_mark(st, "ce_grad_kernel");
+      colsum_final_kernel<<<ceil_div(V, 256), 256, 0, st>>>(cepart, chunks, V, dg + off_bo);
+      CMT_LAUNCHED(); tl_mark(st, "colsum_final_kernel");
+    } else if (fused_ce) {
       const size_t smem = (size_t)V * 4;
       CMT_CUDA(cudaFuncSetAttribute(ce_colsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       ce_colsum_kernel<<<g_num_sms, CE2_THREADS, smem, st>>>((bf16*)Y, V, (int)NT, tgt_out_d, tgt_mask_d,

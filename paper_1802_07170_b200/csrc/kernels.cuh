@@ -687,6 +687,134 @@ __global__ void __launch_bounds__(CE2_THREADS, 1)
   for (int v = threadIdx.x; v < V; v += CE2_THREADS) part[(long long)blockIdx.x * V + v] = csum[v];
 }
 
+// Two-pass fused CE (ce2 = 2, default): both passes run at full occupancy
+// with no shared-memory column accumulators.
+// Pass 1, one CTA per token row: log-sum-exp, smoothed per-token loss and the
+// row's (lse*log2e, mask/ntok) for pass 2 (training.py:96-120, tensor.py:146-151).
+constexpr int CES_THREADS = 512;
+__global__ void __launch_bounds__(CES_THREADS) ce_stats_kernel(const bf16* __restrict__ Y, int V,
+                                                               const int* __restrict__ tgt,
+                                                               const float* __restrict__ tmask, float eps,
+                                                               float inv_ntok, int tanh_on,
+                                                               float* __restrict__ losstok,
+                                                               int* __restrict__ status, float2* __restrict__ rowst) {
+  __shared__ float red_m[CES_THREADS / 32], red_s[CES_THREADS / 32], red_y[CES_THREADS / 32];
+  const int n = blockIdx.x;
+  const int nv = V >> 3;
+  const uint4* row = (const uint4*)(Y + (long long)n * V);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float mx = tanh_on ? 0.f : -INFINITY, se = 0.f, sy = 0.f;
+  bool bad = false;
+  for (int i0 = threadIdx.x; i0 < nv; i0 += 4 * CES_THREADS) {
+    uint4 qv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * CES_THREADS;
+      qv[u] = i < nv ? __ldg(row + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i0 + u * CES_THREADS >= nv) break;
+      const bf16* e = (const bf16*)&qv[u];
+      float y[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        y[j] = __bfloat162float(e[j]);
+        sy += y[j];
+      }
+      if (tanh_on) {  // |y| <= 1: no max shift; non-finite logits surface in the row sum
+#pragma unroll
+        for (int j = 0; j < 8; ++j) se += ex2f(y[j] * kLog2e);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bad |= !isfinite(y[j]);
+        float lm = y[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) lm = fmaxf(lm, y[j]);
+        if (lm > mx) {
+          se = (mx == -INFINITY) ? 0.f : se * __expf(mx - lm);
+          mx = lm;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) se += __expf(y[j] - mx);
+      }
+    }
+  }
+  const float wm = warp_max(mx);
+  se = (mx == -INFINITY) ? 0.f : se * __expf(mx - wm);
+  se = warp_sum(se);
+  sy = warp_sum(sy);
+  if (tanh_on) bad = !isfinite(sy);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_LOGITS);
+  if (lane == 0) { red_m[warp] = wm; red_s[warp] = se; red_y[warp] = sy; }
+  __syncthreads();
+  if (warp == 0) {
+    const float m2 = lane < CES_THREADS / 32 ? red_m[lane] : -INFINITY;
+    float s2 = lane < CES_THREADS / 32 ? red_s[lane] : 0.f;
+    float y2 = lane < CES_THREADS / 32 ? red_y[lane] : 0.f;
+    const float gm = warp_max(m2);
+    s2 = (m2 == -INFINITY) ? 0.f : s2 * __expf(m2 - gm);
+    s2 = warp_sum(s2);
+    y2 = warp_sum(y2);
+    if (lane == 0) {
+      const float lse = gm + logf(s2);
+      const float gold = __bfloat162float(Y[(long long)n * V + tgt[n]]);
+      const float per = lse - (1.f - eps) * gold - (eps / (float)V) * y2;
+      const float m = tmask[n];
+      losstok[n] = per * m;
+      if (!isfinite(per)) atomicOr(status, ST_LOSS);
+      rowst[n] = make_float2(lse * kLog2e, m * inv_ntok);
+    }
+  }
+}
+// Pass 2: CTA = (2048-column slice, chunk of CEG_ROWS rows); a thread owns 8
+// adjacent columns: it rewrites Y in place with the gradient
+// d = (p - eps/V - (1-eps)[v=gold]) m/ntok (* (1 - y^2) under the output tanh)
+// and keeps the 8 column sums (the bias grad, layers.py:72-73) in registers;
+// part[chunk][v] is reduced by colsum_final_kernel in chunk order.
+constexpr int CEG_THREADS = 256;
+constexpr int CEG_COLS = 8 * CEG_THREADS;
+constexpr int CEG_ROWS = 64;
+__global__ void __launch_bounds__(CEG_THREADS) ce_grad_kernel(bf16* __restrict__ Y, int V, int rows,
+                                                              const int* __restrict__ tgt,
+                                                              const float2* __restrict__ rowst, float eps,
+                                                              int tanh_on, float* __restrict__ part) {
+  const int c = blockIdx.x * CEG_COLS + threadIdx.x * 8;
+  const int r0 = blockIdx.y * CEG_ROWS, r1 = min(rows, r0 + CEG_ROWS);
+  if (c >= V) return;
+  const float eV = eps / (float)V;
+  float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int rb = r0; rb < r1; rb += 4) {
+    uint4 qv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      qv[u] = rb + u < r1 ? __ldcs((const uint4*)(Y + (long long)(rb + u) * V + c)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = rb + u;
+      if (r >= r1) break;
+      const float2 st = __ldg(rowst + r);  // (lse * log2e, m / ntok)
+      const int gj = __ldg(tgt + r) - c;    // the gold column falls in this vector iff 0 <= gj < 8
+      const float ewv = eV * st.y, gw = (1.f - eps) * st.y;
+      const bf16* e = (const bf16*)&qv[u];
+      __align__(16) bf16 o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float y = __bfloat162float(e[j]);
+        float d = fmaf(ex2f(fmaf(y, kLog2e, -st.x)), st.y, -ewv);
+        if (j == gj) d -= gw;
+        if (tanh_on) d *= fmaf(-y, y, 1.f);
+        o[j] = __float2bfloat16_rn(d);
+        cs[j] += d;
+      }
+      __stcs((uint4*)(Y + (long long)r * V + c), *(const uint4*)o);
+    }
+  }
+  float4* pp = (float4*)(part + (long long)blockIdx.y * V + c);
+  pp[0] = make_float4(cs[0], cs[1], cs[2], cs[3]);
+  pp[1] = make_float4(cs[4], cs[5], cs[6], cs[7]);
+}
+
 template <typename T>
 __global__ void colsum_partial_kernel(const T* __restrict__ D, long long ld, int rows, int cols, int rows_per,
                                       float* __restrict__ part) {
