@@ -429,3 +429,29 @@ def test_pipeline_matches_sequential_steps(mode):
     assert out[0][2] == out[1][2]
     for n in out[0][1]:
         assert np.array_equal(out[0][1][n], out[1][1][n]), n
+
+
+@pytest.mark.parametrize("tanh_", [True, False])
+def test_ce_variants_agree(tanh_):
+    """The three CE implementations (ce2=2 two-pass default, ce2=1 one-pass
+    persistent, ce2=0 per-row kernel + separate column sums) give the same loss
+    and gradients (including the output bias, a column sum of the CE
+    gradient) within bf16 tolerance of the oracle, with and without the
+    output tanh (training.py:96-120, layers.py:64-73)."""
+    from paper_1802_07170_b200.engine import Engine
+    from paper_1802_07170_b200.model import Batch
+    from tests.gpu_helpers import cfg_of
+    d = O.Dims(520, 64, 128, 1, 0.0, tanh_, False)
+    params = scaled_params(d, 8, 0.3)
+    src, sm, tgt, tm = O.synthetic_batch(520, 7, 9, 20, seed=3, ragged=True)
+    ol, _, og, _, _ = oracle_step(d, params, (src, sm, tgt, tm), 0.1, 1.0, 5.0, 1, update=False)
+    for ce2 in (2, 1, 0):
+        eng = Engine(cfg_of(d), mode="bf16")
+        eng.set_option("ce2", ce2)
+        eng.upload(params)
+        loss, _ = eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, None, update=False)
+        grads = eng.grads()
+        eng.close()
+        assert abs(loss - ol) <= BF16_TOL * abs(ol), ce2
+        for n in ("out.w", "out.b", "att.w_c.w", "tgt_embed"):
+            assert O.norm_rel_err(grads[n], og[n]) < BF16_TOL, (ce2, n)
