@@ -133,6 +133,7 @@ struct Mat {
 };
 
 static int g_num_sms = 148;
+static int g_grid_cap = 0;  // > 0: persistent GEMMs use at most this many CTAs (work beside a running scan)
 constexpr int FLAG_STRIDE = 128;  // step counters per scan (per-k-block readiness flags)
 
 // ---- kernel timeline (debug option "timeline"): an event after every launch
@@ -176,7 +177,8 @@ static void launch_tc_impl(cudaStream_t st, int M, int N, int K, Mat A, Mat B, c
   if constexpr (ST) make_map_c(&tcm, e.C, N, M, e.ldc, e.c_bf16 != 0);
   else tcm = ta;
   int tiles = ceil_div(M, C::TILE_M) * ceil_div(N, BN) * (ks > 0 ? ks : 1);
-  int grid = ks > 0 ? CG * std::min(tiles, g_num_sms / CG) : CG * (g_num_sms / CG);
+  const int sms = g_grid_cap > 0 ? std::min(g_num_sms, g_grid_cap) : g_num_sms;
+  int grid = ks > 0 ? CG * std::min(tiles, sms / CG) : CG * (sms / CG);
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3(grid);
   c.blockDim = dim3(tc::NUM_THREADS);
@@ -372,7 +374,7 @@ class Engine {
   int att_split = 2;  // option: 2 tiled split attention (S,T <= 128), 1 split (<= 64), 0 per-sentence
   int allow_empty_targets = 0;  // option: stage batches with no unmasked target (dev_entropy)
   bool last_infer = false;
-  float *ux, *ux2, *alpha, *ho, *losstok, *dcst, *dXemb, *dtop, *dhc, *dcc, *colpart;
+  float *ux, *ux2, *ux3, *alpha, *ho, *losstok, *dcst, *dXemb, *dtop, *dhc, *dcc, *colpart;
   std::vector<void*> drop_enc, drop_dec;
   std::vector<uint8_t*> keep_enc, keep_dec;
   uint8_t* keep_o;
@@ -393,6 +395,7 @@ class Engine {
   int cg2 = 1;         // option: CTA-pair (cta_group::2) tiles for the large GEMMs
   int dual = 1;        // option: run independent scans of the layer graph two at a time
   int fwd_tm = 1;      // option: forward scans with W_h split over smem + TMEM (lstm_tm.cuh)
+  int early_dec1 = 1;  // option: dec.l1's input projection runs beside the enc.l1 scans on the idle SMs
   // option: BPTT scans with W_h split over smem + TMEM (lstm_tm_bwd.cuh; 1: paired scans, 2: also single).
   // Off by default: at c3 it runs 12.3 us/step paired vs 11.5 for lstm_bwd_multi<128>
   // (halving the dU stream does not pay for the slower MMA drain; profiles/r01/s3/trace_bwd.txt)
@@ -913,6 +916,7 @@ class Engine {
     top = carve<char>(cur, NS * H * asz);
     ux = carve<float>(cur, Nmax * 4 * H * 4);
     ux2 = carve<float>(cur, Nmax * 4 * H * 4);
+    ux3 = carve<float>(cur, NT * 4 * H * 4);  // dec.l1 input projection, computed early (see run())
     dU = carve<char>(cur, Nmax * 4 * H * asz);
     dU2 = carve<char>(cur, Nmax * 4 * H * asz);
     drop_enc.assign(L + 1, nullptr); keep_enc.assign(L + 1, nullptr);
@@ -1783,7 +1787,21 @@ class Engine {
         fwd_prep(a);
         fwd_prep(b);
       }
+      // dec.l1's input projection depends only on the target embeddings: on the
+      // side stream, capped to the SMs the paired enc.l1 scans leave idle, it
+      // runs beside them instead of in level 2
+      const int idle = g_num_sms - 2 * (dual_tm() ? tm::Fwd<64>::ctas(H, B) : mc::Fwd<128>::ctas(H, B));
+      const bool dec1_early = early_dec1 && use_overlap() && L >= 2 && idle >= 8;
+      FwdScan d1{L + 1, Xt, E, T, false, nullptr, ux3};
+      if (dec1_early) fork();
       fwd_pair(a, b);
+      if (dec1_early) {
+        on_side_stream([&]() {
+          g_grid_cap = idle;
+          fwd_prep(d1);
+          g_grid_cap = 0;
+        });
+      }
       add_top();
       const void* cur = top;
       for (int k = 2; k <= L; ++k) {
@@ -1803,7 +1821,10 @@ class Engine {
         if (ov) on_side_stream(dec_side);
         else dec_side();
         FwdScan d{L + k - 1, xd, k - 1 == 1 ? E : H, T, false, nullptr, ux2};
-        if (ov) {
+        if (k == 2 && dec1_early) {
+          d = d1;  // projected beside the enc.l1 scans (joined here)
+          join();
+        } else if (ov) {
           on_side_stream([&]() { fwd_prep(d); });
           join();
         } else {
@@ -2515,6 +2536,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "fwd_tm") e->eng->fwd_tm = (int)value;
     else if (k == "bwd_tm") e->eng->bwd_tm = (int)value;
     else if (k == "ar_overlap") e->eng->ar_overlap = (int)value;
+    else if (k == "early_dec1") e->eng->early_dec1 = (int)value;
     else if (k == "jump") e->eng->use_jump = (int)value;
     else if (k == "att_split") e->eng->att_split = (int)value;
     else if (k == "allow_empty_targets") e->eng->allow_empty_targets = (int)value;
