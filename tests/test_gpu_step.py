@@ -229,6 +229,7 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
         "dual": dict(),  # default: paired forward scans in lstm_fwd_tm, paired BPTT in lstm_bwd_multi<128>
         "dual_multi": dict(fwd_tm=0, bwd_tm=1),  # lstm_fwd_multi<128> / lstm_bwd_tm (W_h over smem + TMEM)
         "tm_single": dict(fwd_tm=2, bwd_tm=2),  # single scans in the TMEM-split kernels too
+        "bg_dw": dict(bg_dw=1),  # BPTT weight grads on the background stream beside the next scans
     }
     for variant, opts in variants.items():
         eng = Engine(cfg_of(d), mode="bf16")
@@ -238,7 +239,7 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
         eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, np.random.Generator(np.random.PCG64(3)), update=False)
         out[variant] = eng.grads()
         eng.close()
-    for v in ("persistent", "cluster", "dual", "dual_multi", "tm_single"):
+    for v in ("persistent", "cluster", "dual", "dual_multi", "tm_single", "bg_dw"):
         for n in og:
             assert O.norm_rel_err(out[v][n], out["per_step"][n]) < BF16_TOL, (v, n)
             assert O.norm_rel_err(out[v][n], og[n]) < BF16_TOL, (v, n)
