@@ -1183,6 +1183,16 @@ class Engine {
   }
   template <typename TI, typename TO>
   void launch_dropout(const void* x, void* y, uint8_t* keep, int N, unsigned long long base, const Pcg& pcg) {
+    if (use_jump == 1) {
+      ensure_jump(pcg);
+      dim3 blk(32, 8);
+      dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, DROP4_DPT), 8));
+      float scale = 1.0f / (float)(1.0 - cfg.dropout);
+      dropout_fwd_kernel4<TI, TO><<<grid, blk, 0, st>>>((const TI*)x, (TO*)y, keep, N, H, pcg, jump_d, base,
+                                                        dropout_threshold(cfg.dropout), scale);
+      CMT_LAUNCHED(); tl_mark(st, "dropout_fwd_kernel4");
+      return;
+    }
     if (use_jump) {
       ensure_jump(pcg);
       dim3 blk(32, 8);
@@ -2600,12 +2610,34 @@ int cmt_test_dropout(unsigned long long sh, unsigned long long sl, unsigned long
     cmt::PcgJump* jt = nullptr;
     CMT_CUDA(cudaMalloc(&jt, sizeof(cmt::PcgJump)));
     cmt::pcg_jump_table_kernel<<<1, 1>>>(jt, ih, il);
+    // the engine's kernel (dropout_fwd_kernel4) writes y / keep; the previous
+    // kernel3 must produce the same bits (checked here)
+    dim3 grid4(cmt::ceil_div(H, 32), cmt::ceil_div(cmt::ceil_div(N, cmt::DROP4_DPT), 8));
+    cmt::dropout_fwd_kernel4<float, float><<<grid4, blk>>>(x, y, keep, N, H, pcg, jt, base, cmt::dropout_threshold(p),
+                                                            1.0f / (float)(1.0 - p));
+    const size_t n = (size_t)N * H;
+    float* y3 = nullptr;
+    unsigned char* k3 = nullptr;
+    CMT_CUDA(cudaMalloc(&y3, n * 4));
+    CMT_CUDA(cudaMalloc(&k3, n));
     dim3 grid3(cmt::ceil_div(H, 32), cmt::ceil_div(cmt::ceil_div(N, cmt::DROP_DPT), 8));
-    cmt::dropout_fwd_kernel3<float, float><<<grid3, blk>>>(x, y, keep, N, H, pcg, jt, base, cmt::dropout_threshold(p),
+    cmt::dropout_fwd_kernel3<float, float><<<grid3, blk>>>(x, y3, k3, N, H, pcg, jt, base, cmt::dropout_threshold(p),
                                                             1.0f / (float)(1.0 - p));
     cudaError_t err = cudaDeviceSynchronize();
+    std::vector<unsigned char> ka(n), kb(n);
+    std::vector<float> ya(n), yb(n);
+    if (err == cudaSuccess) {
+      cudaMemcpy(ka.data(), keep, n, cudaMemcpyDeviceToHost);
+      cudaMemcpy(kb.data(), k3, n, cudaMemcpyDeviceToHost);
+      cudaMemcpy(ya.data(), y, n * 4, cudaMemcpyDeviceToHost);
+      cudaMemcpy(yb.data(), y3, n * 4, cudaMemcpyDeviceToHost);
+    }
     cudaFree(jt);
+    cudaFree(y3);
+    cudaFree(k3);
     CMT_CUDA(err);
+    if (ka != kb || std::memcmp(ya.data(), yb.data(), n * 4) != 0)
+      throw Error(cmt::CMT_ERR_INTERNAL, "dropout kernels 3 and 4 disagree");
     CMT_CUDA(cudaGetLastError());
     CMT_CUDA(cudaDeviceSynchronize());
   });

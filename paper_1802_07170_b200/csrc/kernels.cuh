@@ -249,6 +249,40 @@ __global__ void dropout_fwd_kernel3(const TI* __restrict__ x, TO* __restrict__ y
   }
 }
 
+// Same draws as dropout_fwd_kernel3 with the LCG step written in 64-bit halves
+// against the constant PCG64 multiplier (one umulhi, three low products, one
+// carry), the keep test on the state halves directly, and the element index
+// advanced incrementally: about half the instructions per draw.
+constexpr int DROP4_DPT = 32;
+template <typename TI, typename TO>
+__global__ void dropout_fwd_kernel4(const TI* __restrict__ x, TO* __restrict__ y, uint8_t* __restrict__ keep, int N,
+                                    int H, Pcg pcg, const PcgJump* __restrict__ jt, unsigned long long base,
+                                    unsigned long long thr, float scale) {
+  const int h = blockIdx.x * 32 + threadIdx.x;
+  const int n0 = (blockIdx.y * blockDim.y + threadIdx.y) * DROP4_DPT;
+  if (h >= H || n0 >= N) return;
+  const u128 s0 = pcg_jump(jt, ((u128)pcg.state_hi << 64) | pcg.state_lo, base + (unsigned long long)h * N + n0);
+  unsigned long long sh = (unsigned long long)(s0 >> 64), sl = (unsigned long long)s0;
+  const unsigned long long MH = 0x2360ed051fc65da4ULL, ML = 0x4385df649fccf645ULL;
+  const unsigned long long ih = pcg.inc_hi, il = pcg.inc_lo;
+  const int nend = min(N, n0 + DROP4_DPT);
+  long long i = (long long)n0 * H + h;
+#pragma unroll 4
+  for (int n = n0; n < nend; ++n, i += H) {
+    const unsigned long long lo = sl * ML;
+    const unsigned long long hi = __umul64hi(sl, ML) + sl * MH + sh * ML;
+    sl = lo + il;
+    sh = hi + ih + (sl < lo ? 1ull : 0ull);
+    const unsigned rot = (unsigned)(sh >> 58);
+    const unsigned long long xr = sh ^ sl;
+    const unsigned long long r = (xr >> rot) | (xr << ((64 - rot) & 63));
+    const bool k = (r >> 11) >= thr;
+    keep[i] = k;
+    const float xv = to_f<TI>(x[i]);
+    y[i] = from_f<TO>(k ? xv * scale : xv * 0.f);
+  }
+}
+
 // y = x * keep/(1-p) for one dropout site of shape (H, N) in the reference's
 // C order: element (h, n) is draw (base + h*N + n).  Activations here are
 // token-major [n][h]; a warp covers 32 consecutive h, each thread 32
