@@ -63,6 +63,77 @@ __global__ void __launch_bounds__(dec::GV_THREADS) dec_gemv_partial(const float*
   }
 }
 
+// Bandwidth-shaped variant: CTA = 128 output columns x one K chunk; its 8
+// warps split the chunk, lane = 4 adjacent columns (8-byte bf16 / 16-byte fp32
+// weight loads, a warp reads 256 / 512 contiguous bytes per weight row), all
+// n <= 16 rows accumulate in registers; the 8 warp partials are added in smem
+// in warp order, so part[ks][i][j] is deterministic.
+constexpr int GV2_THREADS = 256, GV2_COLS = 128, GV2_KCH = 256;
+constexpr size_t GV2_SMEM = sizeof(float) * (dec::ROWS * GV2_KCH + (GV2_THREADS / 32) * dec::ROWS * (GV2_COLS + 4));
+template <typename T>
+__global__ void __launch_bounds__(GV2_THREADS) dec_gemv2_partial(const float* __restrict__ Z, int ldz, int n, int K,
+                                                                 const T* __restrict__ W, long long ldw, int N,
+                                                                 float* __restrict__ part) {
+  extern __shared__ float gv2_smem[];  // zs [ROWS][KCH], then red [warps][ROWS][COLS + 4]
+  float(*zs)[GV2_KCH] = (float(*)[GV2_KCH])gv2_smem;
+  float(*red)[dec::ROWS][GV2_COLS + 4] = (float(*)[dec::ROWS][GV2_COLS + 4])(gv2_smem + dec::ROWS * GV2_KCH);
+  const int k0 = blockIdx.y * GV2_KCH, nk = min(GV2_KCH, K - k0);
+  for (int x = threadIdx.x; x < dec::ROWS * GV2_KCH; x += blockDim.x) {
+    const int i = x / GV2_KCH, k = x % GV2_KCH;
+    zs[i][k] = (i < n && k < nk) ? Z[(long long)i * ldz + k0 + k] : 0.f;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * GV2_COLS + lane * 4;
+  constexpr int KW = GV2_KCH / (GV2_THREADS / 32);  // k rows per warp
+  float acc[dec::ROWS][4];
+#pragma unroll
+  for (int i = 0; i < dec::ROWS; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  if (c < N) {
+    const bool full4 = c + 3 < N && (ldw & 3) == 0;
+    const int kb = warp * KW, ke = min(nk, kb + KW);
+#pragma unroll 4
+    for (int k = kb; k < ke; ++k) {
+      const T* wp = W + (long long)(k0 + k) * ldw + c;
+      float w[4];
+      if (full4) {
+        if constexpr (sizeof(T) == 2) {
+          const uint2 q = __ldg((const uint2*)wp);
+          const float2 a = __bfloat1622float2(*(const __nv_bfloat162*)&q.x);
+          const float2 b = __bfloat1622float2(*(const __nv_bfloat162*)&q.y);
+          w[0] = a.x; w[1] = a.y; w[2] = b.x; w[3] = b.y;
+        } else {
+          const float4 q = __ldg((const float4*)wp);
+          w[0] = q.x; w[1] = q.y; w[2] = q.z; w[3] = q.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = c + j < N ? to_f<T>(wp[j]) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < dec::ROWS; ++i) {
+        const float z = zs[i][k];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(z, w[j], acc[i][j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < dec::ROWS; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[warp][i][lane * 4 + j] = acc[i][j];
+  __syncthreads();
+  for (int x = threadIdx.x; x < n * GV2_COLS; x += blockDim.x) {
+    const int i = x / GV2_COLS, cc = x % GV2_COLS;
+    const int col = blockIdx.x * GV2_COLS + cc;
+    if (col >= N) continue;
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < GV2_THREADS / 32; ++w) t += red[w][i][cc];
+    part[((long long)blockIdx.y * n + i) * N + col] = t;
+  }
+}
+
 // Y[i][j] = act(sum_ks part[ks][i][j] + bias[j]); act 1 = tanh
 __global__ void dec_gemv_final(const float* __restrict__ part, int ks, int n, int N, const float* __restrict__ bias,
                                int act, float* __restrict__ Y, int ldy) {

@@ -824,13 +824,28 @@ class Engine {
   template <typename T>
   void dec_gemv(const float* Z, int ldz, int n, int K, const T* W, long long ldw, int N, const float* bias, int act,
                 float* Y, int ldy) {
+    if (n <= dec::ROWS) {  // all rows in one pass: every weight byte is read once
+      const int ks = ceil_div(K, GV2_KCH);
+      if ((size_t)ks * n * N > dec_part_n) throw Error(CMT_ERR_INTERNAL, "decode partials too small");
+      static bool attr = false;
+      if (!attr) {
+        CMT_CUDA(cudaFuncSetAttribute(dec_gemv2_partial<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GV2_SMEM));
+        attr = true;
+      }
+      dec_gemv2_partial<T><<<dim3(ceil_div(N, GV2_COLS), ks), GV2_THREADS, GV2_SMEM, st>>>(Z, ldz, n, K, W, ldw, N,
+                                                                                          dec_part);
+      CMT_LAUNCHED(); tl_mark(st, "gemv2 " + std::to_string(n) + "x" + std::to_string(K) + "x" + std::to_string(N));
+      dec_gemv_final<<<(int)ceil_div((long long)n * N, 256), 256, 0, st>>>(dec_part, ks, n, N, bias, act, Y, ldy);
+      CMT_LAUNCHED(); tl_mark(st, "gemv_final");
+      return;
+    }
     const int ks = ceil_div(K, dec::KCH);
     if ((size_t)ks * n * N > dec_part_n) throw Error(CMT_ERR_INTERNAL, "decode partials too small");
     dim3 g(ceil_div(N, dec::GV_COLS), ks, ceil_div(n, dec::ROWS));
     dec_gemv_partial<T><<<g, dec::GV_THREADS, 0, st>>>(Z, ldz, n, K, W, ldw, N, dec_part);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "gemv " + std::to_string(n) + "x" + std::to_string(K) + "x" + std::to_string(N));
     dec_gemv_final<<<(int)ceil_div((long long)n * N, 256), 256, 0, st>>>(dec_part, ks, n, N, bias, act, Y, ldy);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "gemv_final");
   }
   template <typename T>
   void decode_step_t(int n, int k) {
@@ -842,33 +857,33 @@ class Engine {
     dim3 gg(n, L);
     dec_gather_states<<<gg, 256, 0, st>>>(dec_h(dec_cur), dec_c(dec_cur), dec_fin, dec_fin + (size_t)L * H,
                                           dec_par_set ? dec_par : nullptr, n, H, ls, dec_h(in), dec_c(in));
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "dec_gather_states");
     const T* table = bf ? (const T*)(const void*)emb_sh[tgt_table()] : (const T*)(const void*)emb_w[tgt_table()];
     dec_embed<T><<<n, 256, 0, st>>>(table, dec_ids, E, dec_z, zc);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "dec_embed");
     for (int k1 = 1; k1 <= L; ++k1) {  // decoder layers (lstm_cell_forward, layers.py:344-363)
       const Layer& ly = layers[L + k1];
       const int din = ly.din;
       dec_copy_rows<<<n, 256, 0, st>>>(dec_h(in) + (k1 - 1) * ls, H, dec_z + din, zc, H);
-      CMT_LAUNCHED();
+      CMT_LAUNCHED(); tl_mark(st, "dec_copy_rows");
       dec_gemv<T>(dec_z, zc, n, din + H, wts + ly.w_off, 4LL * H, 4 * H, dw + ly.b_off, 0, dec_u, 4 * H);
       // the next layer's input (the x rows of z) is this layer's h
       dec_lstm_cell<<<n, 256, 0, st>>>(dec_u, dec_c(in) + (k1 - 1) * ls, H, dec_h(outb) + (k1 - 1) * ls,
                                        dec_c(outb) + (k1 - 1) * ls, k1 < L ? dec_z : nullptr, zc);
-      CMT_LAUNCHED();
+      CMT_LAUNCHED(); tl_mark(st, "dec_lstm_cell");
     }
     const float* x = dec_h(outb) + (L - 1) * ls;  // top decoder h [n][H]
     // attention (attend_values): u = W_a^T x; context; H_o = tanh(W_c^T [ctx; x])
     dec_gemv<T>(x, H, n, H, wts + off_wa, H, H, nullptr, 0, dec_u, H);
     dec_attention<<<n, 256, (size_t)dec_S * 4, st>>>(dec_hs, dec_S, H, dec_u, dec_z, zc);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "dec_attention");
     dec_copy_rows<<<n, 256, 0, st>>>(x, H, dec_z + H, zc, H);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "dec_copy_rows");
     dec_gemv<T>(dec_z, zc, n, 2 * H, wts + off_wc, H, H, nullptr, 1, dec_ho, H);
     // output layer (model.py:232-235), log-softmax and the k best entries per row
     dec_gemv<T>(dec_ho, H, n, H, wts + off_wo, V, V, dw + off_bo, cfg.output_tanh ? 1 : 0, dec_y, V);
     dec_logsoftmax_topk<<<n, dec::TOPK_THREADS, 0, st>>>(dec_y, V, k, dec_topv, dec_topi, status_d);
-    CMT_LAUNCHED();
+    CMT_LAUNCHED(); tl_mark(st, "dec_topk");
     dec_cur = outb;
   }
   void decode_step(int n, const long long* prev, const int* parent, int k, float* top_val, int* top_tok) {
