@@ -70,17 +70,25 @@ __global__ void __launch_bounds__(dec::GV_THREADS) dec_gemv_partial(const float*
 // in warp order, so part[ks][i][j] is deterministic.
 constexpr int GV2_THREADS = 256, GV2_COLS = 128, GV2_KCH = 256;
 constexpr size_t GV2_SMEM = sizeof(float) * (dec::ROWS * GV2_KCH + (GV2_THREADS / 32) * dec::ROWS * (GV2_COLS + 4));
+// Inputs come as two column segments (Z1: K1 columns, Z2: K2 columns; K =
+// K1 + K2), so [x; h] and [ctx; h] need no concatenation copies.  The last CTA
+// of a column block (atomic ticket, reset by it) adds the K-chunk partials in
+// chunk order, applies bias and activation and writes Y: one launch per product.
 template <typename T>
-__global__ void __launch_bounds__(GV2_THREADS) dec_gemv2_partial(const float* __restrict__ Z, int ldz, int n, int K,
-                                                                 const T* __restrict__ W, long long ldw, int N,
-                                                                 float* __restrict__ part) {
+__global__ void __launch_bounds__(GV2_THREADS) dec_gemv2(const float* __restrict__ Z1, int ld1, int K1,
+                                                         const float* __restrict__ Z2, int ld2, int K2, int n,
+                                                         const T* __restrict__ W, long long ldw, int N,
+                                                         float* __restrict__ part, unsigned* __restrict__ ticket,
+                                                         const float* __restrict__ bias, int act, float* __restrict__ Y,
+                                                         int ldy) {
+  const int K = K1 + K2;
   extern __shared__ float gv2_smem[];  // zs [ROWS][KCH], then red [warps][ROWS][COLS + 4]
   float(*zs)[GV2_KCH] = (float(*)[GV2_KCH])gv2_smem;
   float(*red)[dec::ROWS][GV2_COLS + 4] = (float(*)[dec::ROWS][GV2_COLS + 4])(gv2_smem + dec::ROWS * GV2_KCH);
   const int k0 = blockIdx.y * GV2_KCH, nk = min(GV2_KCH, K - k0);
   for (int x = threadIdx.x; x < dec::ROWS * GV2_KCH; x += blockDim.x) {
-    const int i = x / GV2_KCH, k = x % GV2_KCH;
-    zs[i][k] = (i < n && k < nk) ? Z[(long long)i * ldz + k0 + k] : 0.f;
+    const int i = x / GV2_KCH, k = x % GV2_KCH, kg = k0 + k;
+    zs[i][k] = (i < n && k < nk) ? (kg < K1 ? Z1[(long long)i * ld1 + kg] : Z2[(long long)i * ld2 + kg - K1]) : 0.f;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -132,6 +140,23 @@ __global__ void __launch_bounds__(GV2_THREADS) dec_gemv2_partial(const float* __
     for (int w = 0; w < GV2_THREADS / 32; ++w) t += red[w][i][cc];
     part[((long long)blockIdx.y * n + i) * N + col] = t;
   }
+  __threadfence();
+  __shared__ unsigned last;
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket + blockIdx.x, 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int x = threadIdx.x; x < n * GV2_COLS; x += blockDim.x) {
+    const int i = x / GV2_COLS, col = blockIdx.x * GV2_COLS + x % GV2_COLS;
+    if (col >= N) continue;
+    float t = 0.f;
+    for (int q = 0; q < (int)gridDim.y; ++q) t += __ldcg(part + ((long long)q * n + i) * N + col);
+    if (bias) t += bias[col];
+    if (act == 1) t = tanhf(t);
+    Y[(long long)i * ldy + col] = t;
+  }
+  if (threadIdx.x == 0) ticket[blockIdx.x] = 0u;
 }
 
 // Y[i][j] = act(sum_ks part[ks][i][j] + bias[j]); act 1 = tanh
@@ -187,7 +212,7 @@ __global__ void dec_lstm_cell(const float* __restrict__ U, const float* __restri
                               float* __restrict__ h_out, float* __restrict__ c_out, float* __restrict__ z_next,
                               int ldz) {
   const int i = blockIdx.x;
-  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+  for (int j = blockIdx.y * blockDim.x + threadIdx.x; j < H; j += gridDim.y * blockDim.x) {
     const float4 u = *(const float4*)(U + ((long long)i * H + j) * 4);
     const float ig = dec_sigmoid(u.x), fg = dec_sigmoid(u.y), gg = tanhf(u.z), og = dec_sigmoid(u.w);
     const float c = fg * c_in[(long long)i * H + j] + ig * gg;

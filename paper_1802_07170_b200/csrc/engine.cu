@@ -751,6 +751,8 @@ class Engine {
   float *dec_hs = nullptr, *dec_fin = nullptr, *dec_st = nullptr, *dec_z = nullptr, *dec_u = nullptr;
   float *dec_ho = nullptr, *dec_y = nullptr, *dec_part = nullptr, *dec_topv = nullptr;
   int *dec_ids = nullptr, *dec_par = nullptr, *dec_topi = nullptr;
+  unsigned* dec_ticket = nullptr;  // dec_gemv2 column-block tickets (self-resetting)
+  static constexpr int DEC_TICKETS = 4096;
   int dec_S = 0, dec_Smax = 0, dec_cur = 0;
   bool dec_ready = false, dec_par_set = false;
   size_t dec_part_n = 0;
@@ -773,6 +775,8 @@ class Engine {
       CMT_CUDA(cudaMalloc(&dec_topi, (size_t)DEC_NMAX * dec::MAXK * 4));
       CMT_CUDA(cudaMalloc(&dec_ids, DEC_NMAX * 4));
       CMT_CUDA(cudaMalloc(&dec_par, DEC_NMAX * 4));
+      CMT_CUDA(cudaMalloc(&dec_ticket, DEC_TICKETS * 4));
+      CMT_CUDA(cudaMemset(dec_ticket, 0, DEC_TICKETS * 4));
     }
     if (S_ > dec_Smax) {
       if (dec_hs) cudaFree(dec_hs);
@@ -785,6 +789,7 @@ class Engine {
       if (p) cudaFree(p);
     for (int* p : {dec_ids, dec_par, dec_topi})
       if (p) cudaFree(p);
+    if (dec_ticket) cudaFree(dec_ticket);
   }
   template <typename T>
   void dec_cvt(const void* src, float* dst, long long n) {
@@ -822,30 +827,23 @@ class Engine {
     dec_ready = true;
   }
   template <typename T>
-  void dec_gemv(const float* Z, int ldz, int n, int K, const T* W, long long ldw, int N, const float* bias, int act,
-                float* Y, int ldy) {
-    if (n <= dec::ROWS) {  // all rows in one pass: every weight byte is read once
-      const int ks = ceil_div(K, GV2_KCH);
-      if ((size_t)ks * n * N > dec_part_n) throw Error(CMT_ERR_INTERNAL, "decode partials too small");
-      static bool attr = false;
-      if (!attr) {
-        CMT_CUDA(cudaFuncSetAttribute(dec_gemv2_partial<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GV2_SMEM));
-        attr = true;
-      }
-      dec_gemv2_partial<T><<<dim3(ceil_div(N, GV2_COLS), ks), GV2_THREADS, GV2_SMEM, st>>>(Z, ldz, n, K, W, ldw, N,
-                                                                                          dec_part);
-      CMT_LAUNCHED(); tl_mark(st, "gemv2 " + std::to_string(n) + "x" + std::to_string(K) + "x" + std::to_string(N));
-      dec_gemv_final<<<(int)ceil_div((long long)n * N, 256), 256, 0, st>>>(dec_part, ks, n, N, bias, act, Y, ldy);
-      CMT_LAUNCHED(); tl_mark(st, "gemv_final");
-      return;
+  void dec_gemv(const float* Z1, int ld1, int K1, const float* Z2, int ld2, int K2, int n, const T* W, long long ldw,
+                int N, const float* bias, int act, float* Y, int ldy) {
+    const int ks = ceil_div(K1 + K2, GV2_KCH);
+    if ((size_t)ks * std::min(n, dec::ROWS) * N > dec_part_n || ceil_div(N, GV2_COLS) > DEC_TICKETS)
+      throw Error(CMT_ERR_INTERNAL, "decode GEMV out of range");
+    static bool attr = false;
+    if (!attr) {
+      CMT_CUDA(cudaFuncSetAttribute(dec_gemv2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GV2_SMEM));
+      attr = true;
     }
-    const int ks = ceil_div(K, dec::KCH);
-    if ((size_t)ks * n * N > dec_part_n) throw Error(CMT_ERR_INTERNAL, "decode partials too small");
-    dim3 g(ceil_div(N, dec::GV_COLS), ks, ceil_div(n, dec::ROWS));
-    dec_gemv_partial<T><<<g, dec::GV_THREADS, 0, st>>>(Z, ldz, n, K, W, ldw, N, dec_part);
-    CMT_LAUNCHED(); tl_mark(st, "gemv " + std::to_string(n) + "x" + std::to_string(K) + "x" + std::to_string(N));
-    dec_gemv_final<<<(int)ceil_div((long long)n * N, 256), 256, 0, st>>>(dec_part, ks, n, N, bias, act, Y, ldy);
-    CMT_LAUNCHED(); tl_mark(st, "gemv_final");
+    for (int r0 = 0; r0 < n; r0 += dec::ROWS) {  // 16 rows per pass (beam sizes up to 16 read the weights once)
+      const int nr = std::min(dec::ROWS, n - r0);
+      dec_gemv2<T><<<dim3(ceil_div(N, GV2_COLS), ks), GV2_THREADS, GV2_SMEM, st>>>(
+          Z1 + (size_t)r0 * ld1, ld1, K1, Z2 ? Z2 + (size_t)r0 * ld2 : nullptr, ld2, K2, nr, W, ldw, N, dec_part,
+          dec_ticket, bias, act, Y + (size_t)r0 * ldy, ldy);
+      CMT_LAUNCHED(); tl_mark(st, "gemv " + std::to_string(nr) + "x" + std::to_string(K1 + K2) + "x" + std::to_string(N));
+    }
   }
   template <typename T>
   void decode_step_t(int n, int k) {
@@ -864,24 +862,23 @@ class Engine {
     for (int k1 = 1; k1 <= L; ++k1) {  // decoder layers (lstm_cell_forward, layers.py:344-363)
       const Layer& ly = layers[L + k1];
       const int din = ly.din;
-      dec_copy_rows<<<n, 256, 0, st>>>(dec_h(in) + (k1 - 1) * ls, H, dec_z + din, zc, H);
-      CMT_LAUNCHED(); tl_mark(st, "dec_copy_rows");
-      dec_gemv<T>(dec_z, zc, n, din + H, wts + ly.w_off, 4LL * H, 4 * H, dw + ly.b_off, 0, dec_u, 4 * H);
-      // the next layer's input (the x rows of z) is this layer's h
-      dec_lstm_cell<<<n, 256, 0, st>>>(dec_u, dec_c(in) + (k1 - 1) * ls, H, dec_h(outb) + (k1 - 1) * ls,
-                                       dec_c(outb) + (k1 - 1) * ls, k1 < L ? dec_z : nullptr, zc);
+      // z = [x; h_prev]: x is the embedding (layer 1) or the layer below's new h
+      const float* xin = (k1 == 1) ? dec_z : dec_h(outb) + (k1 - 2) * ls;
+      dec_gemv<T>(xin, k1 == 1 ? zc : H, din, dec_h(in) + (k1 - 1) * ls, H, H, n, wts + ly.w_off, 4LL * H, 4 * H,
+                  dw + ly.b_off, 0, dec_u, 4 * H);
+      dec_lstm_cell<<<dim3(n, ceil_div(H, 256)), 256, 0, st>>>(dec_u, dec_c(in) + (k1 - 1) * ls, H,
+                                                               dec_h(outb) + (k1 - 1) * ls, dec_c(outb) + (k1 - 1) * ls,
+                                                               nullptr, 0);
       CMT_LAUNCHED(); tl_mark(st, "dec_lstm_cell");
     }
     const float* x = dec_h(outb) + (L - 1) * ls;  // top decoder h [n][H]
     // attention (attend_values): u = W_a^T x; context; H_o = tanh(W_c^T [ctx; x])
-    dec_gemv<T>(x, H, n, H, wts + off_wa, H, H, nullptr, 0, dec_u, H);
+    dec_gemv<T>(x, H, H, nullptr, 0, 0, n, wts + off_wa, H, H, nullptr, 0, dec_u, H);
     dec_attention<<<n, 256, (size_t)dec_S * 4, st>>>(dec_hs, dec_S, H, dec_u, dec_z, zc);
     CMT_LAUNCHED(); tl_mark(st, "dec_attention");
-    dec_copy_rows<<<n, 256, 0, st>>>(x, H, dec_z + H, zc, H);
-    CMT_LAUNCHED(); tl_mark(st, "dec_copy_rows");
-    dec_gemv<T>(dec_z, zc, n, 2 * H, wts + off_wc, H, H, nullptr, 1, dec_ho, H);
+    dec_gemv<T>(dec_z, zc, H, x, H, H, n, wts + off_wc, H, H, nullptr, 1, dec_ho, H);
     // output layer (model.py:232-235), log-softmax and the k best entries per row
-    dec_gemv<T>(dec_ho, H, n, H, wts + off_wo, V, V, dw + off_bo, cfg.output_tanh ? 1 : 0, dec_y, V);
+    dec_gemv<T>(dec_ho, H, H, nullptr, 0, 0, n, wts + off_wo, V, V, dw + off_bo, cfg.output_tanh ? 1 : 0, dec_y, V);
     dec_logsoftmax_topk<<<n, dec::TOPK_THREADS, 0, st>>>(dec_y, V, k, dec_topv, dec_topi, status_d);
     CMT_LAUNCHED(); tl_mark(st, "dec_topk");
     dec_cur = outb;

@@ -125,3 +125,25 @@ def test_decode_errors_and_states():
     with pytest.raises(ConfigError):
         eng.decode_begin([])
     eng.close()
+
+
+@pytest.mark.gpu
+def test_decode_wide_beam_rows_match_single_rows():
+    """More than 16 live rows (two GEMV passes): every row equals the same row
+    decoded alone."""
+    from paper_1802_07170_b200.engine import Engine
+    g = load()
+    model = model_of(g, "d_wide")
+    eng = Engine(model.config, mode="fp32")
+    eng.upload(model.params)
+    src = [int(x) for x in g["d_wide/s1/src"]]
+    toks = [4 + 7 * i for i in range(20)]
+    eng.decode_begin(src)
+    eng.decode_step([2], None, 1)
+    vw, tw = eng.decode_step(toks, [0] * 20, 5)
+    for i in (0, 15, 16, 19):
+        eng.decode_begin(src)
+        eng.decode_step([2], None, 1)
+        v1, t1 = eng.decode_step([toks[i]], [0], 5)
+        assert np.array_equal(t1[0], tw[i]) and np.allclose(v1[0], vw[i], rtol=0, atol=1e-5), i
+    eng.close()
