@@ -46,15 +46,29 @@ struct EpiStore {
   // F = 63: any combination, each stage gated at run time.
   // Every global load of the chunk is issued up front (vectorised where the
   // row is 16-byte aligned) and the element loop is branch-free.
+  // the chunk's 32 bias values; issued by the epilogue before its TMEM load so
+  // the two latencies overlap (compute_t then takes them from `pb`)
+  CMT_D void load_bias(int n0, int N, float* bv) const {
+    if (n0 + 32 <= N && (((uintptr_t)(bias + n0)) & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) *(float4*)&bv[4 * q] = __ldg((const float4*)(bias + n0) + q);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) bv[j] = (n0 + j < N) ? __ldg(bias + n0 + j) : 0.f;
+    }
+  }
   template <int F>
-  CMT_D void compute_t(int m, int n0, const float* v, int M, int N, float* x) const {
+  CMT_D void compute_t(int m, int n0, const float* v, int M, int N, float* x, const float* pb = nullptr) const {
     const bool full = (n0 + 32 <= N);
     const bool row_ok = m < M;
     const long long rm = row_ok ? (long long)m : 0;
     const int fl = (F & 32) ? flags() : F;
     float bv[(F & 1) ? 32 : 1], tg[(F & 8) ? 32 : 1], ad[(F & 16) ? 32 : 1];
     uint8_t km[(F & 4) ? 32 : 1];
-    if ((F & 1) && (fl & 1)) {
+    if ((F & 1) && (fl & 1) && pb) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) bv[j] = pb[j];
+    } else if ((F & 1) && (fl & 1)) {
       if (full && (((uintptr_t)(bias + n0)) & 15) == 0) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) *(float4*)&bv[4 * q] = __ldg((const float4*)(bias + n0) + q);
@@ -107,17 +121,17 @@ struct EpiStore {
   CMT_D int flags() const {
     return (bias ? 1 : 0) | (act == 1 ? 2 : 0) | (dmask ? 4 : 0) | (tgrad_y ? 8 : 0) | (add ? 16 : 0);
   }
-  CMT_D void compute(int m, int n0, const float* v, int M, int N, float* x) const {
+  CMT_D void compute(int m, int n0, const float* v, int M, int N, float* x, const float* pb = nullptr) const {
     switch (flags()) {
       case 0: compute_t<0>(m, n0, v, M, N, x); break;
-      case 1: compute_t<1>(m, n0, v, M, N, x); break;
+      case 1: compute_t<1>(m, n0, v, M, N, x, pb); break;
       case 2: compute_t<2>(m, n0, v, M, N, x); break;
-      case 3: compute_t<3>(m, n0, v, M, N, x); break;
+      case 3: compute_t<3>(m, n0, v, M, N, x, pb); break;
       case 4: compute_t<4>(m, n0, v, M, N, x); break;
       case 8: compute_t<8>(m, n0, v, M, N, x); break;
       case 12: compute_t<12>(m, n0, v, M, N, x); break;
       case 16: compute_t<16>(m, n0, v, M, N, x); break;
-      default: compute_t<63>(m, n0, v, M, N, x);
+      default: compute_t<63>(m, n0, v, M, N, x, pb);
     }
   }
 
@@ -548,6 +562,12 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
 #pragma unroll 1
       for (int c = c_lo; c < ((opt & 4) ? c_lo : c_hi); ++c) {  // opt bit 2: mainloop-only timing experiment
         float v[32];
+        float bvp[32];  // bias prefetch (overlaps the TMEM load)
+        bool pre = false;
+        if constexpr (ST) {  // ST is only instantiated with EpiStore
+          pre = epi.bias != nullptr && n0 + c * 32 < N;
+          if (pre) epi.load_bias(n0 + c * 32, N, bvp);
+        }
         if (num_kb > 0) {
           ptx::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN + c * 32, v);
         } else {
@@ -562,7 +582,7 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
           }
           if (nc < N && mw < M) {
             float x[32];
-            epi.compute(m, nc, v, M, N, x);
+            epi.compute(m, nc, v, M, N, x, pre ? bvp : nullptr);
             if (opt & 8) {  // timing experiment: no store
               if (x[lane] == 123.456f) epi.C = nullptr;
               continue;
