@@ -1320,7 +1320,6 @@ class Engine {
     prm.hrow0 = f.reverse ? B : 0;
     prm.trace = (trace_layer == f.l) ? trace_d : nullptr;
     prm.stages = mc::Fwd<ROWS>::stages(H);
-    CMT_CUDA(cudaMemsetAsync(prm.flag, 0, FLAG_STRIDE * 4, st));
     return prm;
   }
   // lstm_fwd_tm<ROWS>: one or two scans per cooperative launch
@@ -1449,7 +1448,6 @@ class Engine {
       prm.hrow0 = reverse ? B : 0;
       prm.trace = (trace_layer == l) ? trace_d : nullptr;
       prm.stages = cl::fwd_stages(H);
-      CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
       launch_coop(lstm_fwd_cluster, cl::FWD_KS * (4 * H / cl::FWD_NG), tmH, tmW, prm, cl::fwd_smem(H), cl::FWD_KS);
       return;
     }
@@ -1464,7 +1462,6 @@ class Engine {
       prm.hrow0 = reverse ? B : 0;
       prm.trace = (trace_layer == l) ? trace_d : nullptr;
       prm.stages = pr::stages_for(H);
-      CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
       launch_coop(lstm_fwd_persistent, 4 * H / pr::FWD_NG * ceil_div(B, pr::ROWS), tmH, tmW, prm);
       return;
     }
@@ -1577,7 +1574,6 @@ class Engine {
     prm.steps = f.steps; prm.B = B; prm.H = H; prm.din = f.din; prm.reverse = f.reverse ? 1 : 0;
     prm.trace = (trace_layer == 100 + f.l) ? trace_d : nullptr;
     prm.stages = mc::Bwd<ROWS>::stages(H);
-    CMT_CUDA(cudaMemsetAsync(prm.flag, 0, FLAG_STRIDE * 4, st));
     return prm;
   }
   template <int ROWS>
@@ -1665,7 +1661,6 @@ class Engine {
       prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
       prm.trace = (trace_layer == 100 + l) ? trace_d : nullptr;
       prm.stages = cl::bwd_stages(H);
-      CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
       launch_coop(lstm_bwd_cluster, cl::BWD_KS * (H / cl::BWD_NU), tmA, tmW, prm, cl::bwd_smem(H), cl::BWD_KS);
     } else if (use_persistent()) {
       CUtensorMap tmA, tmW;
@@ -1678,7 +1673,6 @@ class Engine {
       prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
       prm.trace = nullptr;
       prm.stages = pr::stages_for(H);
-      CMT_CUDA(cudaMemsetAsync(prm.flag, 0, 4, st));
       launch_coop(lstm_bwd_persistent, H / pr::BWD_NU * ceil_div(B, pr::ROWS), tmA, tmW, prm);
     } else
     for (int p = steps - 1; p >= 0; --p) {
@@ -1799,6 +1793,9 @@ class Engine {
     double ntok = a.global_ntok > 0 ? a.global_ntok : ntok_local;
     float inv_ntok = ntok > 0 ? (float)(1.0 / (double)(float)ntok) : 0.f;
     CMT_CUDA(cudaMemsetAsync(out_d, 0, sizeof(StepOut), st));
+    // every recurrent launch of the step owns one flag region (forward layer l:
+    // region l, BPTT: region 32 + l): one memset instead of one per launch
+    CMT_CUDA(cudaMemsetAsync(flags, 0, 64 * FLAG_STRIDE * 4, st));
     tl_mark(st, "<start>");
 
     // ===== forward =====
