@@ -1194,14 +1194,15 @@ class Engine {
     jump_ok = true;
   }
   template <typename TI, typename TO>
-  void launch_dropout(const void* x, void* y, uint8_t* keep, int N, unsigned long long base, const Pcg& pcg) {
-    if (use_jump == 1) {
+  void launch_dropout(const void* x, void* y, uint8_t* keep, int N, unsigned long long base, const Pcg& pcg,
+                      const void* x2 = nullptr) {
+    if (use_jump == 1 || x2) {
       ensure_jump(pcg);
       dim3 blk(32, 8);
       dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, DROP4_DPT), 8));
       float scale = 1.0f / (float)(1.0 - cfg.dropout);
       dropout_fwd_kernel4<TI, TO><<<grid, blk, 0, st>>>((const TI*)x, (TO*)y, keep, N, H, pcg, jump_d, base,
-                                                        dropout_threshold(cfg.dropout), scale);
+                                                        dropout_threshold(cfg.dropout), scale, (const TI*)x2);
       CMT_LAUNCHED(); tl_mark(st, "dropout_fwd_kernel4");
       return;
     }
@@ -1836,6 +1837,13 @@ class Engine {
       dropout_site(cur, drop_enc[k], keep_enc[k], NS, enc_base(k));
       return drop_enc[k];
     };
+    // enc.l2's input: dropout(y_f + y_b) in one pass (the sum is not stored)
+    auto enc_input_l1sum = [&]() -> const void* {
+      ScanViews f = views(0, false), r = views(1, true);
+      if (bf) launch_dropout<bf16, bf16>(f.ybase, drop_enc[2], keep_enc[2], (int)NS, enc_base(2), pcg, r.ybase);
+      else launch_dropout<float, float>(f.ybase, drop_enc[2], keep_enc[2], (int)NS, enc_base(2), pcg, r.ybase);
+      return drop_enc[2];
+    };
     auto add_top = [&]() {
       ScanViews f = views(0, false), r = views(1, true);
       if (bf) add2_kernel<bf16><<<grid_for(NS * H), 256, 0, st>>>((const bf16*)f.ybase, (const bf16*)r.ybase, (bf16*)top, NS * H);
@@ -1873,14 +1881,17 @@ class Engine {
           g_grid_cap = 0;
         });
       }
-      add_top();
+      // with dropout the summed top is only the input of enc.l2's dropout site:
+      // the sum is formed inside that dropout kernel (no separate add pass)
+      const bool fused_top = drop && L >= 2;
+      if (!fused_top) add_top();
       const void* cur = top;
       for (int k = 2; k <= L; ++k) {
         // the two scans' inputs (dropout, initial state, input projection) are
         // independent: the decoder side is issued on the side stream
         const bool ov = use_overlap();
         if (ov) fork();
-        const void* in = enc_input(k, cur);
+        const void* in = (k == 2 && fused_top) ? enc_input_l1sum() : enc_input(k, cur);
         zero_enc_state(k);
         FwdScan e{k, in, H, S, false, src_mask_d, ux};
         fwd_prep(e);

@@ -257,7 +257,7 @@ constexpr int DROP4_DPT = 32;
 template <typename TI, typename TO>
 __global__ void dropout_fwd_kernel4(const TI* __restrict__ x, TO* __restrict__ y, uint8_t* __restrict__ keep, int N,
                                     int H, Pcg pcg, const PcgJump* __restrict__ jt, unsigned long long base,
-                                    unsigned long long thr, float scale) {
+                                    unsigned long long thr, float scale, const TI* __restrict__ x2 = nullptr) {
   const int h = blockIdx.x * 32 + threadIdx.x;
   const int n0 = (blockIdx.y * blockDim.y + threadIdx.y) * DROP4_DPT;
   if (h >= H || n0 >= N) return;
@@ -278,7 +278,9 @@ __global__ void dropout_fwd_kernel4(const TI* __restrict__ x, TO* __restrict__ y
     const unsigned long long r = (xr >> rot) | (xr << ((64 - rot) & 63));
     const bool k = (r >> 11) >= thr;
     keep[i] = k;
-    const float xv = to_f<TI>(x[i]);
+    // x2: the input is x + x2 rounded to TI, exactly what add2_kernel stores
+    // (the bidirectional sum of encoder layer 1, layers.py:162-180)
+    const float xv = x2 ? to_f<TI>(from_f<TI>(to_f<TI>(x[i]) + to_f<TI>(x2[i]))) : to_f<TI>(x[i]);
     y[i] = from_f<TO>(k ? xv * scale : xv * 0.f);
   }
 }
