@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcytonb200.so")
+# CMT_LIB: an alternative build of the same library (A/B timing of two builds)
+LIB_PATH = os.environ.get("CMT_LIB") or os.path.join(HERE, "libcytonb200.so")
 
 CMT_OK = 0
 CMT_ERR_CONFIG = 1
