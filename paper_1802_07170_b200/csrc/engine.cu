@@ -414,7 +414,7 @@ class Engine {
   int bwd_tm = 0;
   int use_jump = 1;    // option: table-driven PCG64 jump-ahead dropout kernel
   int ce2 = 2;         // option: fused CE + bias-grad column sums: 2 two-pass (stats, gradient), 1 persistent one-pass
-  bool use_ce2() const { return bf && ce2 && V % 8 == 0 && V <= CE2_MAXV; }
+  bool use_ce2() const { return bf && ce2 && V % 8 == 0 && (ce2 == 2 || V <= CE2_MAXV); }  // two-pass: any V
   // data parallel (NCCL): dense all-reduce of grads, loss and status
   void* comm = nullptr;
   int rank = 0, world = 1;
