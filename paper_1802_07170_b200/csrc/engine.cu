@@ -1415,12 +1415,15 @@ class Engine {
 
   void scan_fwd(int l, const void* X, int din, int steps, bool reverse, const float* mask) {
     // single scans: lstm_fwd_multi<64> (128 CTAs, 6.4 us/step at c3) beats the
-    // TMEM-split kernel with 32-row slices (6.9 us/step); the latter is kept
-    // behind fwd_tm=2 for measurement
-    if (fwd_tm == 2 && (fwd_tm_ok<32>() || fwd_tm_ok<64>())) {
+    // TMEM-split kernel with 32-row slices (6.9 us/step), but when the batch
+    // needs 128-row multi slices (B > 128) the TMEM-split kernel with 64-row
+    // slices is faster (c5: 28.5 -> 28.2 ms/step); fwd_tm=2 forces it
+    const bool tm_single = fwd_tm == 2 ? (fwd_tm_ok<32>() || fwd_tm_ok<64>())
+                                       : (fwd_tm == 1 && single_fwd_rows() == 128 && fwd_tm_ok<64>());
+    if (tm_single) {
       FwdScan f{l, X, din, steps, reverse, mask, ux};
       fwd_prep(f);
-      if (fwd_tm_ok<32>()) fwd_tm_launch<32>(f, nullptr);
+      if (fwd_tm == 2 && fwd_tm_ok<32>()) fwd_tm_launch<32>(f, nullptr);
       else fwd_tm_launch<64>(f, nullptr);
       return;
     }
