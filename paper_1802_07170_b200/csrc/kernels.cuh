@@ -40,6 +40,11 @@ __global__ void gather_rows_kernel(const T* __restrict__ table, int E, const int
   if (n >= N) return;
   const T* src = table + (long long)ids[n] * E;
   T* dst = out + (long long)n * E;
+  if (((E * sizeof(T)) & 15) == 0 && (((uintptr_t)table | (uintptr_t)out) & 15) == 0) {  // 16-byte rows
+    const int nv = (int)(E * sizeof(T) / 16);
+    for (int e = threadIdx.x; e < nv; e += blockDim.x) ((uint4*)dst)[e] = __ldg((const uint4*)src + e);
+    return;
+  }
   for (int e = threadIdx.x; e < E; e += blockDim.x) dst[e] = src[e];
 }
 
@@ -147,6 +152,36 @@ __global__ void add2_kernel(const T* __restrict__ a, const T* __restrict__ b, T*
 template <typename TS, typename TD>
 __global__ void copy2d_kernel(const TS* __restrict__ s, long long lds, TD* __restrict__ d, long long ldd, int rows,
                               int cols) {
+  // 8 elements per thread when rows are 8-aligned (16-byte bf16 / 32-byte fp32 accesses)
+  if ((cols & 7) == 0 && (lds & 7) == 0 && (ldd & 7) == 0 && (((uintptr_t)s | (uintptr_t)d) & 31) == 0) {
+    const long long n8 = (long long)rows * (cols >> 3);
+    const int c8 = cols >> 3;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+      const long long r = i / c8, c = (i % c8) * 8;
+      const TS* sp = s + r * lds + c;
+      TD* dp = d + r * ldd + c;
+      float f[8];
+      if constexpr (sizeof(TS) == 2) {
+        const uint4 q = *(const uint4*)sp;
+        const bf16* b = (const bf16*)&q;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = __bfloat162float(b[j]);
+      } else {
+        const float4 a = *(const float4*)sp, b = *((const float4*)sp + 1);
+        f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+      }
+      if constexpr (sizeof(TD) == 2) {
+        __align__(16) bf16 o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16_rn(f[j]);
+        *(uint4*)dp = *(const uint4*)o;
+      } else {
+        *(float4*)dp = make_float4(f[0], f[1], f[2], f[3]);
+        *((float4*)dp + 1) = make_float4(f[4], f[5], f[6], f[7]);
+      }
+    }
+    return;
+  }
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)rows * cols;
        i += (long long)gridDim.x * blockDim.x) {
     long long r = i / cols, c = i % cols;
@@ -982,6 +1017,25 @@ __global__ void sgd_rows_kernel(float* __restrict__ table, bf16* __restrict__ sh
   if (u >= nrows) return;
   const float s = *s32;
   long long r = (long long)ids[u] * E;
+  if ((E & 3) == 0) {  // float4 rows (the arena and tables are 256-byte aligned)
+    float4* tw = (float4*)(table + r);
+    const float4* g4 = (const float4*)(gc + (long long)u * E);
+    for (int e = threadIdx.x; e < (E >> 2); e += blockDim.x) {
+      const float4 w = tw[e], gv = g4[e];
+      float4 nw;
+      nw.x = __fsub_rn(w.x, __fmul_rn(s, gv.x));
+      nw.y = __fsub_rn(w.y, __fmul_rn(s, gv.y));
+      nw.z = __fsub_rn(w.z, __fmul_rn(s, gv.z));
+      nw.w = __fsub_rn(w.w, __fmul_rn(s, gv.w));
+      tw[e] = nw;
+      if (shadow) {
+        __align__(8) bf16 b4[4] = {__float2bfloat16_rn(nw.x), __float2bfloat16_rn(nw.y), __float2bfloat16_rn(nw.z),
+                                   __float2bfloat16_rn(nw.w)};
+        *(uint2*)(shadow + r + 4 * e) = *(uint2*)b4;
+      }
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     float nw = __fsub_rn(table[r + e], __fmul_rn(s, gc[(long long)u * E + e]));
     table[r + e] = nw;
