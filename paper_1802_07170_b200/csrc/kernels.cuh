@@ -924,15 +924,28 @@ __global__ void sumsq_partial_kernel(const float* __restrict__ g, long long n, d
   if ((((uintptr_t)g) & 15) == 0) {
     const long long n4 = n >> 2;
     const float4* g4 = (const float4*)g;
-    for (long long i = tid; i < n4; i += stride) {
+    long long i = tid;
+    for (; i + 3 * stride < n4; i += 4 * stride) {  // 4 independent 16-byte loads in flight
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(g4 + i + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a = fmaf(v[u].x, v[u].x, a);
+        a = fmaf(v[u].y, v[u].y, a);
+        a = fmaf(v[u].z, v[u].z, a);
+        a = fmaf(v[u].w, v[u].w, a);
+      }
+      if (++cnt == 16) { ad += a; a = 0.f; cnt = 0; }
+    }
+    for (; i < n4; i += stride) {
       const float4 v = g4[i];
       a = fmaf(v.x, v.x, a);
       a = fmaf(v.y, v.y, a);
       a = fmaf(v.z, v.z, a);
       a = fmaf(v.w, v.w, a);
-      if (++cnt == 64) { ad += a; a = 0.f; cnt = 0; }
     }
-    for (long long i = 4 * n4 + tid; i < n; i += stride) a = fmaf(g[i], g[i], a);
+    for (long long j = 4 * n4 + tid; j < n; j += stride) a = fmaf(g[j], g[j], a);
   } else {
     for (long long i = tid; i < n; i += stride) {
       float v = g[i];
