@@ -456,3 +456,25 @@ def test_ce_variants_agree(tanh_):
         assert abs(loss - ol) <= BF16_TOL * abs(ol), ce2
         for n in ("out.w", "out.b", "att.w_c.w", "tgt_embed"):
             assert O.norm_rel_err(grads[n], og[n]) < BF16_TOL, (ce2, n)
+
+
+def test_pipeline_numeric_error_surfaces_at_collection():
+    """Engine.pipeline: a non-finite step raises NumericError when its result is
+    collected, before the next batch is launched, and the device skipped its
+    update (training.py:128-135, 148-155)."""
+    from paper_1802_07170_b200.engine import Engine
+    from paper_1802_07170_b200.errors import NumericError
+    from paper_1802_07170_b200.model import Batch
+    from tests.gpu_helpers import cfg_of
+    d, params, (src, sm, tgt, tm) = _small()
+    params = {k: v.copy() for k, v in params.items()}
+    params["out.w"][5, 3] = np.nan
+    eng = Engine(cfg_of(d), mode="bf16")
+    eng.upload(params)
+    gen = eng.pipeline(iter([Batch(src, tgt, sm, tm)] * 3), 1.0, 5.0, 0.1, np.random.default_rng(0))
+    with pytest.raises(NumericError):
+        next(gen)
+    after = eng.params()
+    for n in params:
+        assert np.array_equal(after[n], params[n], equal_nan=True), n
+    eng.close()
