@@ -21,6 +21,7 @@ import subprocess
 import sys
 import tempfile
 import time
+import types
 
 import numpy as np
 
@@ -55,12 +56,13 @@ def synthetic_batch(V, S, T, B, seed):
 
 
 def peaks():
+    """(burst bf16 TF/s, sustained bf16 TF/s, HBM GB/s, source) from MEASURED_PEAKS.json."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p["bf16_tflops_sustained"], p["hbm_gbs"], "measured (MEASURED_PEAKS.json, sustained bf16)"
+        return p["bf16_tflops"], p["bf16_tflops_sustained"], p["hbm_gbs"], "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
+        return 1639.1, 1380.2, 6551.4, "fallback (SURVEY §8(d) / B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -174,6 +176,30 @@ def gemm_roofline(bd, peak_tf):
             "source": "per-launch CUDA events on the engine stream (one untimed step, side stream off)"}
 
 
+def hbm_classes(tl, cfg_t, peak_hbm):
+    """Achieved HBM bandwidth of the bandwidth-bound kernel classes of one
+    serialised step (algorithmic bytes) against the HBM peak."""
+    V, E, H, L, B, S, T = cfg_t
+    NS, NT = S * B, T * B
+    # dense (non-embedding) parameters: 3 layers read E + H inputs, 2(L-1) read 2H; attention; output
+    dense = 3 * ((E + H) * 4 * H + 4 * H) + 2 * (L - 1) * (2 * H * 4 * H + 4 * H) + 3 * H * H + H * V + V
+    cls = {
+        # two-pass CE: stats read the bf16 logits, the gradient pass reads and rewrites them
+        "CE (ce_stats + ce_grad)": (("ce_stats", "ce_grad"), 3 * 2.0 * NT * V),
+        # norm (fp32 grad read) + SGD (fp32 w, g read, w write, bf16 shadow write), dense part only
+        "norm + SGD (dense)": (("sumsq", "sgd_dense", "clip"), (4 + 14) * float(dense)),
+        # dropout: read x (bf16), write y (bf16) and the keep byte, per element of each site
+        "dropout (7 sites)": (("dropout",), 5.0 * H * ((L - 1) * NS + (L - 1) * NT + NT)),
+    }
+    out = {}
+    for name, (prefixes, nbytes) in cls.items():
+        ms = sum(m for lab, m in tl if lab.startswith(prefixes))
+        if ms > 0:
+            gbs = nbytes / (ms / 1e3) / 1e9
+            out[name] = {"bytes": nbytes, "ms": round(ms, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peak_hbm, 3)}
+    return out
+
+
 def run_reference(args, cfg_t):
     """--impl reference: the reference's CPU implementation of the path, timed here."""
     from paper_1802_07170_b200.model import Model, ModelConfig, Rng
@@ -255,7 +281,7 @@ def main():
     clocks = ClockSampler(local)
     time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
     clocks.mark()
-    eng.set_option("time_dominant", 1)
+    eng.set_option("time_dominant", 7)  # CUDA-event probes: logits GEMM, BPTT scans, forward scans
     l0 = launch_count()
     eng.record(0)
     for _ in range(args.steps):
@@ -264,7 +290,7 @@ def main():
     r = eng.wait()
     ms_total = eng.elapsed_ms(0, 1)
     launches = (launch_count() - l0) // args.steps
-    dom_ms, dom_n = eng.stat("dominant_ms")
+    probes = {c: eng.stat(f"probe_ms:{c}") for c in (0, 1, 2)}  # (mean ms per launch, launches)
     eng.set_option("time_dominant", 0)
     ck = clocks.stop()
 
@@ -279,20 +305,29 @@ def main():
         breakdown = step_breakdown(tl)
 
     # ---- end-to-end through the public API (host buffers, H2D + D2H inside) ----
+    # The reference-facing call: training.train_step(model, batch, cfg, lr, rng)
+    # (training.py:145-159) with device-resident parameters (sync="lazy", the
+    # mode install() wires into the reference Trainer): every step validates and
+    # converts the host ids/masks, segment-sorts the embedding rows, copies them
+    # H2D, runs the step and reads the loss back as a Python float.
+    from paper_1802_07170_b200 import training as TR
+    TR._ENGINES[model] = eng
+    tcfg = types.SimpleNamespace(grad_clip_norm=clip, label_smoothing=eps)
     if dist:
         dist.barrier()
-    # Engine.pipeline: the public training-loop API; every step stages its
-    # batch from host arrays (validation, id conversion, segment sort, pinned
-    # H2D) and reads its loss back, the host work of step i+1 overlapping the
-    # device work of step i
     eng.record(2)
     t0 = time.perf_counter()
-    for loss, _ in eng.pipeline((batch for _ in range(args.steps)), lr, clip, eps, rng, global_ntok=ntok_global):
-        pass
+    for _ in range(args.steps):
+        loss = TR.train_step(model, batch, tcfg, lr, rng, sync="lazy")
     t_e2e = time.perf_counter() - t0
     eng.record(3)
-    ms_e2e_dev = eng.elapsed_ms(2, 3)
-    ms_e2e = max(1e3 * t_e2e, ms_e2e_dev)
+    ms_e2e = max(1e3 * t_e2e, eng.elapsed_ms(2, 3))
+    # Engine.pipeline: the same per-step work with batch i+1 staged on the host
+    # while step i runs on the device
+    t0 = time.perf_counter()
+    for _ in eng.pipeline((batch for _ in range(args.steps)), lr, clip, eps, rng, global_ntok=ntok_global):
+        pass
+    ms_pipe = 1e3 * (time.perf_counter() - t0)
 
     ms_step = ms_total / args.steps
     if dist:
@@ -303,19 +338,40 @@ def main():
         ms_e2e_step = ms_e2e / args.steps
     value = world * ntok_local / (ms_step / 1e3)
     e2e_value = world * ntok_local / (ms_e2e_step / 1e3)
+    pipe_value = world * ntok_local / (ms_pipe / args.steps / 1e3)
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
-    peak_tf, peak_hbm, peak_src = peaks()
-    dom_flops = 2.0 * T * B * H * V
-    achieved = dom_flops / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else None
+    burst_tf, sus_tf, peak_hbm, peak_src = peaks()
+    # the run's clocks decide the denominator: burst unless the power cap engaged
+    capped = bool(ck and "sw_power_cap" in ck.get("reasons", []))
+    peak_tf = sus_tf if capped else burst_tf
+    peak_src += ", sustained bf16 (power cap seen)" if capped else ", burst bf16 (no power cap in the timed region)"
+    # roofline of the kernel class with the largest device time per step
+    # (CUDA events around its launches on the engine stream, inside the timed steps)
+    rec = 2.0 * B * 4 * H * H * (L * T + (L + 1) * S)  # recurrent products of all 2L+1 scans
+    kinds = {
+        0: ("logits GEMM tanh(W_o^T H_o + b_o) (tcgen05 CTA-pair, gemm_tc_kernel)", 2.0 * T * B * H * V),
+        1: ("recurrent BPTT scans (lstm_bwd_multi, persistent tcgen05)", rec),
+        2: ("recurrent forward scans (lstm_fwd_tm / lstm_fwd_multi, persistent tcgen05)", rec),
+    }
+    classes = {}
+    for c, (name, fl) in kinds.items():
+        mean_ms, n = probes[c]
+        ms = mean_ms * n / args.steps
+        if ms > 0:
+            ach = fl / (ms / 1e3) / 1e12
+            classes[c] = {"kernel": name, "ms_per_step": ms, "launches_per_step": n / args.steps,
+                          "flops_per_step": fl, "achieved": ach, "frac": ach / peak_tf}
+    dom = max(classes, key=lambda c: classes[c]["ms_per_step"]) if classes else None
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "dominant_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and dom is not None:
         try:
-            traffic = json.load(open(tpath)).get("bytes_per_launch")
+            tj = json.load(open(tpath))
+            traffic = tj.get(str(dom), {}).get("bytes_per_launch") if isinstance(tj.get(str(dom)), dict) else None
         except Exception:
             traffic = None
     fstep = flops_per_step(*cfg_t)
@@ -328,13 +384,21 @@ def main():
                    "global_batch": B * world, "src_len": S, "tgt_len": T, "dropout": 0.2, "label_smoothing": eps,
                    "clip": clip, "parallelism": f"dp{world}",
                    "l2": "working set > L2 (bf16 logits alone 0.64 GB per step)"},
-        "e2e": {"value": e2e_value, "unit": "tgt_tok/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40},
+        "e2e": {"value": e2e_value, "unit": "tgt_tok/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40,
+                "api": "paper_1802_07170_b200.training.train_step (reference signature, sync='lazy')"},
+        "e2e_pipeline": {"value": pipe_value, "unit": "tgt_tok/s",
+                         "api": "Engine.pipeline (host staging of batch i+1 overlaps step i)"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "tensor", "kernel": "logits GEMM (tanh(W_o^T H_o + b_o), K13) tcgen05",
-                     "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": (achieved / peak_tf) if achieved else None, "traffic": traffic,
-                     "flops_per_launch": dom_flops, "launch_ms": dom_ms, "launches_timed": dom_n,
-                     "peak_source": peak_src},
+        "roofline": None if dom is None else {
+            "bound": "tensor", "kernel": classes[dom]["kernel"], "achieved": classes[dom]["achieved"],
+            "peak": peak_tf, "unit": "TFLOP/s", "frac": classes[dom]["frac"], "traffic": traffic,
+            "flops_per_launch": classes[dom]["flops_per_step"] / classes[dom]["launches_per_step"],
+            "launch_ms": classes[dom]["ms_per_step"] / classes[dom]["launches_per_step"],
+            "launches_per_step": classes[dom]["launches_per_step"], "peak_source": peak_src},
+        "roofline_classes": {v["kernel"].split(" (")[0]: {k: (round(x, 4) if isinstance(x, float) else x)
+                                                       for k, x in v.items() if k != "kernel"}
+                             for v in classes.values()},
+        "hbm_classes": hbm_classes(tl, cfg_t, peak_hbm) if breakdown else None,
         "gemm_roofline": gemm_roofline(breakdown, peak_tf),
         "breakdown": breakdown and breakdown["shares"],
         "step_roofline": {"flops_per_step": fstep, "achieved_tflops": fstep / (ms_step / 1e3) / 1e12,

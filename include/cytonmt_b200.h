@@ -60,7 +60,7 @@ typedef struct {
 /* per-step arguments: TrainConfig fields used by train_step + the dropout RNG */
 typedef struct {
   double lr;          /* learning rate (train_step arg) */
-  double clip_norm;   /* TrainConfig.grad_clip_norm; <= 0 means None */
+  double clip_norm;   /* TrainConfig.grad_clip_norm; < 0 (or NaN) means None; 0 clips to a zero step */
   double epsilon;     /* TrainConfig.label_smoothing */
   unsigned long long pcg_state_hi, pcg_state_lo, pcg_inc_hi, pcg_inc_lo; /* numpy PCG64 state */
   double global_ntok; /* data-parallel: sum of tgt_mask over all ranks (<= 0: this batch) */
@@ -88,19 +88,34 @@ int cmt_block_info(cmt_engine* e, int idx, char* name, int name_cap, long long* 
 int cmt_upload_param(cmt_engine* e, int idx, const float* host_rowmajor, long long rows, long long cols);
 int cmt_download_param(cmt_engine* e, int idx, float* host_rowmajor, long long rows, long long cols);
 int cmt_download_grad(cmt_engine* e, int idx, float* host_rowmajor, long long rows, long long cols);
+/* ParamBlock.learnable (graph.py:20-31): a frozen block (learnable = 0) is left
+ * out of the global grad norm and the update (training.py:128-139); its grad is
+ * still computed (cmt_download_grad).  Every block starts learnable. */
+int cmt_set_learnable(cmt_engine* e, int idx, int learnable);
 
-/* GPU translation.  decode_begin encodes one source
- * sentence (ids int64, length S) with the INFER-mode forward and sets the
- * decoder states to the encoder finals (model.py:180-208).  decode_step runs
- * model.decode_step (model.py:211-236) for n <= 64 live hypotheses: row i
- * feeds token prev_tokens[i] to the state row parent[i] of the previous call's
- * output (parent = NULL: the encoder finals), and returns the k <= 32 best
- * log-probabilities of each row with their token ids, ordered by log-prob
- * descending then token ascending (the tie order of decoding.py:120-121).
- * The host drives beam search / greedy decoding (decoding.py:89-184). */
-int cmt_decode_begin(cmt_engine* e, const long long* src_ids, int S);
-int cmt_decode_step(cmt_engine* e, int n, const long long* prev_tokens, const int* parent, int k,
-                    float* top_logprob, int* top_token);
+/* GPU translation: batched beam search on the device.
+ * The reference translates sentence by sentence, one decode_step per live
+ * hypothesis (decoding.py:89-153, model.py:180-236).  cmt_beam_begin encodes a
+ * padded batch of B source sentences (ids int64 (S, B) C order, mask float32
+ * {0,1}) with the INFER-mode forward and starts one beam of `beam` (<= 32)
+ * slots per sentence; max_len[b] = DecodeConfig.cap_for(len) (>= 1);
+ * lp_table[n] = length_penalty(n) = ((5 + n) / 6) ** alpha for n in
+ * [0, lp_table_len), lp_table_len >= max(max_len) + 2 (computed by the caller
+ * so scores are bit-identical to the reference's).  cmt_beam_step runs up to
+ * max_steps decoder steps for every unfinished sentence (all live hypotheses of
+ * all sentences as the rows of one step) and returns the number of sentences
+ * still searching.  Once that is 0, cmt_beam_result returns sentence b's
+ * result `rank`: the finished hypotheses ordered by (score desc, arrival
+ * asc), at most max(n_best, 1), tokens without the final EOS (*n_results = how
+ * many); when nothing finished within max_len, one truncated entry (the best
+ * live hypothesis, *truncated = 1, *score = NaN: the caller divides log_prob by
+ * length_penalty(max(len, 1)) as decoding.py:150-153).  Greedy decoding is the
+ * beam of 1 with alpha = 0 (decoding.py:156-171). */
+int cmt_beam_begin(cmt_engine* e, const long long* src_ids, const float* src_mask, int S, int B, int beam,
+                   int n_best, const int* max_len, const double* lp_table, int lp_table_len);
+int cmt_beam_step(cmt_engine* e, int max_steps, int* n_active);
+int cmt_beam_result(cmt_engine* e, int b, int rank, int* tokens, int cap, int* n_tokens, double* score,
+                    double* log_prob, int* truncated, int* n_results);
 
 /* device-resident parameter snapshots: replaces the host round trip of
  * ModelParams.copy_data / load_data (model.py:104-115) that the Trainer uses
@@ -127,6 +142,9 @@ int cmt_wait(cmt_engine* e, cmt_step_result* res);
 /* data parallel: NCCL communicator from a 128-byte ncclUniqueId (from cmt_nccl_unique_id on rank 0).
    Grads, loss and status are summed over ranks inside every step; pass global_ntok in cmt_step_args. */
 int cmt_set_comm(cmt_engine* e, const void* nccl_unique_id, int rank, int world);
+/* the rule that combines the ranks' status words inside a data-parallel step
+ * (flag by flag: a flag is raised iff some rank raised it); host-only, no GPU */
+int cmt_status_combine(const int* words, int n);
 int cmt_nccl_unique_id(void* out128);
 
 /* timing / introspection */

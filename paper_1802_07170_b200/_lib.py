@@ -37,7 +37,7 @@ EXPORTS = [
     "cmt_run_step", "cmt_train_step", "cmt_wait", "cmt_set_comm", "cmt_nccl_unique_id", "cmt_event_record",
     "cmt_event_elapsed", "cmt_launch_count", "cmt_set_option", "cmt_get_stat", "cmt_debug_buffer", "cmt_test_gemm", "cmt_test_dropout", "cmt_timeline",
     "cmt_snapshot_save", "cmt_snapshot_restore", "cmt_snapshot_download", "cmt_snapshot_free",
-    "cmt_decode_begin", "cmt_decode_step",
+    "cmt_beam_begin", "cmt_beam_step", "cmt_beam_result", "cmt_set_learnable", "cmt_status_combine",
 ]
 
 
@@ -88,13 +88,17 @@ def load(path=LIB_PATH):
     for f in (lib.cmt_snapshot_save, lib.cmt_snapshot_restore, lib.cmt_snapshot_free):
         f.argtypes = [VP, I]
     lib.cmt_snapshot_download.argtypes = [VP, I, I, fp, LL, LL]
-    lib.cmt_decode_begin.argtypes = [VP, llp, I]
-    lib.cmt_decode_step.argtypes = [VP, I, llp, P(I), I, fp, P(I)]
+    dp = P(D)
+    lib.cmt_beam_begin.argtypes = [VP, llp, fp, I, I, I, I, P(I), dp, I]
+    lib.cmt_beam_step.argtypes = [VP, I, P(I)]
+    lib.cmt_beam_result.argtypes = [VP, I, I, P(I), I, P(I), dp, dp, P(I), P(I)]
     lib.cmt_stage_batch.argtypes = [VP, llp, fp, I, llp, fp, I, I]
     lib.cmt_run_step.argtypes = [VP, P(StepArgs), P(StepResult)]
     lib.cmt_train_step.argtypes = [VP, llp, fp, I, llp, fp, I, I, P(StepArgs), P(StepResult)]
     lib.cmt_wait.argtypes = [VP, P(StepResult)]
     lib.cmt_set_comm.argtypes = [VP, VP, I, I]
+    lib.cmt_set_learnable.argtypes = [VP, I, I]
+    lib.cmt_status_combine.argtypes = [P(I), I]
     lib.cmt_nccl_unique_id.argtypes = [VP]
     lib.cmt_event_record.argtypes = [VP, I]
     lib.cmt_event_elapsed.argtypes = [VP, I, I, P(ctypes.c_float)]

@@ -34,7 +34,8 @@ enum Status {
 };
 
 // device status bits (set by kernels, read once per step)
-enum StatusBits { ST_SCORES = 1, ST_LOGITS = 2, ST_LOSS = 4, ST_NORM = 8 };
+// ST_HANG: a recurrent scan's flag wait exceeded its budget (lstm_common.cuh SpinGuard)
+enum StatusBits { ST_SCORES = 1, ST_LOGITS = 2, ST_LOSS = 4, ST_NORM = 8, ST_HANG = 16 };
 
 #define CMT_CUDA(x)                                                                   \
   do {                                                                                \

@@ -27,11 +27,8 @@
 #include "../../include/cytonmt_b200.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
-#include "lstm_persistent.cuh"
-#include "lstm_cluster.cuh"
 #include "lstm_multi.cuh"
 #include "lstm_tm.cuh"
-#include "lstm_tm_bwd.cuh"
 #include "attention.cuh"
 #include "decode.cuh"
 
@@ -124,7 +121,7 @@ struct NcclApi {
 };
 static NcclApi g_nccl;
 struct NcclUid { char internal[128]; };
-enum { NCCL_INT32 = 2, NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8, NCCL_SUM = 0 };
+enum { NCCL_INT32 = 2, NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8, NCCL_SUM = 0, NCCL_MAX = 2 };
 
 struct Mat {
   const void* p;
@@ -133,6 +130,20 @@ struct Mat {
 };
 
 static int g_num_sms = 148;
+// Recurrent scans are cooperative launches (every CTA co-resident: the steps
+// wait on each other's readiness flags).  Under a profiler's kernel replay
+// (an injection library is attached: ncu sets NV_NSIGHT_INJECTION_*) the cluster
+// kernels fail as cooperative launches (LaunchFailed), and each launch runs
+// alone on an idle device anyway, so the attribute is dropped there
+// (CMT_COOP=0/1 overrides).  A launch that is ever not co-resident cannot hang:
+// the flag waits are bounded (lstm_common.cuh SpinGuard) and fail the step.
+static int coop_default() {
+  if (const char* v = getenv("CMT_COOP")) return atoi(v) != 0;
+  const bool profiler = getenv("CUDA_INJECTION64_PATH") || getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") ||
+                        getenv("NV_TPS_LAUNCH_TOKEN");
+  return profiler ? 0 : 1;
+}
+static int g_coop = coop_default();
 static int g_grid_cap = 0;  // > 0: persistent GEMMs use at most this many CTAs (work beside a running scan)
 constexpr int FLAG_STRIDE = 128;  // step counters per scan (per-k-block readiness flags)
 
@@ -312,6 +323,7 @@ struct StepOut {  // device -> host step result
   double scal[2];  // sumsq, norm
   int status;
   int pad;
+  int flag4[8];  // data parallel: the status word spread one flag per int (combined with ncclMax)
 };
 
 class Engine {
@@ -324,16 +336,6 @@ class Engine {
   // side stream for independent work of the two scans of a level (their input
   // projections / weight-gradient GEMMs overlap and pack each other's waves)
   cudaStream_t st2 = nullptr;
-  // background stream for the BPTT weight gradients (bg_dw): launched after a
-  // scan, grid-capped to the SMs the next scan leaves idle
-  cudaStream_t stb = nullptr;
-  cudaEvent_t ev_bg[32] = {};
-  int n_ev_bg = 0;
-  bool on_bg = false;
-  // option, off by default: measured 10.42 vs 9.91 ms/step at c3 -- a level's weight
-  // grads need ~2.5x the SM-time that the 20 idle SMs offer during the next scan,
-  // so most of the work ends up after the last scan on 20 SMs
-  int bg_dw = 0;
   // data parallel: gradient buckets are all-reduced on stc as soon as the
   // backward has produced them; the clip waits for stc
   cudaStream_t stc = nullptr;
@@ -376,11 +378,9 @@ class Engine {
   int *src_ids_d, *tgt_in_d, *tgt_out_d;
   float *src_mask_d, *tgt_mask_d;
   void *Xs, *Xt, *top, *u_att, *cst_att, *hod, *Y, *dhpre, *du_att, *dU, *dU2;
-  std::vector<void*> dUl;  // bg_dw: one dU buffer per layer (its weight grads run after the next scan started)
   float* cepart = nullptr;  // per-CTA dY column sums of the fused CE kernel
   float2* cerow = nullptr;  // per-token (lse * log2e, mask / ntok) between the two CE passes
   float* colpart2 = nullptr;  // column-sum scratch of the side stream
-  float* colpart3 = nullptr;  // column-sum scratch of the background stream
   float* dho32 = nullptr;   // fp32 split-K scratch of dH_o (bf16 mode)
   float *att_part = nullptr, *att_dsc = nullptr;  // split attention: score slices, d scores
   int att_split = 2;  // option: 2 tiled split attention (S,T <= 128), 1 split (<= 64), 0 per-sentence
@@ -401,20 +401,56 @@ class Engine {
   int nseg_pos[2] = {0, 0};
   double* normpart;
   unsigned* flags;
+  // readiness-flag regions: one per recurrent launch of a step (forward scan of
+  // layer l: region l; its BPTT scan: region nlayers + l), sized by the layer
+  // count so no two scans of a step ever share counters
+  // ParamBlock.learnable (graph.py:20-31): frozen blocks are left out of the
+  // global norm and the update (training.py:128-139).  The dense grads enter
+  // the norm and the update as segments; in a gate-interleaved LSTM region
+  // element i belongs to gate i & 3, so a segment carries a 4-bit gate mask.
+  struct GradSeg { size_t off, n; int lanes; };
+  std::vector<char> learnable;
+  std::vector<GradSeg> segs;
+  bool table_learn[2] = {true, true};
+  void set_learnable(int idx, bool v) {
+    if (idx < 0 || idx >= (int)blocks.size()) throw Error(CMT_ERR_SHAPE, "block index out of range");
+    learnable[idx] = v ? 1 : 0;
+    rebuild_segs();
+  }
+  void rebuild_segs() {
+    segs.clear();
+    std::vector<int> wm(layers.size(), 0), bm(layers.size(), 0);
+    bool all = true;
+    for (size_t i = 0; i < blocks.size(); ++i) {
+      const BlockInfo& b = blocks[i];
+      const bool on = learnable[i] != 0;
+      if (b.kind == BK_EMB) { table_learn[b.table] = on; continue; }
+      all = all && on;
+      if (!on) continue;
+      if (b.kind == BK_LSTM_W) wm[b.layer] |= 1 << b.gate;
+      else if (b.kind == BK_LSTM_B) bm[b.layer] |= 1 << b.gate;
+      else segs.push_back({b.off, (size_t)(b.rows * b.cols), 15});
+    }
+    if (n_tables == 1) table_learn[1] = table_learn[0];
+    if (all) {  // the common case: one segment over the whole arena (alignment gaps are zero)
+      segs.assign(1, GradSeg{0, dense_n, 15});
+      return;
+    }
+    for (size_t l = 0; l < layers.size(); ++l) {
+      if (wm[l]) segs.push_back({layers[l].w_off, (size_t)(layers[l].din + H) * 4 * H, wm[l]});
+      if (bm[l]) segs.push_back({layers[l].b_off, (size_t)4 * H, bm[l]});
+    }
+  }
+  size_t flag_words() const { return 2 * layers.size() * FLAG_STRIDE; }
+  unsigned* fwd_flags(int l) const { return flags + (size_t)l * FLAG_STRIDE; }
+  unsigned* bwd_flags(int l) const { return flags + (layers.size() + l) * FLAG_STRIDE; }
   int persistent = 1;  // option: persistent recurrent kernels in bf16 mode
-  int clustered = 1;   // option: cluster K-split variant of the persistent kernels (backward)
-  int clustered_fwd = 0;  // option: cluster K-split forward (slower than the plain persistent one at c3)
   int cg2 = 1;         // option: CTA-pair (cta_group::2) tiles for the large GEMMs
   int dual = 1;        // option: run independent scans of the layer graph two at a time
   int fwd_tm = 1;      // option: forward scans with W_h split over smem + TMEM (lstm_tm.cuh)
   int early_dec1 = 1;  // option: dec.l1's input projection runs beside the enc.l1 scans on the idle SMs
-  // option: BPTT scans with W_h split over smem + TMEM (lstm_tm_bwd.cuh; 1: paired scans, 2: also single).
-  // Off by default: at c3 it runs 12.3 us/step paired vs 11.5 for lstm_bwd_multi<128>
-  // (halving the dU stream does not pay for the slower MMA drain; profiles/r01/s3/trace_bwd.txt)
-  int bwd_tm = 0;
-  int use_jump = 1;    // option: table-driven PCG64 jump-ahead dropout kernel
-  int ce2 = 2;         // option: fused CE + bias-grad column sums: 2 two-pass (stats, gradient), 1 persistent one-pass
-  bool use_ce2() const { return bf && ce2 && V % 8 == 0 && (ce2 == 2 || V <= CE2_MAXV); }  // two-pass: any V
+  int ce2 = 2;         // option: fused two-pass CE + bias-grad column sums (0: per-row kernel + column sums)
+  bool use_ce2() const { return bf && ce2 && V % 8 == 0; }
   // data parallel (NCCL): dense all-reduce of grads, loss and status
   void* comm = nullptr;
   int rank = 0, world = 1;
@@ -456,11 +492,11 @@ class Engine {
       allreduce_bucket(dg + off_wo, dense_n - off_wo);  // out.w, out.b
     }
   }
-  void allreduce_bucket(void* buf, size_t n, int dtype = NCCL_FLOAT32) {
+  void allreduce_bucket(void* buf, size_t n, int dtype = NCCL_FLOAT32, int op = NCCL_SUM) {
     const int slot = n_ev_ar < 63 ? n_ev_ar++ : 63;  // events are reusable once waited on
     CMT_CUDA(cudaEventRecord(ev_ar[slot], st));
     CMT_CUDA(cudaStreamWaitEvent(stc, ev_ar[slot], 0));
-    nccl_check(g_nccl.all_reduce(buf, buf, n, dtype, NCCL_SUM, comm, stc), "ncclAllReduce");
+    nccl_check(g_nccl.all_reduce(buf, buf, n, dtype, op, comm, stc), "ncclAllReduce");
   }
   void allreduce_join() {
     if (!n_ev_ar) return;
@@ -471,12 +507,12 @@ class Engine {
   // Every collective of a step is issued on ONE stream (stc while buckets are
   // in flight, else the engine stream), so all ranks execute the shared
   // communicator's operations in the same order.
-  void allreduce(void* buf, size_t n, int dtype) {
+  void allreduce(void* buf, size_t n, int dtype, int op = NCCL_SUM) {
     if (ar_buckets) {
-      allreduce_bucket(buf, n, dtype);
+      allreduce_bucket(buf, n, dtype, op);
       return;
     }
-    nccl_check(g_nccl.all_reduce(buf, buf, n, dtype, NCCL_SUM, comm, st), "ncclAllReduce");
+    nccl_check(g_nccl.all_reduce(buf, buf, n, dtype, op, comm, st), "ncclAllReduce");
   }
   int trace_layer = -1;  // debug: record per-step phase timestamps of this layer's forward scan
   unsigned long long* trace_d = nullptr;
@@ -508,19 +544,19 @@ class Engine {
     asz = bf ? 2 : 4;
     CMT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     CMT_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
-    CMT_CUDA(cudaStreamCreateWithFlags(&stb, cudaStreamNonBlocking));
-    for (auto& e : ev_bg) CMT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CMT_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     CMT_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     for (auto& e : pin_ev) CMT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : ev) CMT_CUDA(cudaEventCreate(&e));
     build_registry();
+    learnable.assign(blocks.size(), 1);
+    rebuild_segs();
     alloc_params();
     out_h = (StepOut*)pin_out.get(sizeof(StepOut));
   }
   ~Engine() {
     cudaStreamSynchronize(st);
-    cudaFree(dw); cudaFree(dg); cudaFree(dsh);
+    cudaFree(dw); cudaFree(dg); cudaFree(dsh); cudaFree(gate_stage_d);
     for (int i = 0; i < 2; ++i) {
       if (i == 0 || !cfg.shared_embeddings) { cudaFree(emb_w[i]); cudaFree(emb_sh[i]); }
     }
@@ -530,7 +566,7 @@ class Engine {
       for (int t = 0; t < n_tables; ++t)
         if (sn.emb[t]) cudaFree(sn.emb[t]);
     }
-    dec_free();
+    beam_free();
     if (jump_d) cudaFree(jump_d);
     for (int t = 0; t < 2; ++t) if (demb[t]) cudaFree(demb[t]);
     if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
@@ -541,8 +577,6 @@ class Engine {
     for (auto& e : ev) cudaEventDestroy(e);
     cudaStreamDestroy(st);
     cudaStreamDestroy(st2);
-    cudaStreamDestroy(stb);
-    for (auto& e : ev_bg) cudaEventDestroy(e);
     cudaEventDestroy(ev_fork);
     cudaEventDestroy(ev_join);
     for (auto& e : pin_ev) cudaEventDestroy(e);
@@ -632,24 +666,27 @@ class Engine {
       if (bf) refresh_shadow(dw + b.off, dsh + b.off, (size_t)rows * cols);
       return;
     }
+    // LSTM gate block: H2D of exactly this block, interleaved on the device
     const Layer& ly = layers[b.layer];
-    size_t n4 = (size_t)4 * H;
-    if (b.kind == BK_LSTM_W) {
-      // gather the current interleaved matrix, patch gate q, write back
-      size_t rowsW = ly.din + H;
-      std::vector<float> tmp(rowsW * n4);
-      copy_sync(tmp.data(), dw + ly.w_off, tmp.size() * 4, cudaMemcpyDeviceToHost);
-      for (size_t r = 0; r < rowsW; ++r)
-        for (int j = 0; j < H; ++j) tmp[r * n4 + 4 * j + b.gate] = h[r * H + j];
-      copy_sync(dw + ly.w_off, tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice);
-      if (bf) refresh_shadow(dw + ly.w_off, dsh + ly.w_off, tmp.size());
-    } else {
-      std::vector<float> tmp(n4);
-      copy_sync(tmp.data(), dw + ly.b_off, n4 * 4, cudaMemcpyDeviceToHost);
-      for (int j = 0; j < H; ++j) tmp[4 * j + b.gate] = h[j];
-      copy_sync(dw + ly.b_off, tmp.data(), n4 * 4, cudaMemcpyHostToDevice);
-      if (bf) refresh_shadow(dw + ly.b_off, dsh + ly.b_off, n4);
+    const size_t n = (size_t)rows * cols;
+    float* stage_d = gate_stage(n);
+    copy_sync(stage_d, h, n * 4, cudaMemcpyHostToDevice);
+    const size_t off = b.kind == BK_LSTM_W ? ly.w_off : ly.b_off;
+    const long long grows = b.kind == BK_LSTM_W ? rows : 1;  // a bias is one row of H
+    gate_copy_kernel<<<grid_for((long long)n), 256, 0, st>>>(dw + off, stage_d, grows, H, b.gate, 1);
+    CMT_LAUNCHED(); tl_mark(st, "gate_copy_kernel");
+    if (bf) refresh_shadow(dw + off, dsh + off, (size_t)grows * 4 * H);
+    else CMT_CUDA(cudaStreamSynchronize(st));
+  }
+  float* gate_stage_d = nullptr;  // staging of one LSTM gate block for upload / download
+  size_t gate_stage_n = 0;
+  float* gate_stage(size_t n) {
+    if (n > gate_stage_n) {
+      if (gate_stage_d) CMT_CUDA(cudaFree(gate_stage_d));
+      CMT_CUDA(cudaMalloc(&gate_stage_d, n * 4));
+      gate_stage_n = n;
     }
+    return gate_stage_d;
   }
   void refresh_shadow(const float* s, bf16* d, size_t n) {
     to_bf16_kernel<<<std::min<long long>(4096, ceil_div(n, 256)), 256, 0, st>>>(s, d, (long long)n);
@@ -682,19 +719,16 @@ class Engine {
       copy_sync(h, base + b.off, (size_t)rows * cols * 4, cudaMemcpyDeviceToHost);
       return;
     }
+    // LSTM gate block: de-interleaved on the device, D2H of exactly this block
     const Layer& ly = layers[b.layer];
-    size_t n4 = (size_t)4 * H;
-    if (b.kind == BK_LSTM_W) {
-      size_t rowsW = ly.din + H;
-      std::vector<float> tmp(rowsW * n4);
-      copy_sync(tmp.data(), base + ly.w_off, tmp.size() * 4, cudaMemcpyDeviceToHost);
-      for (size_t r = 0; r < rowsW; ++r)
-        for (int j = 0; j < H; ++j) h[r * H + j] = tmp[r * n4 + 4 * j + b.gate];
-    } else {
-      std::vector<float> tmp(n4);
-      copy_sync(tmp.data(), base + ly.b_off, n4 * 4, cudaMemcpyDeviceToHost);
-      for (int j = 0; j < H; ++j) h[j] = tmp[4 * j + b.gate];
-    }
+    const size_t n = (size_t)rows * cols;
+    float* stage_d = gate_stage(n);
+    const size_t off = b.kind == BK_LSTM_W ? ly.w_off : ly.b_off;
+    const long long grows = b.kind == BK_LSTM_W ? rows : 1;  // a bias is one row of H
+    gate_copy_kernel<<<grid_for((long long)n), 256, 0, st>>>(const_cast<float*>(base) + off, stage_d, grows, H,
+                                                            b.gate, 0);
+    CMT_LAUNCHED(); tl_mark(st, "gate_copy_kernel");
+    copy_sync(h, stage_d, n * 4, cudaMemcpyDeviceToHost);
   }
 
   // ---- device-resident parameter snapshots (ModelParams.copy_data/load_data,
@@ -744,172 +778,249 @@ class Engine {
     sn = Snapshot();
   }
 
-  // ---- GPU translation: encode one sentence with the
-  // training forward in INFER mode, then decode_step for n live hypotheses
-  // (model.py:180-236, driven by decoding.py:89-184) ----
-  static constexpr int DEC_NMAX = 64;
-  float *dec_hs = nullptr, *dec_fin = nullptr, *dec_st = nullptr, *dec_z = nullptr, *dec_u = nullptr;
-  float *dec_ho = nullptr, *dec_y = nullptr, *dec_part = nullptr, *dec_topv = nullptr;
-  int *dec_ids = nullptr, *dec_par = nullptr, *dec_topi = nullptr;
-  unsigned* dec_ticket = nullptr;  // dec_gemv2 column-block tickets (self-resetting)
-  static constexpr int DEC_TICKETS = 4096;
-  int dec_S = 0, dec_Smax = 0, dec_cur = 0;
-  bool dec_ready = false, dec_par_set = false;
-  size_t dec_part_n = 0;
-  long long dec_lstride() const { return (long long)DEC_NMAX * H; }
-  float* dec_h(int buf) { return dec_st + (size_t)buf * 2 * L * dec_lstride(); }
-  float* dec_c(int buf) { return dec_h(buf) + (size_t)L * dec_lstride(); }
-  void dec_alloc(int S_) {
-    if (!dec_z) {
-      const int zc = std::max(E + H, 2 * H);
-      CMT_CUDA(cudaMalloc(&dec_fin, (size_t)2 * L * H * 4));
-      CMT_CUDA(cudaMalloc(&dec_st, (size_t)2 * 2 * L * DEC_NMAX * H * 4));
-      CMT_CUDA(cudaMalloc(&dec_z, (size_t)DEC_NMAX * zc * 4));
-      CMT_CUDA(cudaMalloc(&dec_u, (size_t)DEC_NMAX * 4 * H * 4));
-      CMT_CUDA(cudaMalloc(&dec_ho, (size_t)DEC_NMAX * H * 4));
-      CMT_CUDA(cudaMalloc(&dec_y, (size_t)DEC_NMAX * V * 4));
-      const int kmax = std::max({E + H, 2 * H, H});
-      dec_part_n = (size_t)ceil_div(kmax, dec::KCH) * DEC_NMAX * std::max(4 * H, V);
-      CMT_CUDA(cudaMalloc(&dec_part, dec_part_n * 4));
-      CMT_CUDA(cudaMalloc(&dec_topv, (size_t)DEC_NMAX * dec::MAXK * 4));
-      CMT_CUDA(cudaMalloc(&dec_topi, (size_t)DEC_NMAX * dec::MAXK * 4));
-      CMT_CUDA(cudaMalloc(&dec_ids, DEC_NMAX * 4));
-      CMT_CUDA(cudaMalloc(&dec_par, DEC_NMAX * 4));
-      CMT_CUDA(cudaMalloc(&dec_ticket, DEC_TICKETS * 4));
-      CMT_CUDA(cudaMemset(dec_ticket, 0, DEC_TICKETS * 4));
+  // ---- batched beam search on the device (decode.cuh):
+  // every live hypothesis of every sentence of a batch is a row of one decoder
+  // step (model.py:211-236); the beam bookkeeping of decoding.py:89-153 runs
+  // in beam_select_kernel.  The encoder is the training forward in INFER mode
+  // on the padded batch (padding carries state / is masked out exactly, so a
+  // sentence's states equal those of encoding it alone). ----
+  struct BeamWs {
+    int B = 0, K = 0, kk = 0, nb = 0, S = 0, Tmax = 0, rows = 0, cur = 0;
+    bool ready = false, finished = false;
+    char* mem = nullptr;
+    size_t cap = 0;
+    void* hs = nullptr;
+    float *smask, *fin_h, *fin_c, *hst[2], *cst[2], *cin, *U, *u, *Y, *topv;
+    void *zc, *ho;
+    void* z[64];
+    void** zp_d;
+    int *zld_d, *zoff_d, *topi, *ids, *par, *nactive;
+    BeamSent* sent;
+    double *live_lp, *lptab;
+    int2* bp;
+    BeamFin* fin;
+    std::vector<BeamSent> h_sent;
+    std::vector<BeamFin> h_fin;
+    std::vector<int2> h_bp;
+    std::vector<double> h_lp;
+  } bw;
+  int* bw_active_h = nullptr;  // pinned
+  void beam_free() {
+    if (bw.mem) cudaFree(bw.mem);
+    bw.mem = nullptr;
+    bw.cap = 0;
+    if (bw_active_h) cudaFreeHost(bw_active_h);
+    bw_active_h = nullptr;
+  }
+  void beam_begin(const long long* src, const float* smask, int S_, int B_, int beam, int n_best, const int* max_len,
+                  const double* lptab, int nlp) {
+    if (S_ < 1 || B_ < 1) throw Error(CMT_ERR_SHAPE, "beam search needs a (S >= 1, B >= 1) source batch");
+    if (beam < 1 || beam > bm::MAXK) throw Error(CMT_ERR_CONFIG, "beam_size must be in [1, 32]");
+    if (L > 63) throw Error(CMT_ERR_CONFIG, "beam search supports depth <= 63");
+    int Tmax = 0;
+    for (int b = 0; b < B_; ++b) {
+      if (max_len[b] < 1) throw Error(CMT_ERR_CONFIG, "max_len must be >= 1");
+      Tmax = std::max(Tmax, max_len[b]);
     }
-    if (S_ > dec_Smax) {
-      if (dec_hs) cudaFree(dec_hs);
-      CMT_CUDA(cudaMalloc(&dec_hs, (size_t)S_ * H * 4));
-      dec_Smax = S_;
-    }
-  }
-  void dec_free() {
-    for (float* p : {dec_hs, dec_fin, dec_st, dec_z, dec_u, dec_ho, dec_y, dec_part, dec_topv})
-      if (p) cudaFree(p);
-    for (int* p : {dec_ids, dec_par, dec_topi})
-      if (p) cudaFree(p);
-    if (dec_ticket) cudaFree(dec_ticket);
-  }
-  template <typename T>
-  void dec_cvt(const void* src, float* dst, long long n) {
-    copy2d_kernel<T, float><<<grid_for(n), 256, 0, st>>>((const T*)src, n, dst, n, 1, (int)n);
-    CMT_LAUNCHED();
-  }
-  void decode_begin(const long long* src, int S_) {
-    if (S_ < 1) throw Error(CMT_ERR_CONFIG, "cannot translate an empty source sentence");
-    std::vector<float> ones((size_t)S_, 1.f);
-    const long long eos = 3;
-    const float one = 1.f;
-    stage(src, ones.data(), S_, &eos, &one, 1, 1);
+    if (nlp < Tmax + 2) throw Error(CMT_ERR_SHAPE, "length-penalty table shorter than max_len + 2");
+    // encoder: the training forward in INFER mode on the padded batch (dummy target row)
+    std::vector<long long> eos((size_t)B_, 3);
+    std::vector<float> one((size_t)B_, 1.f);
+    stage(src, smask, S_, eos.data(), one.data(), 1, B_);
     cmt_step_args a = {};
     a.flags = CMT_FLAG_INFER;
     a.pcg_inc_lo = 1;
     cmt_step_result r = {};
-    run(a, &r);  // the training forward in INFER mode: encoder states for B = 1
+    run(a, &r);
     if (r.status != CMT_OK) throw Error(r.status, "non-finite values while encoding the source");
-    dec_alloc(S_);
+    BeamWs& w = bw;
+    w.B = B_; w.K = beam; w.kk = std::min(beam, V); w.nb = std::max(n_best, 1); w.S = S_; w.Tmax = Tmax;
+    w.rows = B_ * beam; w.cur = 0; w.finished = false;
+    const long long rows = w.rows, SB = (long long)S_ * B_;
+    const int zc = std::max(E, H) + H;
+    // carve one allocation
+    size_t need = 0;
+    auto sz = [&](size_t bytes) { size_t o = need; need += (bytes + 255) & ~(size_t)255; return o; };
+    const size_t o_hs = sz(SB * H * asz), o_sm = sz(SB * 4), o_fh = sz((size_t)L * B_ * H * 4),
+                 o_fc = sz((size_t)L * B_ * H * 4);
+    size_t o_h[2], o_c[2];
+    for (int q = 0; q < 2; ++q) { o_h[q] = sz((size_t)L * rows * H * 4); o_c[q] = sz((size_t)L * rows * H * 4); }
+    const size_t o_cin = sz((size_t)L * rows * H * 4), o_U = sz((size_t)rows * 4 * H * 4), o_u = sz((size_t)rows * H * 4),
+                 o_Y = sz((size_t)rows * V * 4), o_tv = sz((size_t)rows * w.kk * 4), o_ti = sz((size_t)rows * w.kk * 4),
+                 o_zc = sz((size_t)rows * 2 * H * asz), o_ho = sz((size_t)rows * H * asz);
+    size_t o_z[64];
+    for (int k = 0; k < L; ++k) o_z[k] = sz((size_t)rows * zc * asz);
+    const size_t o_zp = sz(64 * sizeof(void*)), o_zld = sz(64 * 4), o_zoff = sz(64 * 4), o_ids = sz(rows * 4),
+                 o_par = sz(rows * 4), o_na = sz(4), o_sent = sz((size_t)B_ * sizeof(BeamSent)),
+                 o_llp = sz((size_t)rows * 8), o_lpt = sz((size_t)nlp * 8),
+                 o_bp = sz((size_t)B_ * Tmax * beam * sizeof(int2)), o_fin = sz((size_t)B_ * w.nb * sizeof(BeamFin));
+    if (need > w.cap) {
+      if (w.mem) CMT_CUDA(cudaFree(w.mem));
+      CMT_CUDA(cudaMalloc(&w.mem, need));
+      w.cap = need;
+    }
+    if (!bw_active_h) CMT_CUDA(cudaMallocHost(&bw_active_h, 4));
+    char* m0 = w.mem;
+    w.hs = m0 + o_hs; w.smask = (float*)(m0 + o_sm); w.fin_h = (float*)(m0 + o_fh); w.fin_c = (float*)(m0 + o_fc);
+    for (int q = 0; q < 2; ++q) { w.hst[q] = (float*)(m0 + o_h[q]); w.cst[q] = (float*)(m0 + o_c[q]); }
+    w.cin = (float*)(m0 + o_cin); w.U = (float*)(m0 + o_U); w.u = (float*)(m0 + o_u); w.Y = (float*)(m0 + o_Y);
+    w.topv = (float*)(m0 + o_tv); w.topi = (int*)(m0 + o_ti); w.zc = m0 + o_zc; w.ho = m0 + o_ho;
+    for (int k = 0; k < L; ++k) w.z[k] = m0 + o_z[k];
+    w.zp_d = (void**)(m0 + o_zp); w.zld_d = (int*)(m0 + o_zld); w.zoff_d = (int*)(m0 + o_zoff);
+    w.ids = (int*)(m0 + o_ids); w.par = (int*)(m0 + o_par); w.nactive = (int*)(m0 + o_na);
+    w.sent = (BeamSent*)(m0 + o_sent); w.live_lp = (double*)(m0 + o_llp); w.lptab = (double*)(m0 + o_lpt);
+    w.bp = (int2*)(m0 + o_bp); w.fin = (BeamFin*)(m0 + o_fin);
+    // encoder outputs: the top layer (rows s*B + b), the mask, the finals (model.py:207-208)
     const void* Hs = (L == 1) ? top : views(L, false).ybase;
-    if (bf) dec_cvt<bf16>(Hs, dec_hs, (long long)S_ * H);
-    else CMT_CUDA(cudaMemcpyAsync(dec_hs, Hs, (size_t)S_ * H * 4, cudaMemcpyDeviceToDevice, st));
-    for (int k = 1; k <= L; ++k) {  // init_decoder_states (model.py:207-208): l1.bwd final, then enc.lk finals
+    CMT_CUDA(cudaMemcpyAsync(w.hs, Hs, SB * H * asz, cudaMemcpyDeviceToDevice, st));
+    CMT_CUDA(cudaMemcpyAsync(w.smask, src_mask_d, SB * 4, cudaMemcpyDeviceToDevice, st));
+    const long long BH = (long long)B_ * H;
+    for (int k = 1; k <= L; ++k) {  // l1.bwd's final sits in slot 0, deep layers' in slot S
       const int el = (k == 1) ? 1 : k;
-      const size_t slot = (k == 1) ? 0 : (size_t)S_;  // B = 1
-      const void* hsrc = (const char*)lw[el].yext + slot * H * asz;
-      if (bf) dec_cvt<bf16>(hsrc, dec_fin + (size_t)(k - 1) * H, H);
-      else CMT_CUDA(cudaMemcpyAsync(dec_fin + (size_t)(k - 1) * H, hsrc, H * 4, cudaMemcpyDeviceToDevice, st));
-      CMT_CUDA(cudaMemcpyAsync(dec_fin + (size_t)(L + k - 1) * H, lw[el].cext + slot * H, H * 4,
-                               cudaMemcpyDeviceToDevice, st));
+      const size_t slot = (k == 1) ? 0 : (size_t)S_;
+      const void* hsrc = (const char*)lw[el].yext + slot * BH * asz;
+      if (bf) copy2d_kernel<bf16, float><<<grid_for(BH), 256, 0, st>>>((const bf16*)hsrc, BH, w.fin_h + (k - 1) * BH, BH, 1, (int)BH);
+      else copy2d_kernel<float, float><<<grid_for(BH), 256, 0, st>>>((const float*)hsrc, BH, w.fin_h + (k - 1) * BH, BH, 1, (int)BH);
+      CMT_LAUNCHED(); tl_mark(st, "copy2d_kernel");
+      CMT_CUDA(cudaMemcpyAsync(w.fin_c + (k - 1) * BH, lw[el].cext + slot * BH, BH * 4, cudaMemcpyDeviceToDevice, st));
     }
+    // layer inputs z_k = [x | h_prev]: x is E (k = 1) or H wide
+    std::vector<void*> zp(64, nullptr);
+    std::vector<int> zld(64, 0), zoff(64, 0);
+    for (int k = 0; k < L; ++k) {
+      const int din = layers[L + 1 + k].din;
+      zp[k] = w.z[k]; zld[k] = din + H; zoff[k] = din;
+    }
+    CMT_CUDA(cudaMemcpyAsync(w.zp_d, zp.data(), 64 * sizeof(void*), cudaMemcpyHostToDevice, st));
+    CMT_CUDA(cudaMemcpyAsync(w.zld_d, zld.data(), 64 * 4, cudaMemcpyHostToDevice, st));
+    CMT_CUDA(cudaMemcpyAsync(w.zoff_d, zoff.data(), 64 * 4, cudaMemcpyHostToDevice, st));
+    // beam state: one live hypothesis (no tokens, log-prob 0) per sentence, fed BOS
+    std::vector<BeamSent> sent((size_t)B_);
+    for (int b = 0; b < B_; ++b) {
+      BeamSent& q = sent[b];
+      q = BeamSent{};
+      q.n_live = 1; q.max_len = max_len[b]; q.trunc_slot = -1;
+      q.best_fin = -INFINITY; q.lp_cap = lptab[max_len[b]];
+    }
+    std::vector<int> ids((size_t)rows, 2), par((size_t)rows, -1);
+    std::vector<double> llp((size_t)rows, 0.0);
+    CMT_CUDA(cudaMemcpyAsync(w.sent, sent.data(), sent.size() * sizeof(BeamSent), cudaMemcpyHostToDevice, st));
+    CMT_CUDA(cudaMemcpyAsync(w.ids, ids.data(), rows * 4, cudaMemcpyHostToDevice, st));
+    CMT_CUDA(cudaMemcpyAsync(w.par, par.data(), rows * 4, cudaMemcpyHostToDevice, st));
+    CMT_CUDA(cudaMemcpyAsync(w.live_lp, llp.data(), rows * 8, cudaMemcpyHostToDevice, st));
+    CMT_CUDA(cudaMemcpyAsync(w.lptab, lptab, (size_t)nlp * 8, cudaMemcpyHostToDevice, st));
     CMT_CUDA(cudaStreamSynchronize(st));
-    dec_S = S_;
-    dec_cur = 0;
-    dec_ready = true;
+    w.ready = true;
   }
-  template <typename T>
-  void dec_gemv(const float* Z1, int ld1, int K1, const float* Z2, int ld2, int K2, int n, const T* W, long long ldw,
-                int N, const float* bias, int act, float* Y, int ldy) {
-    const int ks = ceil_div(K1 + K2, GV2_KCH);
-    if ((size_t)ks * std::min(n, dec::ROWS) * N > dec_part_n || ceil_div(N, GV2_COLS) > DEC_TICKETS)
-      throw Error(CMT_ERR_INTERNAL, "decode GEMV out of range");
-    static bool attr = false;
-    if (!attr) {
-      CMT_CUDA(cudaFuncSetAttribute(dec_gemv2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GV2_SMEM));
-      attr = true;
+  template <typename A>
+  void beam_step_t() {
+    BeamWs& w = bw;
+    const int rows = w.rows, in = w.cur, out = w.cur ^ 1;
+    const long long RH = (long long)rows * H;
+    beam_gather_kernel<A><<<dim3(rows, L), 256, 0, st>>>(w.hst[in], w.cst[in], w.fin_h, w.fin_c, w.par, rows, w.K,
+                                                          w.B, H, (A* const*)w.zp_d, w.zld_d, w.zoff_d, w.cin);
+    CMT_LAUNCHED(); tl_mark(st, "beam_gather_kernel");
+    beam_embed_kernel<A><<<rows, 128, 0, st>>>((const A*)table_v(tgt_table()), w.ids, E, (A*)w.z[0],
+                                                layers[L + 1].din + H);
+    CMT_LAUNCHED(); tl_mark(st, "beam_embed_kernel");
+    for (int k = 1; k <= L; ++k) {  // decoder layers (lstm_cell_forward, layers.py:344-363)
+      const Layer& ly = layers[L + k];
+      EpiStore e = store(w.U, 4LL * H, false);
+      e.bias = dw + ly.b_off;
+      gemm(rows, 4 * H, ly.din + H, Mat{w.z[k - 1], ly.din + H, 0}, Mat{wv(ly.w_off), 4LL * H, 1}, e);
+      A* xn = (k < L) ? (A*)w.z[k] : (A*)w.zc + H;  // next layer's x, or h_top into [ctx | h_top]
+      const int ldx = (k < L) ? layers[L + k + 1].din + H : 2 * H;
+      beam_cell_kernel<A><<<dim3(rows, ceil_div(H, 256)), 256, 0, st>>>(w.U, w.cin + (k - 1) * RH, H,
+                                                                         w.hst[out] + (k - 1) * RH,
+                                                                         w.cst[out] + (k - 1) * RH, xn, ldx);
+      CMT_LAUNCHED(); tl_mark(st, "beam_cell_kernel");
     }
-    for (int r0 = 0; r0 < n; r0 += dec::ROWS) {  // 16 rows per pass (beam sizes up to 16 read the weights once)
-      const int nr = std::min(dec::ROWS, n - r0);
-      dec_gemv2<T><<<dim3(ceil_div(N, GV2_COLS), ks), GV2_THREADS, GV2_SMEM, st>>>(
-          Z1 + (size_t)r0 * ld1, ld1, K1, Z2 ? Z2 + (size_t)r0 * ld2 : nullptr, ld2, K2, nr, W, ldw, N, dec_part,
-          dec_ticket, bias, act, Y + (size_t)r0 * ldy, ldy);
-      CMT_LAUNCHED(); tl_mark(st, "gemv " + std::to_string(nr) + "x" + std::to_string(K1 + K2) + "x" + std::to_string(N));
+    // attention (attend_values, attention.py:235-250): u = W_a^T h_top, context, H_o = tanh(W_c^T [ctx; h_top])
+    gemm(rows, H, H, Mat{(A*)w.zc + H, 2LL * H, 0}, Mat{wv(off_wa), H, 1}, store(w.u, H, false));
+    beam_attention_kernel<A><<<rows, bm::ATT_THREADS, (size_t)w.S * 4, st>>>((const A*)w.hs, w.S, w.B, H, w.smask,
+                                                                              w.u, w.K, (A*)w.zc, 2 * H);
+    CMT_LAUNCHED(); tl_mark(st, "beam_attention_kernel");
+    {
+      EpiStore e = store(w.ho, H, true);
+      e.act = 1;
+      gemm(rows, H, 2 * H, Mat{w.zc, 2LL * H, 0}, Mat{wv(off_wc), H, 1}, e);
     }
+    {  // output layer (model.py:232-235), fp32 logits
+      EpiStore e = store(w.Y, V, false);
+      e.bias = dw + off_bo;
+      e.act = cfg.output_tanh ? 1 : 0;
+      gemm(rows, V, H, Mat{w.ho, H, 0}, Mat{wv(off_wo), V, 1}, e);
+    }
+    CMT_CUDA(cudaMemsetAsync(w.nactive, 0, 4, st));
+    beam_topk_kernel<<<rows, bm::TOPK_THREADS, 0, st>>>(w.Y, V, w.kk, w.K, w.sent, w.topv, w.topi, status_d);
+    CMT_LAUNCHED(); tl_mark(st, "beam_topk_kernel");
+    beam_select_kernel<<<w.B, 32, 0, st>>>(w.sent, w.live_lp, w.topv, w.topi, w.K, w.kk, w.K, w.bp, w.Tmax, w.fin,
+                                           w.nb, w.lptab, w.ids, w.par, w.nactive, 3);
+    CMT_LAUNCHED(); tl_mark(st, "beam_select_kernel");
+    w.cur = out;
   }
-  template <typename T>
-  void decode_step_t(int n, int k) {
-    const int zc = std::max(E + H, 2 * H);
-    const T* wts = bf ? (const T*)(const void*)dsh : (const T*)(const void*)dw;
-    const long long ls = dec_lstride();
-    const int in = dec_cur ^ 1, outb = dec_cur;  // gather the inputs into `in`, write new states to `outb`
-    // input states: the parents' new states of the previous step (or the encoder finals)
-    dim3 gg(n, L);
-    dec_gather_states<<<gg, 256, 0, st>>>(dec_h(dec_cur), dec_c(dec_cur), dec_fin, dec_fin + (size_t)L * H,
-                                          dec_par_set ? dec_par : nullptr, n, H, ls, dec_h(in), dec_c(in));
-    CMT_LAUNCHED(); tl_mark(st, "dec_gather_states");
-    const T* table = bf ? (const T*)(const void*)emb_sh[tgt_table()] : (const T*)(const void*)emb_w[tgt_table()];
-    dec_embed<T><<<n, 256, 0, st>>>(table, dec_ids, E, dec_z, zc);
-    CMT_LAUNCHED(); tl_mark(st, "dec_embed");
-    for (int k1 = 1; k1 <= L; ++k1) {  // decoder layers (lstm_cell_forward, layers.py:344-363)
-      const Layer& ly = layers[L + k1];
-      const int din = ly.din;
-      // z = [x; h_prev]: x is the embedding (layer 1) or the layer below's new h
-      const float* xin = (k1 == 1) ? dec_z : dec_h(outb) + (k1 - 2) * ls;
-      dec_gemv<T>(xin, k1 == 1 ? zc : H, din, dec_h(in) + (k1 - 1) * ls, H, H, n, wts + ly.w_off, 4LL * H, 4 * H,
-                  dw + ly.b_off, 0, dec_u, 4 * H);
-      dec_lstm_cell<<<dim3(n, ceil_div(H, 256)), 256, 0, st>>>(dec_u, dec_c(in) + (k1 - 1) * ls, H,
-                                                               dec_h(outb) + (k1 - 1) * ls, dec_c(outb) + (k1 - 1) * ls,
-                                                               nullptr, 0);
-      CMT_LAUNCHED(); tl_mark(st, "dec_lstm_cell");
-    }
-    const float* x = dec_h(outb) + (L - 1) * ls;  // top decoder h [n][H]
-    // attention (attend_values): u = W_a^T x; context; H_o = tanh(W_c^T [ctx; x])
-    dec_gemv<T>(x, H, H, nullptr, 0, 0, n, wts + off_wa, H, H, nullptr, 0, dec_u, H);
-    dec_attention<<<n, 256, (size_t)dec_S * 4, st>>>(dec_hs, dec_S, H, dec_u, dec_z, zc);
-    CMT_LAUNCHED(); tl_mark(st, "dec_attention");
-    dec_gemv<T>(dec_z, zc, H, x, H, H, n, wts + off_wc, H, H, nullptr, 1, dec_ho, H);
-    // output layer (model.py:232-235), log-softmax and the k best entries per row
-    dec_gemv<T>(dec_ho, H, H, nullptr, 0, 0, n, wts + off_wo, V, V, dw + off_bo, cfg.output_tanh ? 1 : 0, dec_y, V);
-    dec_logsoftmax_topk<<<n, dec::TOPK_THREADS, 0, st>>>(dec_y, V, k, dec_topv, dec_topi, status_d);
-    CMT_LAUNCHED(); tl_mark(st, "dec_topk");
-    dec_cur = outb;
-  }
-  void decode_step(int n, const long long* prev, const int* parent, int k, float* top_val, int* top_tok) {
-    if (!dec_ready) throw Error(CMT_ERR_CONFIG, "decode_step before decode_begin");
-    if (n < 1 || n > DEC_NMAX) throw Error(CMT_ERR_SHAPE, "decode_step: 1 <= n <= 64 hypotheses");
-    if (k < 1 || k > dec::MAXK || k > V) throw Error(CMT_ERR_SHAPE, "decode_step: 1 <= k <= min(32, V)");
-    std::vector<int> ids(n), par(n);
-    for (int i = 0; i < n; ++i) {
-      if (prev[i] < 0 || prev[i] >= V)
-        throw Error(CMT_ERR_CONFIG, "token id " + std::to_string(prev[i]) + " outside vocabulary of size " +
-                                        std::to_string(V));
-      ids[i] = (int)prev[i];
-      if (parent) {
-        if (parent[i] < 0 || parent[i] >= DEC_NMAX) throw Error(CMT_ERR_SHAPE, "decode_step: bad parent index");
-        par[i] = parent[i];
-      }
-    }
-    CMT_CUDA(cudaMemcpyAsync(dec_ids, ids.data(), n * 4, cudaMemcpyHostToDevice, st));
-    if (parent) CMT_CUDA(cudaMemcpyAsync(dec_par, par.data(), n * 4, cudaMemcpyHostToDevice, st));
-    dec_par_set = parent != nullptr;
+  int beam_step(int max_steps) {
+    if (!bw.ready) throw Error(CMT_ERR_CONFIG, "beam_step before beam_begin");
+    int active = bw.finished ? 0 : 1;
     CMT_CUDA(cudaMemsetAsync(status_d, 0, 4, st));
-    if (bf) decode_step_t<bf16>(n, k);
-    else decode_step_t<float>(n, k);
-    CMT_CUDA(cudaMemcpyAsync(top_val, dec_topv, (size_t)n * k * 4, cudaMemcpyDeviceToHost, st));
-    CMT_CUDA(cudaMemcpyAsync(top_tok, dec_topi, (size_t)n * k * 4, cudaMemcpyDeviceToHost, st));
-    int stt = 0;
-    CMT_CUDA(cudaMemcpyAsync(&stt, status_d, 4, cudaMemcpyDeviceToHost, st));
-    CMT_CUDA(cudaStreamSynchronize(st));
-    if (stt & ST_LOGITS) throw Error(CMT_ERR_NUM_LOGITS, "log_softmax_columns received non-finite input");
+    for (int i = 0; i < max_steps && active; ++i) {
+      if (bf) beam_step_t<bf16>();
+      else beam_step_t<float>();
+      CMT_CUDA(cudaMemcpyAsync(bw_active_h, bw.nactive, 4, cudaMemcpyDeviceToHost, st));
+      CMT_CUDA(cudaStreamSynchronize(st));
+      active = *bw_active_h;
+      int stt = 0;
+      CMT_CUDA(cudaMemcpy(&stt, status_d, 4, cudaMemcpyDeviceToHost));
+      if (stt & ST_LOGITS) throw Error(CMT_ERR_NUM_LOGITS, "log_softmax_columns received non-finite input");
+    }
+    if (!active && !bw.finished) {  // read the search results back once
+      BeamWs& w = bw;
+      w.h_sent.resize(w.B);
+      w.h_fin.resize((size_t)w.B * w.nb);
+      w.h_bp.resize((size_t)w.B * w.Tmax * w.K);
+      w.h_lp.resize((size_t)w.rows);
+      copy_sync(w.h_sent.data(), w.sent, w.h_sent.size() * sizeof(BeamSent), cudaMemcpyDeviceToHost);
+      copy_sync(w.h_fin.data(), w.fin, w.h_fin.size() * sizeof(BeamFin), cudaMemcpyDeviceToHost);
+      copy_sync(w.h_bp.data(), w.bp, w.h_bp.size() * sizeof(int2), cudaMemcpyDeviceToHost);
+      copy_sync(w.h_lp.data(), w.live_lp, w.h_lp.size() * 8, cudaMemcpyDeviceToHost);
+      w.finished = true;
+    }
+    return active;
+  }
+  // tokens of live slot m after step t (back-pointers, decoding.py:114 child.tokens)
+  int beam_path(int b, int t, int m, int* tokens, int cap) {
+    const BeamWs& w = bw;
+    const int n = t + 1;
+    if (n > cap) throw Error(CMT_ERR_SHAPE, "token buffer too small");
+    for (int q = t; q >= 0; --q) {
+      const int2 e = w.h_bp[((size_t)b * w.Tmax + q) * w.K + m];
+      tokens[q] = e.y;
+      m = e.x;
+    }
+    return n;
+  }
+  // result `rank` of sentence b: finished hypotheses best first (score desc,
+  // arrival asc), tokens without the EOS; or the truncation fallback
+  int beam_result(int b, int rank, int* tokens, int cap, int* n_tok, double* score, double* logp, int* trunc) {
+    const BeamWs& w = bw;
+    if (!w.finished) throw Error(CMT_ERR_CONFIG, "beam search still running");
+    if (b < 0 || b >= w.B) throw Error(CMT_ERR_SHAPE, "sentence index out of range");
+    const BeamSent& q = w.h_sent[b];
+    const int count = q.nf > 0 ? std::min(q.nf, w.nb) : 1;
+    if (rank < 0 || rank >= count) throw Error(CMT_ERR_SHAPE, "result rank out of range");
+    if (q.nf > 0) {
+      const BeamFin& f = w.h_fin[(size_t)b * w.nb + rank];
+      *n_tok = f.t > 0 ? beam_path(b, f.t - 1, f.parent, tokens, cap) : 0;
+      *score = f.score;
+      *logp = f.logp;
+      *trunc = 0;
+    } else {
+      *n_tok = q.t > 0 ? beam_path(b, q.t - 1, q.trunc_slot, tokens, cap) : 0;
+      *logp = w.h_lp[(size_t)b * w.K + q.trunc_slot];
+      *score = NAN;  // log_prob / lp(max(len, 1)): computed by the caller (decoding.py:150-153)
+      *trunc = 1;
+    }
+    return count;
   }
 
   // ---- workspace carving for (S, T, B) ----
@@ -947,10 +1058,6 @@ class Engine {
     ux3 = carve<float>(cur, NT * 4 * H * 4);  // dec.l1 input projection, computed early (see run())
     dU = carve<char>(cur, Nmax * 4 * H * asz);
     dU2 = carve<char>(cur, Nmax * 4 * H * asz);
-    dUl.assign(nl, nullptr);
-    if (bg_dw)
-      for (int l = 0; l < nl; ++l) dUl[l] = carve<char>(cur, ((l <= L) ? NS : NT) * 4 * H * asz);
-    colpart3 = carve<float>(cur, 64 * std::max<long long>(V, 4LL * H) * 4);
     drop_enc.assign(L + 1, nullptr); keep_enc.assign(L + 1, nullptr);
     drop_dec.assign(L + 1, nullptr); keep_dec.assign(L + 1, nullptr);
     for (int k = 2; k <= L; ++k) {
@@ -993,8 +1100,8 @@ class Engine {
       uniq_d[t] = carve<int>(cur, (NS + NT) * 4);
       gcomp[t] = carve<float>(cur, (NS + NT) * E * 4);
     }
-    normpart = carve<double>(cur, 3 * NORM_BLOCKS * 8);
-    flags = carve<unsigned>(cur, 64 * FLAG_STRIDE * 4);
+    normpart = carve<double>(cur, (2 * layers.size() + 8) * NORM_BLOCKS * 8);
+    flags = carve<unsigned>(cur, flag_words() * 4);
     scal_d = carve<StepScalars>(cur, sizeof(StepScalars));
     out_d = carve<StepOut>(cur, sizeof(StepOut));
     s32_d = carve<float>(cur, 4);
@@ -1193,73 +1300,21 @@ class Engine {
     jump_inc[0] = pcg.inc_hi; jump_inc[1] = pcg.inc_lo;
     jump_ok = true;
   }
+  // dropout site (layers.py:265-296): numpy-exact PCG64 draws by jump-ahead;
+  // x2 (optional) is added to x first (the bidirectional sum feeding enc.l2)
   template <typename TI, typename TO>
   void launch_dropout(const void* x, void* y, uint8_t* keep, int N, unsigned long long base, const Pcg& pcg,
                       const void* x2 = nullptr) {
-    if (use_jump == 1 || x2) {
-      ensure_jump(pcg);
-      dim3 blk(32, 8);
-      dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, DROP4_DPT), 8));
-      float scale = 1.0f / (float)(1.0 - cfg.dropout);
-      dropout_fwd_kernel4<TI, TO><<<grid, blk, 0, st>>>((const TI*)x, (TO*)y, keep, N, H, pcg, jump_d, base,
-                                                        dropout_threshold(cfg.dropout), scale, (const TI*)x2);
-      CMT_LAUNCHED(); tl_mark(st, "dropout_fwd_kernel4");
-      return;
-    }
-    if (use_jump) {
-      ensure_jump(pcg);
-      dim3 blk(32, 8);
-      dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, DROP_DPT), 8));
-      float scale = 1.0f / (float)(1.0 - cfg.dropout);
-      dropout_fwd_kernel3<TI, TO><<<grid, blk, 0, st>>>((const TI*)x, (TO*)y, keep, N, H, pcg, jump_d, base,
-                                                        dropout_threshold(cfg.dropout), scale);
-      CMT_LAUNCHED(); tl_mark(st, "dropout_fwd_kernel3");
-      return;
-    }
+    ensure_jump(pcg);
     dim3 blk(32, 8);
-    dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, 32), 8));
+    dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, DROP4_DPT), 8));
     float scale = 1.0f / (float)(1.0 - cfg.dropout);
-    dropout_fwd_kernel2<TI, TO><<<grid, blk, 0, st>>>((const TI*)x, (TO*)y, keep, N, H, pcg, base, cfg.dropout, scale);
-    CMT_LAUNCHED(); tl_mark(st, "dropout_fwd_kernel2");
+    dropout_fwd_kernel4<TI, TO><<<grid, blk, 0, st>>>((const TI*)x, (TO*)y, keep, N, H, pcg, jump_d, base,
+                                                      dropout_threshold(cfg.dropout), scale, (const TI*)x2);
+    CMT_LAUNCHED(); tl_mark(st, "dropout_fwd_kernel4");
   }
 
   // ---- persistent recurrent kernels (bf16) ----
-  bool use_persistent() const {
-    return bf && persistent && (H % (64 * pr::KBOX) == 0) && B <= 128 && (H / 16) * ceil_div(B, pr::ROWS) <= g_num_sms &&
-           pr::stages_for(H) >= 2;
-  }
-  bool use_cluster_fwd() const {
-    return use_persistent() && clustered && H % 256 == 0 && H / 8 <= g_num_sms && cl::fwd_stages(H) >= 2;
-  }
-  bool use_cluster_bwd() const {
-    return use_persistent() && clustered && H % 128 == 0 && H / 8 <= g_num_sms && cl::bwd_stages(H) >= 2;
-  }
-  template <typename P>
-  void launch_coop(void (*k)(const CUtensorMap, const CUtensorMap, P), int grid, const CUtensorMap& a,
-                   const CUtensorMap& b, const P& prm, size_t smem = 0, int cluster = 1) {
-    if (!smem) smem = pr::smem_bytes(H);
-    CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (cluster > 1) CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    cudaLaunchConfig_t c = {};
-    c.gridDim = dim3(grid);
-    c.blockDim = dim3(pr::THREADS);
-    c.dynamicSmemBytes = smem;
-    c.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    at[1].id = cudaLaunchAttributeClusterDimension;
-    at[1].val.clusterDim.x = cluster;
-    at[1].val.clusterDim.y = 1;
-    at[1].val.clusterDim.z = 1;
-    c.attrs = at;
-    c.numAttrs = cluster > 1 ? 2 : 1;
-    CMT_CUDA(cudaLaunchKernelEx(&c, k, a, b, prm));
-    CMT_LAUNCHED();
-    tl_mark(st, std::string(std::is_same<P, LstmFwdP>::value ? "lstm_fwd" : "lstm_bwd") +
-                    (cluster > 1 ? "_cluster" : "_persistent"));
-  }
-
   // ---- LSTM scans ----
   struct ScanViews {
     void* ybase;        // y[0]
@@ -1316,7 +1371,7 @@ class Engine {
     make_map(tmW, wv(ly.w_off), 4LL * H, f.din + H, 4LL * H, 64, 64);
     LstmFwdP prm;
     prm.ux = f.uxb; prm.y = (bf16*)v.ybase; prm.hprev = (const bf16*)v.hprev; prm.cst = v.cbase; prm.cprev = v.cprev;
-    prm.acts = lw[f.l].acts; prm.tcache = lw[f.l].tc; prm.mask = f.mask; prm.flag = flags + (f.l & 31) * FLAG_STRIDE;
+    prm.acts = lw[f.l].acts; prm.tcache = lw[f.l].tc; prm.mask = f.mask; prm.flag = fwd_flags(f.l); prm.status = status_d;
     prm.steps = f.steps; prm.B = B; prm.H = H; prm.din = f.din; prm.reverse = f.reverse ? 1 : 0;
     prm.hrow0 = f.reverse ? B : 0;
     prm.trace = (trace_layer == f.l) ? trace_d : nullptr;
@@ -1350,10 +1405,12 @@ class Engine {
     c.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    at[0].val.cooperative = g_coop;
     c.attrs = at;
     c.numAttrs = 1;
+    cudaEvent_t p0 = probe_begin(2);
     CMT_CUDA(cudaLaunchKernelEx(&c, k, tmap[0], tmap[1], tmap[2], tmap[3], m));
+    probe_end(2, p0);
     CMT_LAUNCHED();
     tl_mark(st, b ? "lstm_fwd_tm_pair" : "lstm_fwd_tm_single");
   }
@@ -1376,10 +1433,12 @@ class Engine {
     c.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    at[0].val.cooperative = g_coop;
     c.attrs = at;
     c.numAttrs = 1;
+    cudaEvent_t p0 = probe_begin(2);
     CMT_CUDA(cudaLaunchKernelEx(&c, k, tm[0], tm[1], tm[2], tm[3], m));
+    probe_end(2, p0);
     CMT_LAUNCHED();
     tl_mark(st, "lstm_fwd_pair");
   }
@@ -1405,10 +1464,12 @@ class Engine {
     c.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    at[0].val.cooperative = g_coop;
     c.attrs = at;
     c.numAttrs = 1;
+    cudaEvent_t p0 = probe_begin(2);
     CMT_CUDA(cudaLaunchKernelEx(&c, k, tm[0], tm[1], tm[0], tm[1], m));
+    probe_end(2, p0);
     CMT_LAUNCHED();
     tl_mark(st, "lstm_fwd_single");
   }
@@ -1417,14 +1478,11 @@ class Engine {
     // single scans: lstm_fwd_multi<64> (128 CTAs, 6.4 us/step at c3) beats the
     // TMEM-split kernel with 32-row slices (6.9 us/step), but when the batch
     // needs 128-row multi slices (B > 128) the TMEM-split kernel with 64-row
-    // slices is faster (c5: 28.5 -> 28.2 ms/step); fwd_tm=2 forces it
-    const bool tm_single = fwd_tm == 2 ? (fwd_tm_ok<32>() || fwd_tm_ok<64>())
-                                       : (fwd_tm == 1 && single_fwd_rows() == 128 && fwd_tm_ok<64>());
-    if (tm_single) {
+    // slices is faster (c5: 28.5 -> 28.2 ms/step)
+    if (fwd_tm == 1 && single_fwd_rows() == 128 && fwd_tm_ok<64>()) {
       FwdScan f{l, X, din, steps, reverse, mask, ux};
       fwd_prep(f);
-      if (fwd_tm == 2 && fwd_tm_ok<32>()) fwd_tm_launch<32>(f, nullptr);
-      else fwd_tm_launch<64>(f, nullptr);
+      fwd_tm_launch<64>(f, nullptr);
       return;
     }
     if (const int rows = single_fwd_rows()) {
@@ -1434,41 +1492,15 @@ class Engine {
       else fwd_single<128>(f);
       return;
     }
+    // general fallback (fp32 validation mode, shapes the persistent kernels do
+    // not cover): the hoisted projection, then one GEMM per step with the cell
+    // fused in its epilogue
     const Layer& ly = layers[l];
-    long long N = (long long)steps * B;
     // hoisted input projection Ux = X W_x + b   (layers.py:354-357, K3)
     EpiStore e = store(ux, 4LL * H, false);
     e.bias = dw + ly.b_off;
-    gemm((int)N, 4 * H, din, Mat{X, din, 0}, Mat{wv(ly.w_off), 4LL * H, 1}, e);
+    gemm(steps * B, 4 * H, din, Mat{X, din, 0}, Mat{wv(ly.w_off), 4LL * H, 1}, e);
     ScanViews v = views(l, reverse);
-    if (use_cluster_fwd() && clustered_fwd) {
-      CUtensorMap tmH, tmW;
-      make_map_kblocks(&tmH, lw[l].yext, (long long)(steps + 1) * B, H, H, cl::ROWS, cl::KBOX);
-      make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 64);
-      LstmFwdP prm;
-      prm.ux = ux; prm.y = (bf16*)v.ybase; prm.hprev = (const bf16*)v.hprev; prm.cst = v.cbase; prm.cprev = v.cprev;
-      prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.mask = mask; prm.flag = flags + (l & 31) * FLAG_STRIDE;
-      prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
-      prm.hrow0 = reverse ? B : 0;
-      prm.trace = (trace_layer == l) ? trace_d : nullptr;
-      prm.stages = cl::fwd_stages(H);
-      launch_coop(lstm_fwd_cluster, cl::FWD_KS * (4 * H / cl::FWD_NG), tmH, tmW, prm, cl::fwd_smem(H), cl::FWD_KS);
-      return;
-    }
-    if (use_persistent()) {
-      CUtensorMap tmH, tmW;
-      make_map_kblocks(&tmH, lw[l].yext, (long long)(steps + 1) * B, H, H, pr::ROWS, pr::KBOX);
-      make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 64);
-      LstmFwdP prm;
-      prm.ux = ux; prm.y = (bf16*)v.ybase; prm.hprev = (const bf16*)v.hprev; prm.cst = v.cbase; prm.cprev = v.cprev;
-      prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.mask = mask; prm.flag = flags + (l & 31) * FLAG_STRIDE;
-      prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
-      prm.hrow0 = reverse ? B : 0;
-      prm.trace = (trace_layer == l) ? trace_d : nullptr;
-      prm.stages = pr::stages_for(H);
-      launch_coop(lstm_fwd_persistent, 4 * H / pr::FWD_NG * ceil_div(B, pr::ROWS), tmH, tmW, prm);
-      return;
-    }
     const void* Wh = (const char*)wv(ly.w_off) + (size_t)din * 4 * H * asz;
     for (int p = 0; p < steps; ++p) {
       int t = reverse ? steps - 1 - p : p;
@@ -1506,61 +1538,11 @@ class Engine {
            (4 * H / 64) * ((B + ROWS - 1) / ROWS) <= FLAG_STRIDE && F::ctas(H, B) <= g_num_sms &&
            F::stages(H) >= 2 && (size_t)F::stages(H) * F::STAGE >= F::xbuf_bytes();
   }
-  template <int ROWS>
-  bool bwd_tm_ok() const {
-    using F = tmb::Bwd<ROWS>;
-    const int nh = (B + ROWS - 1) / ROWS;
-    return bf && persistent && bwd_tm && F::ok(H, B) && (H / 32) * nh <= FLAG_STRIDE && F::ctas(H, B) <= g_num_sms;
-  }
-  bool dual_bwd_tm() const { return dual && bwd_tm_ok<64>() && 2 * tmb::Bwd<64>::ctas(H, B) <= g_num_sms; }
-  bool use_dual_bwd() const {
-    return dual_bwd_tm() || (bwd_multi_ok<128>() && 2 * mc::Bwd<128>::ctas(H, B) <= g_num_sms);
-  }
-  template <int ROWS>
-  void bwd_tm_launch(const BwdScan& a, const BwdScan* b) {
-    using F = tmb::Bwd<ROWS>;
-    CUtensorMap tmap[4];
-    LstmBwdMulti m;
-    auto prm = [&](const BwdScan& f, CUtensorMap* tA, CUtensorMap* tW) {
-      LstmBwdP r = bwd_params<128>(f, tA, tW);
-      const Layer& ly = layers[f.l];
-      make_map_kblocks(tA, f.dUb, (long long)f.steps * B, 4LL * H, 4LL * H, ROWS, tmb::KBOX);
-      make_map(tW, wv(ly.w_off), 4LL * H, f.din + H, 4LL * H, 64, tmb::NU);
-      r.stages = F::stages(H);
-      return r;
-    };
-    m.c[0] = prm(a, &tmap[0], &tmap[1]);
-    if (b) m.c[1] = prm(*b, &tmap[2], &tmap[3]);
-    else { m.c[1] = m.c[0]; tmap[2] = tmap[0]; tmap[3] = tmap[1]; }
-    const int g = F::ctas(H, B);
-    m.split = g;
-    auto k = lstm_bwd_tm<ROWS>;
-    const size_t smem = F::smem(H);
-    CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaLaunchConfig_t c = {};
-    c.gridDim = dim3(b ? 2 * g : g);
-    c.blockDim = dim3(tmb::THREADS);
-    c.dynamicSmemBytes = smem;
-    c.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    at[1].id = cudaLaunchAttributeClusterDimension;
-    at[1].val.clusterDim.x = tmb::KS_CL;
-    at[1].val.clusterDim.y = 1;
-    at[1].val.clusterDim.z = 1;
-    c.attrs = at;
-    c.numAttrs = 2;
-    CMT_CUDA(cudaLaunchKernelEx(&c, k, tmap[0], tmap[1], tmap[2], tmap[3], m));
-    CMT_LAUNCHED();
-    tl_mark(st, b ? "lstm_bwd_tm_pair" : "lstm_bwd_tm_single");
-  }
+  bool use_dual_bwd() const { return bwd_multi_ok<128>() && 2 * mc::Bwd<128>::ctas(H, B) <= g_num_sms; }
   // one scan over batch slices of ROWS rows (64: two halves of B<=128; 128: B<=256)
   int single_bwd_rows() const { return bwd_multi_ok<64>() ? 64 : bwd_multi_ok<128>() ? 128 : 0; }
   void bwd_single(const BwdScan& f, bool post = true) {
-    if (bwd_tm == 2 && bwd_tm_ok<32>()) bwd_tm_launch<32>(f, nullptr);
-    else if (bwd_tm == 2 && bwd_tm_ok<64>()) bwd_tm_launch<64>(f, nullptr);
-    else if (single_bwd_rows() == 64) bwd_launch<64>(f, nullptr);
+    if (single_bwd_rows() == 64) bwd_launch<64>(f, nullptr);
     else bwd_launch<128>(f, nullptr);
     if (post) bwd_post(f);
   }
@@ -1574,7 +1556,8 @@ class Engine {
     LstmBwdP prm;
     prm.dy = f.dy; prm.acts = lw[f.l].acts; prm.tcache = lw[f.l].tc; prm.cprev = v.cprev; prm.mask = f.mask;
     prm.dU = (bf16*)f.dUb; prm.dh_final = f.dh_final; prm.dc_final = f.dc_final; prm.dh0 = f.dh0; prm.dc0 = f.dc0;
-    prm.flag = flags + (32 + (f.l & 31)) * FLAG_STRIDE;
+    prm.flag = bwd_flags(f.l);
+    prm.status = status_d;
     prm.steps = f.steps; prm.B = B; prm.H = H; prm.din = f.din; prm.reverse = f.reverse ? 1 : 0;
     prm.trace = (trace_layer == 100 + f.l) ? trace_d : nullptr;
     prm.stages = mc::Bwd<ROWS>::stages(H);
@@ -1599,21 +1582,20 @@ class Engine {
     c.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    at[0].val.cooperative = g_coop;
     at[1].id = cudaLaunchAttributeClusterDimension;
     at[1].val.clusterDim.x = mc::BWD_KS;
     at[1].val.clusterDim.y = 1;
     at[1].val.clusterDim.z = 1;
     c.attrs = at;
     c.numAttrs = 2;
+    cudaEvent_t p0 = probe_begin(1);
     CMT_CUDA(cudaLaunchKernelEx(&c, k, tm[0], tm[1], tm[2], tm[3], m));
+    probe_end(1, p0);
     CMT_LAUNCHED();
     tl_mark(st, b ? "lstm_bwd_pair" : "lstm_bwd_single");
   }
-  void bwd_pair(const BwdScan& a, const BwdScan& b) {
-    if (dual_bwd_tm()) bwd_tm_launch<64>(a, &b);
-    else bwd_launch<128>(a, &b);
-  }
+  void bwd_pair(const BwdScan& a, const BwdScan& b) { bwd_launch<128>(a, &b); }
   // weight grads, bias grads and input grads of a finished BPTT scan
   void bwd_post(const BwdScan& f) {
     bwd_post_w(f);
@@ -1654,31 +1636,7 @@ class Engine {
     else CMT_CUDA(cudaMemsetAsync(dcc, 0, BH * 4, st));
     const void* WhN = (const char*)wv(ly.w_off) + (size_t)din * 4 * H * asz;  // rows din.. of [din+H][4H]
     auto time_of = [&](int p) { return reverse ? steps - 1 - p : p; };
-    if (use_cluster_bwd()) {
-      CUtensorMap tmA, tmW;
-      make_map_kblocks(&tmA, dU, N, 4LL * H, 4LL * H, cl::ROWS, cl::KBOX);
-      make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, cl::BWD_NU);
-      LstmBwdP prm;
-      prm.dy = dy; prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.cprev = v.cprev; prm.mask = mask;
-      prm.dU = (bf16*)dU; prm.dh_final = dh_final; prm.dc_final = dc_final; prm.dh0 = dh0; prm.dc0 = dc0;
-      prm.flag = flags + (32 + (l & 31)) * FLAG_STRIDE;
-      prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
-      prm.trace = (trace_layer == 100 + l) ? trace_d : nullptr;
-      prm.stages = cl::bwd_stages(H);
-      launch_coop(lstm_bwd_cluster, cl::BWD_KS * (H / cl::BWD_NU), tmA, tmW, prm, cl::bwd_smem(H), cl::BWD_KS);
-    } else if (use_persistent()) {
-      CUtensorMap tmA, tmW;
-      make_map_kblocks(&tmA, dU, N, 4LL * H, 4LL * H, pr::ROWS, pr::KBOX);
-      make_map(&tmW, wv(ly.w_off), 4LL * H, din + H, 4LL * H, 64, 16);
-      LstmBwdP prm;
-      prm.dy = dy; prm.acts = lw[l].acts; prm.tcache = lw[l].tc; prm.cprev = v.cprev; prm.mask = mask;
-      prm.dU = (bf16*)dU; prm.dh_final = dh_final; prm.dc_final = dc_final; prm.dh0 = dh0; prm.dc0 = dc0;
-      prm.flag = flags + (32 + (l & 31)) * FLAG_STRIDE;
-      prm.steps = steps; prm.B = B; prm.H = H; prm.din = din; prm.reverse = reverse ? 1 : 0;
-      prm.trace = nullptr;
-      prm.stages = pr::stages_for(H);
-      launch_coop(lstm_bwd_persistent, H / pr::BWD_NU * ceil_div(B, pr::ROWS), tmA, tmW, prm);
-    } else
+    // general fallback: one GEMM per step with the cell backward in its epilogue
     for (int p = steps - 1; p >= 0; --p) {
       int t = time_of(p);
       EpiLstmBwd f;
@@ -1693,7 +1651,7 @@ class Engine {
         gemm(B, H, 4 * H, Mat{a, 4LL * H, 0}, Mat{WhN, 4LL * H, 0}, f);
       }
     }
-    if (dh0 && !use_persistent()) {
+    if (dh0) {
       EpiInitGrad f{dh0, dc0, dhc, dcc, H};
       const void* a = (const char*)dU + (size_t)time_of(0) * B * 4 * H * asz;
       gemm(B, H, 4 * H, Mat{a, 4LL * H, 0}, Mat{WhN, 4LL * H, 0}, f);
@@ -1730,41 +1688,13 @@ class Engine {
     std::swap(st, st2);
     on_side = false;
   }
-  // issue f's launches on the background stream after the work issued so far on
-  // the engine stream, with persistent GEMM grids capped to `cap` CTAs
-  template <class F>
-  void on_bg_stream(int cap, F&& f) {
-    const int slot = n_ev_bg < 31 ? n_ev_bg++ : 31;
-    CMT_CUDA(cudaEventRecord(ev_bg[slot], st));
-    CMT_CUDA(cudaStreamWaitEvent(stb, ev_bg[slot], 0));
-    std::swap(st, stb);
-    on_bg = true;
-    g_grid_cap = cap;
-    try {
-      f();
-    } catch (...) {
-      std::swap(st, stb);
-      on_bg = false;
-      g_grid_cap = 0;
-      throw;
-    }
-    std::swap(st, stb);
-    on_bg = false;
-    g_grid_cap = 0;
-  }
-  void bg_join() {
-    if (!n_ev_bg) return;
-    CMT_CUDA(cudaEventRecord(ev_bg[0], stb));
-    CMT_CUDA(cudaStreamWaitEvent(st, ev_bg[0], 0));
-    n_ev_bg = 0;
-  }
   void join() {
     CMT_CUDA(cudaEventRecord(ev_join, st2));
     CMT_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
   }
 
   void colsum(const void* D, bool is_act, long long rows, int cols, float* out) {
-    float* colpart = on_bg ? colpart3 : on_side ? colpart2 : this->colpart;
+    float* colpart = on_side ? colpart2 : this->colpart;
     int chunks = (int)std::min<long long>(64, std::max<long long>(1, rows / 64));
     int rows_per = ceil_div(rows, chunks);
     chunks = ceil_div(rows, rows_per);
@@ -1793,13 +1723,13 @@ class Engine {
     const bool infer = (a.flags & CMT_FLAG_INFER) != 0;  // dev_entropy pass (training.py:162-182)
     const bool drop = cfg.dropout > 0.0 && !infer;        // INFER mode: dropout is the identity
     Pcg pcg{a.pcg_state_hi, a.pcg_state_lo, a.pcg_inc_hi, a.pcg_inc_lo};
-    if (drop && use_jump) ensure_jump(pcg);  // before any side-stream dropout reads the table
+    if (drop) ensure_jump(pcg);  // before any side-stream dropout reads the table
     double ntok = a.global_ntok > 0 ? a.global_ntok : ntok_local;
     float inv_ntok = ntok > 0 ? (float)(1.0 / (double)(float)ntok) : 0.f;
     CMT_CUDA(cudaMemsetAsync(out_d, 0, sizeof(StepOut), st));
     // every recurrent launch of the step owns one flag region (forward layer l:
-    // region l, BPTT: region 32 + l): one memset instead of one per launch
-    CMT_CUDA(cudaMemsetAsync(flags, 0, 64 * FLAG_STRIDE * 4, st));
+    // region l, BPTT: region nlayers + l): one memset instead of one per launch
+    CMT_CUDA(cudaMemsetAsync(flags, 0, flag_words() * 4, st));
     tl_mark(st, "<start>");
 
     // ===== forward =====
@@ -2028,22 +1958,14 @@ class Engine {
       EpiStore e = store(Y, V, true);
       e.bias = dw + off_bo;
       e.act = cfg.output_tanh ? 1 : 0;
-      cudaEvent_t e0 = nullptr, e1 = nullptr;
-      if (time_dominant) {
-        CMT_CUDA(cudaEventCreate(&e0));
-        CMT_CUDA(cudaEventCreate(&e1));
-        CMT_CUDA(cudaEventRecord(e0, st));
-      }
+      cudaEvent_t e0 = probe_begin(0);
       gemm((int)NT, V, H, Mat{hin, H, 0}, Mat{wv(off_wo), V, 1}, e);
-      if (time_dominant) {
-        CMT_CUDA(cudaEventRecord(e1, st));
-        dom_events.push_back({e0, e1});
-      }
+      probe_end(0, e0);
     }
     if (stop_after == 1) { CMT_CUDA(cudaStreamSynchronize(st)); return; }
     // fused log-softmax + smoothed CE + grad (training.py:96-120, tensor.py:146-151)
     const bool fused_ce = use_ce2() && cepart;
-    if (fused_ce && ce2 == 2) {
+    if (fused_ce) {
       ce_stats_kernel<<<(int)NT, CES_THREADS, 0, st>>>((const bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon,
                                                        inv_ntok, cfg.output_tanh, losstok, status_d, cerow);
       CMT_LAUNCHED(); tl_mark(st, "ce_stats_kernel");
@@ -2053,15 +1975,6 @@ class Engine {
                                                                                   cfg.output_tanh, cepart);
       CMT_LAUNCHED(); tl_mark(st, "ce_grad_kernel");
       colsum_final_kernel<<<ceil_div(V, 256), 256, 0, st>>>(cepart, chunks, V, dg + off_bo);
-      CMT_LAUNCHED(); tl_mark(st, "colsum_final_kernel");
-    } else if (fused_ce) {
-      const size_t smem = (size_t)V * 4;
-      CMT_CUDA(cudaFuncSetAttribute(ce_colsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      ce_colsum_kernel<<<g_num_sms, CE2_THREADS, smem, st>>>((bf16*)Y, V, (int)NT, tgt_out_d, tgt_mask_d,
-                                                              (float)a.epsilon, inv_ntok, cfg.output_tanh, losstok,
-                                                              status_d, cepart);
-      CMT_LAUNCHED(); tl_mark(st, "ce_colsum_kernel");
-      colsum_final_kernel<<<ceil_div(V, 256), 256, 0, st>>>(cepart, g_num_sms, V, dg + off_bo);
       CMT_LAUNCHED(); tl_mark(st, "colsum_final_kernel");
     } else if (bf) ce_kernel<bf16><<<(int)NT, CE_THREADS, 0, st>>>((bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon, inv_ntok,
                                                            cfg.output_tanh, losstok, status_d);
@@ -2240,40 +2153,7 @@ class Engine {
       scan_bwd(f.l, f.X, f.din, f.steps, f.reverse, f.mask, f.dy, f.dh_final, f.dc_final, f.dh0, f.dc0, f.dX,
                f.dx_beta, f.dx_keep);
     };
-    // bg_dw: a level's weight / bias grads (not needed before the update) run on
-    // the background stream beside the NEXT level's scans, capped to the SMs
-    // those leave idle; only the input grads (the next scans' dy) stay between scans
-    const bool bg = bg_dw && use_overlap() && !dUl.empty() && dUl[0] && !dual_bwd_tm() &&
-                    single_bwd_rows() == 64;
-    const int idle = g_num_sms - 2 * mc::Bwd<128>::ctas(H, B);
-    auto dub = [&](int l, void* fallback) { return bg ? dUl[l] : fallback; };
-    if (use_dual_bwd() && bg && idle >= 8) {
-      BwdScan dl = dec_scan(L, dub(2 * L, dU));
-      bwd_single(dl, false);
-      bwd_post_dx(dl);
-      on_bg_stream(idle, [&]() { bwd_post_w(dl); });
-      for (int k = L - 1; k >= 1; --k) {
-        BwdScan d = dec_scan(k, dub(L + k, dU)), e = enc_scan(k + 1, dub(k + 1, dU2));
-        bwd_pair(d, e);
-        bwd_post_dx(d);
-        bwd_post_dx(e);
-        on_bg_stream(idle, [&]() {
-          bwd_post_w(d);
-          bwd_post_w(e);
-        });
-      }
-      BwdScan b1 = l1_scan(true, dub(1, dU)), f1 = l1_scan(false, dub(0, dU2));
-      bwd_pair(b1, f1);
-      // no scan follows: the last level's weight grads run at full width
-      fork();
-      bwd_post(b1);
-      BwdScan f1w = f1;
-      f1w.dX = nullptr;
-      on_side_stream([&]() { bwd_post(f1w); });
-      join();
-      bwd_post_dx(f1);
-      bg_join();
-    } else if (use_dual_bwd()) {
+    if (use_dual_bwd()) {
       // pairs of independent scans: dL alone, then (d(k), e(k+1)) for k = L-1..1, then (e1 bwd, e1 fwd)
       single(dec_scan(L, dU));
       for (int k = L - 1; k >= 1; --k) {
@@ -2341,32 +2221,44 @@ class Engine {
         allreduce(demb[t], (size_t)V * E, NCCL_FLOAT32);
       }
       allreduce(losssum_d, 1, NCCL_FLOAT64);
-      allreduce(status_d, 1, NCCL_INT32);
+      // the status word is a set of flags: spread it one flag per int, take the
+      // max over ranks and rebuild it (a SUM of the words carries between flags)
+      status_spread_kernel<<<1, 32, 0, st>>>(status_d, out_d->flag4);
+      CMT_LAUNCHED(); tl_mark(st, "status_spread_kernel");
+      allreduce(out_d->flag4, ST_NFLAGS, NCCL_INT32, NCCL_MAX);
       allreduce_join();
+      status_gather_kernel<<<1, 32, 0, st>>>(out_d->flag4, status_d);
+      CMT_LAUNCHED(); tl_mark(st, "status_gather_kernel");
     }
     // ===== global-norm clip + SGD (training.py:123-142) =====
     int nparts = 0;
-    sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(dg, (long long)dense_n, normpart);
-    CMT_LAUNCHED(); tl_mark(st, "sumsq_partial_kernel");
-    nparts += NORM_BLOCKS;
+    for (const GradSeg& sg : segs) {
+      sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(dg + sg.off, (long long)sg.n, normpart + nparts, sg.lanes);
+      CMT_LAUNCHED(); tl_mark(st, "sumsq_partial_kernel");
+      nparts += NORM_BLOCKS;
+    }
     for (int t = 0; t < n_tables; ++t) {
-      if (!dp && nuniq[t] == 0) continue;
+      if (!table_learn[t] || (!dp && nuniq[t] == 0)) continue;
       const float* gsrc = dp ? demb[t] : gcomp[t];
       long long gn = dp ? (long long)V * E : (long long)nuniq[t] * E;
-      sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(gsrc, gn, normpart + nparts);
+      sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(gsrc, gn, normpart + nparts, 15);
       CMT_LAUNCHED(); tl_mark(st, "sumsq_partial_kernel");
       nparts += NORM_BLOCKS;
     }
     clip_scale_kernel<<<1, CLIP_THREADS, 0, st>>>(normpart, nparts, a.lr, a.clip_norm, normscal_d, s32_d, status_d);
     CMT_LAUNCHED(); tl_mark(st, "clip_scale_kernel");
     if (!(a.flags & CMT_FLAG_NO_UPDATE)) {
-      sgd_dense_kernel<<<grid_for((long long)dense_n), 256, 0, st>>>(dw, dg, bf ? dsh : nullptr, (long long)dense_n, s32_d,
-                                                                     status_d);
-      CMT_LAUNCHED(); tl_mark(st, "sgd_dense_kernel");
+      for (const GradSeg& sg : segs) {
+        sgd_dense_kernel<<<grid_for((long long)sg.n), 256, 0, st>>>(dw + sg.off, dg + sg.off,
+                                                                    bf ? dsh + sg.off : nullptr, (long long)sg.n,
+                                                                    s32_d, status_d, sg.lanes);
+        CMT_LAUNCHED(); tl_mark(st, "sgd_dense_kernel");
+      }
       for (int t = 0; t < n_tables; ++t) {
+        if (!table_learn[t]) continue;
         if (dp) {  // union of all ranks' rows: dense update (zero rows are exact no-ops)
           sgd_dense_kernel<<<grid_for((long long)V * E), 256, 0, st>>>(emb_w[t], demb[t], bf ? emb_sh[t] : nullptr,
-                                                                      (long long)V * E, s32_d, status_d);
+                                                                      (long long)V * E, s32_d, status_d, 15);
           CMT_LAUNCHED(); tl_mark(st, "sgd_dense_kernel");
           continue;
         }
@@ -2425,23 +2317,40 @@ class Engine {
   }
   unsigned long long last_draws = 0;
   double last_ntok = 1;
-  int time_dominant = 0;
+  int time_dominant = 0;  // bit c: CUDA-event probes around the launches of kernel class c
   int stop_after = 0;  // debug: 1 = after the logits GEMM, 2 = after the CE
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> dom_events;
-  // mean duration (ms) of the timed dominant-kernel launches since the last call
-  double dominant_ms(double* count) {
+  // probes (bench.py's roofline, timed inside the timed steps on the launching
+  // stream): class 0 the logits GEMM, 1 the BPTT scan launches, 2 the forward scan launches
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> probe_ev[3];
+  cudaEvent_t probe_begin(int cls) {
+    if (!((time_dominant >> cls) & 1)) return nullptr;
+    cudaEvent_t e0;
+    CMT_CUDA(cudaEventCreate(&e0));
+    CMT_CUDA(cudaEventRecord(e0, st));
+    return e0;
+  }
+  void probe_end(int cls, cudaEvent_t e0) {
+    if (!e0) return;
+    cudaEvent_t e1;
+    CMT_CUDA(cudaEventCreate(&e1));
+    CMT_CUDA(cudaEventRecord(e1, st));
+    probe_ev[cls].push_back({e0, e1});
+  }
+  // mean duration (ms) of the probed launches of class cls since the last call
+  double probe_ms(int cls, double* count) {
+    if (cls < 0 || cls > 2) throw Error(CMT_ERR_CONFIG, "probe class out of range");
     CMT_CUDA(cudaStreamSynchronize(st));
     double tot = 0;
-    for (auto& p : dom_events) {
+    for (auto& p : probe_ev[cls]) {
       float ms = 0;
       CMT_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
       tot += ms;
       cudaEventDestroy(p.first);
       cudaEventDestroy(p.second);
     }
-    *count = (double)dom_events.size();
-    double r = dom_events.empty() ? 0.0 : tot / dom_events.size();
-    dom_events.clear();
+    *count = (double)probe_ev[cls].size();
+    double r = probe_ev[cls].empty() ? 0.0 : tot / probe_ev[cls].size();
+    probe_ev[cls].clear();
     return r;
   }
 
@@ -2454,7 +2363,8 @@ class Engine {
     res->grad_norm = out_h->scal[1];
     int s = out_h->status;
     if (last_infer) s &= ~ST_LOSS;  // dev_entropy does not check the loss (training.py:174-181)
-    res->status = (s & ST_SCORES) ? CMT_ERR_NUM_SCORES
+    res->status = (s & ST_HANG)   ? CMT_ERR_INTERNAL
+                : (s & ST_SCORES) ? CMT_ERR_NUM_SCORES
                 : (s & ST_LOGITS) ? CMT_ERR_NUM_LOGITS
                 : (s & ST_LOSS)   ? CMT_ERR_NUM_LOSS
                 : (s & ST_NORM)   ? CMT_ERR_NUM_NORM
@@ -2541,13 +2451,21 @@ int cmt_snapshot_download(cmt_engine* e, int slot, int idx, float* h, long long 
     e->eng->download(idx, h, rows, cols, false, slot);
   });
 }
-int cmt_decode_begin(cmt_engine* e, const long long* src_ids, int S) {
-  return guard(e, [&] { e->eng->decode_begin(src_ids, S); });
+int cmt_beam_begin(cmt_engine* e, const long long* src_ids, const float* src_mask, int S, int B, int beam,
+                   int n_best, const int* max_len, const double* lp_table, int lp_table_len) {
+  return guard(e, [&] { e->eng->beam_begin(src_ids, src_mask, S, B, beam, n_best, max_len, lp_table, lp_table_len); });
 }
-int cmt_decode_step(cmt_engine* e, int n, const long long* prev_tokens, const int* parent, int k, float* top_logprob,
-                    int* top_token) {
-  return guard(e, [&] { e->eng->decode_step(n, prev_tokens, parent, k, top_logprob, top_token); });
+int cmt_beam_step(cmt_engine* e, int max_steps, int* n_active) {
+  return guard(e, [&] { *n_active = e->eng->beam_step(max_steps); });
 }
+int cmt_beam_result(cmt_engine* e, int b, int rank, int* tokens, int cap, int* n_tokens, double* score,
+                    double* log_prob, int* truncated, int* n_results) {
+  return guard(e, [&] { *n_results = e->eng->beam_result(b, rank, tokens, cap, n_tokens, score, log_prob, truncated); });
+}
+int cmt_set_learnable(cmt_engine* e, int idx, int learnable) {
+  return guard(e, [&]() { e->eng->set_learnable(idx, learnable != 0); });
+}
+int cmt_status_combine(const int* words, int n) { return cmt::status_combine(words, n); }
 int cmt_download_grad(cmt_engine* e, int idx, float* h, long long rows, long long cols) {
   return guard(e, [&] { e->eng->download(idx, h, rows, cols, true); });
 }
@@ -2558,7 +2476,8 @@ int cmt_stage_batch(cmt_engine* e, const long long* src, const float* sm, int S,
 int cmt_run_step(cmt_engine* e, const cmt_step_args* a, cmt_step_result* r) {
   int rc = guard(e, [&] { e->eng->run(*a, r); });
   if (rc == 0 && r && !(a->flags & CMT_FLAG_ASYNC) && r->status != 0) {
-    e->err = "numeric error in train step";
+    e->err = r->status == CMT_ERR_INTERNAL ? "recurrent scan flag wait timed out (step aborted, weights unchanged)"
+                                           : "numeric error in train step";
     return r->status;
   }
   return rc;
@@ -2571,6 +2490,7 @@ int cmt_train_step(cmt_engine* e, const long long* src, const float* sm, int S, 
 }
 int cmt_wait(cmt_engine* e, cmt_step_result* r) {
   int rc = guard(e, [&] { e->eng->wait(r); });
+  if (!rc && r->status == CMT_ERR_INTERNAL) e->err = "recurrent scan flag wait timed out (step aborted, weights unchanged)";
   return rc ? rc : r->status;
 }
 int cmt_set_comm(cmt_engine* e, const void* uid, int rank, int world) {
@@ -2633,34 +2553,12 @@ int cmt_test_dropout(unsigned long long sh, unsigned long long sl, unsigned long
     cmt::PcgJump* jt = nullptr;
     CMT_CUDA(cudaMalloc(&jt, sizeof(cmt::PcgJump)));
     cmt::pcg_jump_table_kernel<<<1, 1>>>(jt, ih, il);
-    // the engine's kernel (dropout_fwd_kernel4) writes y / keep; the previous
-    // kernel3 must produce the same bits (checked here)
     dim3 grid4(cmt::ceil_div(H, 32), cmt::ceil_div(cmt::ceil_div(N, cmt::DROP4_DPT), 8));
     cmt::dropout_fwd_kernel4<float, float><<<grid4, blk>>>(x, y, keep, N, H, pcg, jt, base, cmt::dropout_threshold(p),
                                                             1.0f / (float)(1.0 - p));
-    const size_t n = (size_t)N * H;
-    float* y3 = nullptr;
-    unsigned char* k3 = nullptr;
-    CMT_CUDA(cudaMalloc(&y3, n * 4));
-    CMT_CUDA(cudaMalloc(&k3, n));
-    dim3 grid3(cmt::ceil_div(H, 32), cmt::ceil_div(cmt::ceil_div(N, cmt::DROP_DPT), 8));
-    cmt::dropout_fwd_kernel3<float, float><<<grid3, blk>>>(x, y3, k3, N, H, pcg, jt, base, cmt::dropout_threshold(p),
-                                                            1.0f / (float)(1.0 - p));
     cudaError_t err = cudaDeviceSynchronize();
-    std::vector<unsigned char> ka(n), kb(n);
-    std::vector<float> ya(n), yb(n);
-    if (err == cudaSuccess) {
-      cudaMemcpy(ka.data(), keep, n, cudaMemcpyDeviceToHost);
-      cudaMemcpy(kb.data(), k3, n, cudaMemcpyDeviceToHost);
-      cudaMemcpy(ya.data(), y, n * 4, cudaMemcpyDeviceToHost);
-      cudaMemcpy(yb.data(), y3, n * 4, cudaMemcpyDeviceToHost);
-    }
     cudaFree(jt);
-    cudaFree(y3);
-    cudaFree(k3);
     CMT_CUDA(err);
-    if (ka != kb || std::memcmp(ya.data(), yb.data(), n * 4) != 0)
-      throw Error(cmt::CMT_ERR_INTERNAL, "dropout kernels 3 and 4 disagree");
     CMT_CUDA(cudaGetLastError());
     CMT_CUDA(cudaDeviceSynchronize());
   });
@@ -2670,18 +2568,11 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     std::string k(key);
     if (k == "time_dominant") e->eng->time_dominant = (int)value;
     else if (k == "persistent") e->eng->persistent = (int)value;
-    else if (k == "cluster") e->eng->clustered = (int)value;
     else if (k == "cg2") e->eng->cg2 = (int)value;
     else if (k == "dual") e->eng->dual = (int)value;
     else if (k == "fwd_tm") e->eng->fwd_tm = (int)value;
-    else if (k == "bwd_tm") e->eng->bwd_tm = (int)value;
     else if (k == "ar_overlap") e->eng->ar_overlap = (int)value;
     else if (k == "early_dec1") e->eng->early_dec1 = (int)value;
-    else if (k == "bg_dw") {
-      if (e->eng->staged && (value != 0) != (e->eng->bg_dw != 0)) throw Error(cmt::CMT_ERR_CONFIG, "set bg_dw before staging");
-      e->eng->bg_dw = (int)value;
-    }
-    else if (k == "jump") e->eng->use_jump = (int)value;
     else if (k == "att_split") e->eng->att_split = (int)value;
     else if (k == "allow_empty_targets") e->eng->allow_empty_targets = (int)value;
     else if (k == "overlap") e->eng->overlap = (int)value;
@@ -2689,7 +2580,6 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
       if (e->eng->staged && (value != 0) != (e->eng->ce2 != 0)) throw Error(cmt::CMT_ERR_CONFIG, "set ce2 before staging");
       e->eng->ce2 = (int)value;
     }
-    else if (k == "cluster_fwd") e->eng->clustered_fwd = (int)value;
     else if (k == "tma_store") cmt::g_tma_store = (int)value;
     else if (k == "gemm_opt") cmt::g_gemm_opt = (int)value;
     else if (k == "splitk") cmt::g_splitk = (int)value;
@@ -2732,7 +2622,8 @@ int cmt_debug_buffer(cmt_engine* e, const char* name, float* out, long long cap,
 int cmt_get_stat(cmt_engine* e, const char* key, double* value, double* count) {
   return guard(e, [&] {
     std::string k(key);
-    if (k == "dominant_ms") *value = e->eng->dominant_ms(count);
+    if (k == "dominant_ms") *value = e->eng->probe_ms(0, count);
+    else if (k.rfind("probe_ms:", 0) == 0) *value = e->eng->probe_ms(std::stoi(k.substr(9)), count);
     else if (k.rfind("trace:", 0) == 0) {
       int i = std::stoi(k.substr(6));
       unsigned long long v = 0;

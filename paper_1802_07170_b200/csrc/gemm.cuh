@@ -131,7 +131,28 @@ struct EpiStore {
       case 8: compute_t<8>(m, n0, v, M, N, x); break;
       case 12: compute_t<12>(m, n0, v, M, N, x); break;
       case 16: compute_t<16>(m, n0, v, M, N, x); break;
-      default: compute_t<63>(m, n0, v, M, N, x, pb);
+      default: compute_any(m, n0, v, M, N, x, pb);
+    }
+  }
+  // any other stage combination: the same stages, each operand loaded per
+  // element (no 32-wide staging arrays, so this rarely-used path adds no
+  // register pressure to the kernel)
+  CMT_D void compute_any(int m, int n0, const float* v, int M, int N, float* x, const float* pb) const {
+    const bool row_ok = m < M;
+    const long long rm = row_ok ? (long long)m : 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const bool ok = row_ok && n0 + j < N;
+      float t = v[j];
+      if (bias) t += pb ? pb[j] : (n0 + j < N ? __ldg(bias + n0 + j) : 0.f);
+      if (act == 1) t = c_bf16 ? ptx::tanh_fast(t) : tanhf(t);
+      if (dmask) t = (ok && dmask[rm * ld_dmask + n0 + j]) ? t * dscale : 0.f * t;
+      if (tgrad_y) {
+        const float ty = ok ? tgrad_y[rm * ld_tgrad + n0 + j] : 0.f;
+        t *= (1.f - ty * ty);
+      }
+      if (add) t += ok ? add[rm * ld_add + n0 + j] : 0.f;
+      x[j] = t;
     }
   }
 
@@ -560,7 +581,7 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
         ptx::tc_fence_after();
       }
 #pragma unroll 1
-      for (int c = c_lo; c < ((opt & 4) ? c_lo : c_hi); ++c) {  // opt bit 2: mainloop-only timing experiment
+      for (int c = c_lo; c < c_hi; ++c) {
         float v[32];
         float bvp[32];  // bias prefetch (overlaps the TMEM load)
         bool pre = false;
@@ -576,17 +597,9 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
         }
         if constexpr (ST) {
           const int nc = n0 + c * 32, mw = m0 + q * 32;
-          if ((opt & 16) && nc < N) {  // timing experiment: TMEM drain only
-            if (v[lane] == 123.456f) epi.C = nullptr;
-            continue;
-          }
           if (nc < N && mw < M) {
             float x[32];
             epi.compute(m, nc, v, M, N, x, pre ? bvp : nullptr);
-            if (opt & 8) {  // timing experiment: no store
-              if (x[lane] == 123.456f) epi.C = nullptr;
-              continue;
-            }
             // fp32 rows: 2 x 4 KB buffers; bf16 rows (2 KB): 4 buffers in the same space
             uint8_t* sb;
             if (epi.c_bf16) {

@@ -256,35 +256,12 @@ CMT_D u128 pcg_jump(const PcgJump* __restrict__ t, u128 s, unsigned long long de
   return s;
 }
 
-// Same contract as dropout_fwd_kernel2 with the table jump and 64 draws per
-// thread (the jump is amortised over twice as many draws).
-constexpr int DROP_DPT = 16;
+// Dropout site y = x * keep/(1-p) of shape (H, N) in the reference's C order:
+// element (h, n) is draw (base + h*N + n) of numpy's Generator.random.
 // keep  <=>  (r >> 11) * 2^-53 >= p  <=>  (r >> 11) >= ceil(p * 2^53): the
 // reference's double comparison done exactly in integers (p * 2^53 is exact).
 inline unsigned long long dropout_threshold(double p) { return (unsigned long long)std::ceil(p * 9007199254740992.0); }
-template <typename TI, typename TO>
-__global__ void dropout_fwd_kernel3(const TI* __restrict__ x, TO* __restrict__ y, uint8_t* __restrict__ keep, int N,
-                                    int H, Pcg pcg, const PcgJump* __restrict__ jt, unsigned long long base,
-                                    unsigned long long thr, float scale) {
-  const int h = blockIdx.x * 32 + threadIdx.x;
-  const int n0 = (blockIdx.y * blockDim.y + threadIdx.y) * DROP_DPT;
-  if (h >= H || n0 >= N) return;
-  const u128 inc = ((u128)pcg.inc_hi << 64) | pcg.inc_lo;
-  u128 s = pcg_jump(jt, ((u128)pcg.state_hi << 64) | pcg.state_lo, base + (unsigned long long)h * N + n0);
-  const u128 mult = pcg_mult();
-  const int nend = min(N, n0 + DROP_DPT);
-#pragma unroll 4
-  for (int n = n0; n < nend; ++n) {
-    s = s * mult + inc;
-    const bool k = (pcg_out(s) >> 11) >= thr;
-    const long long i = (long long)n * H + h;
-    keep[i] = k;
-    const float xv = to_f<TI>(x[i]);
-    y[i] = from_f<TO>(k ? xv * scale : xv * 0.f);
-  }
-}
-
-// Same draws as dropout_fwd_kernel3 with the LCG step written in 64-bit halves
+// The PCG64 jump-ahead starts each thread's run of draws; the LCG step is written in 64-bit halves
 // against the constant PCG64 multiplier (one umulhi, three low products, one
 // carry), the keep test on the state halves directly, and the element index
 // advanced incrementally: about half the instructions per draw.
@@ -316,33 +293,6 @@ __global__ void dropout_fwd_kernel4(const TI* __restrict__ x, TO* __restrict__ y
     // x2: the input is x + x2 rounded to TI, exactly what add2_kernel stores
     // (the bidirectional sum of encoder layer 1, layers.py:162-180)
     const float xv = x2 ? to_f<TI>(from_f<TI>(to_f<TI>(x[i]) + to_f<TI>(x2[i]))) : to_f<TI>(x[i]);
-    y[i] = from_f<TO>(k ? xv * scale : xv * 0.f);
-  }
-}
-
-// y = x * keep/(1-p) for one dropout site of shape (H, N) in the reference's
-// C order: element (h, n) is draw (base + h*N + n).  Activations here are
-// token-major [n][h]; a warp covers 32 consecutive h, each thread 32
-// consecutive n of its h, so mask writes stay 32-byte coalesced.
-template <typename TI, typename TO>
-__global__ void dropout_fwd_kernel2(const TI* __restrict__ x, TO* __restrict__ y, uint8_t* __restrict__ keep, int N,
-                                   int H, Pcg pcg, unsigned long long base, double p, float scale) {
-  int h = blockIdx.x * 32 + threadIdx.x;
-  int n0 = (blockIdx.y * blockDim.y + threadIdx.y) * 32;
-  if (h >= H || n0 >= N) return;
-  u128 st = ((u128)pcg.state_hi << 64) | pcg.state_lo;
-  u128 inc = ((u128)pcg.inc_hi << 64) | pcg.inc_lo;
-  u128 s = pcg_advance(st, inc, base + (unsigned long long)h * N + n0);
-  const u128 mult = pcg_mult();
-  int nend = min(N, n0 + 32);
-  for (int n = n0; n < nend; ++n) {
-    s = s * mult + inc;
-    unsigned long long r = pcg_out(s);
-    double u = (double)(r >> 11) * (1.0 / 9007199254740992.0);
-    bool k = u >= p;
-    long long i = (long long)n * H + h;
-    keep[i] = k;
-    float xv = to_f<TI>(x[i]);
     y[i] = from_f<TO>(k ? xv * scale : xv * 0.f);
   }
 }
@@ -617,147 +567,15 @@ __global__ void sum_to_double_kernel(const float* __restrict__ x, int n, double*
 // then a fixed-order combine -> deterministic.
 // ---------------------------------------------------------------------------
 // ---------------------------------------------------------------------------
-// Fused log-softmax + smoothed CE + gradient + bias-gradient column sums over
-// bf16 logits (production path; rows 16-byte aligned, V <= CE2_MAXV).  A
-// persistent CTA walks rows blockIdx.x, +gridDim.x, ...; each row is read with
-// 16-byte loads (pass 1: max / sum-exp / sum), then rewritten in place with
-// the gradient (pass 2) while the CTA accumulates d over its rows into a
-// shared-memory column sum (each thread owns fixed columns, so no atomics).
-// The per-CTA partial sums of d are reduced by colsum_final_kernel into
-// db_o = sum_n dY[n][v] (layers.py:72-73).  With the output tanh on, the
-// logits are in [-1, 1] and the sum of exponentials needs no max shift.
-// Same math as ce_kernel (training.py:96-120, tensor.py:146-151).
+// Fused CE over bf16 logits (production path; rows 16-byte aligned), same math
+// as ce_kernel (training.py:96-120, tensor.py:146-151).
 // ---------------------------------------------------------------------------
-constexpr int CE2_THREADS = 1024;
 constexpr float kLog2e = 1.4426950408889634f;
 CMT_D float ex2f(float x) {  // 2^x (MUFU.EX2)
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-constexpr int CE2_MAXV = 55 * 1024;  // smem column sums (fp32)
-constexpr int CE2_UNROLL = 4;        // 16-byte loads in flight per thread
-__global__ void __launch_bounds__(CE2_THREADS, 1)
-    ce_colsum_kernel(bf16* __restrict__ Y, int V, int rows, const int* __restrict__ tgt,
-                     const float* __restrict__ tmask, float eps, float inv_ntok, int tanh_on,
-                     float* __restrict__ losstok, int* __restrict__ status, float* __restrict__ part) {
-  extern __shared__ float csum[];  // [V]
-  __shared__ float red_m[CE2_THREADS / 32], red_s[CE2_THREADS / 32], red_y[CE2_THREADS / 32];
-  __shared__ float bc[2];
-  const int nv = V >> 3;  // 16-byte vectors per row
-  for (int v = threadIdx.x; v < V; v += CE2_THREADS) csum[v] = 0.f;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const float eV = eps / (float)V;
-  for (int n = blockIdx.x; n < rows; n += gridDim.x) {
-    uint4* row = (uint4*)(Y + (long long)n * V);
-    float mx = tanh_on ? 0.f : -INFINITY, se = 0.f, sy = 0.f;
-    bool bad = false;
-    for (int i0 = threadIdx.x; i0 < nv; i0 += CE2_UNROLL * CE2_THREADS) {
-      uint4 qv[CE2_UNROLL];
-#pragma unroll
-      for (int u = 0; u < CE2_UNROLL; ++u) {  // all loads in flight before any use
-        const int i = i0 + u * CE2_THREADS;
-        qv[u] = i < nv ? row[i] : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < CE2_UNROLL; ++u) {
-      if (i0 + u * CE2_THREADS >= nv) break;
-      const bf16* e = (const bf16*)&qv[u];
-      float y[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        y[j] = __bfloat162float(e[j]);
-        sy += y[j];
-      }
-      if (tanh_on) {
-        // |y| <= 1: no max shift; a non-finite logit makes the row sum
-        // non-finite, which is checked once per row below
-#pragma unroll
-        for (int j = 0; j < 8; ++j) se += ex2f(y[j] * kLog2e);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) bad |= !isfinite(y[j]);
-        float lm = y[0];
-#pragma unroll
-        for (int j = 1; j < 8; ++j) lm = fmaxf(lm, y[j]);
-        if (lm > mx) {
-          se = (mx == -INFINITY) ? 0.f : se * __expf(mx - lm);
-          mx = lm;
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) se += __expf(y[j] - mx);
-      }
-      }
-    }
-    float wm = warp_max(mx);
-    se = (mx == -INFINITY) ? 0.f : se * __expf(mx - wm);
-    se = warp_sum(se);
-    sy = warp_sum(sy);
-    if (tanh_on) bad = !isfinite(sy);
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, ST_LOGITS);
-    if (lane == 0) { red_m[warp] = wm; red_s[warp] = se; red_y[warp] = sy; }
-    __syncthreads();
-    if (warp == 0) {
-      float m2 = lane < CE2_THREADS / 32 ? red_m[lane] : -INFINITY;
-      float s2 = lane < CE2_THREADS / 32 ? red_s[lane] : 0.f;
-      float y2 = lane < CE2_THREADS / 32 ? red_y[lane] : 0.f;
-      float gm = warp_max(m2);
-      s2 = (m2 == -INFINITY) ? 0.f : s2 * __expf(m2 - gm);
-      s2 = warp_sum(s2);
-      y2 = warp_sum(y2);
-      if (lane == 0) {
-        const float lse = gm + logf(s2);
-        const int g = tgt[n];
-        const float gold = __bfloat162float(Y[(long long)n * V + g]);
-        const float per = lse - (1.f - eps) * gold - eV * y2;
-        const float m = tmask[n];
-        losstok[n] = per * m;
-        if (!isfinite(per)) atomicOr(status, ST_LOSS);
-        bc[0] = lse;
-        bc[1] = m * inv_ntok;
-      }
-    }
-    __syncthreads();
-    const float lse = bc[0], w = bc[1];
-    const int g = tgt[n];
-    const float lse2 = lse * kLog2e, ewv = eV * w, gw = (1.f - eps) * w;
-    for (int i0 = threadIdx.x; i0 < nv; i0 += CE2_UNROLL * CE2_THREADS) {
-      uint4 qv[CE2_UNROLL];
-#pragma unroll
-      for (int u = 0; u < CE2_UNROLL; ++u) {
-        const int i = i0 + u * CE2_THREADS;
-        qv[u] = i < nv ? row[i] : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < CE2_UNROLL; ++u) {
-      const int i = i0 + u * CE2_THREADS;
-      if (i >= nv) break;
-      const bf16* e = (const bf16*)&qv[u];
-      __align__(16) bf16 o[8];
-      float* cs = csum + i * 8;
-      const float4 c0 = *(const float4*)cs, c1 = *(const float4*)(cs + 4);
-      float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-      const int gj = g - i * 8;  // the gold column falls in this vector iff 0 <= gj < 8
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float y = __bfloat162float(e[j]);
-        // d = (p - eps/V - (1-eps)[v=gold]) * m / ntok   (* (1 - y^2) with the output tanh)
-        float d = fmaf(ex2f(fmaf(y, kLog2e, -lse2)), w, -ewv);
-        if (j == gj) d -= gw;
-        if (tanh_on) d *= fmaf(-y, y, 1.f);
-        o[j] = __float2bfloat16_rn(d);
-        c[j] += d;  // bias grad = column sum of dpre (fp32, layers.py:72-73)
-      }
-      row[i] = *(const uint4*)o;
-      *(float4*)cs = make_float4(c[0], c[1], c[2], c[3]);
-      *(float4*)(cs + 4) = make_float4(c[4], c[5], c[6], c[7]);
-      }
-    }
-    __syncthreads();  // bc / red reuse
-  }
-  for (int v = threadIdx.x; v < V; v += CE2_THREADS) part[(long long)blockIdx.x * V + v] = csum[v];
-}
-
 // Two-pass fused CE (ce2 = 2, default): both passes run at full occupancy
 // with no shared-memory column accumulators.
 // Pass 1, one CTA per token row: log-sum-exp, smoothed per-token loss and the
@@ -914,12 +732,30 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, 
 // Global-norm clip + SGD (training.py:123-142)
 // ---------------------------------------------------------------------------
 constexpr int NORM_BLOCKS = 592;  // 4 x 148 SMs
-__global__ void sumsq_partial_kernel(const float* __restrict__ g, long long n, double* __restrict__ part) {
+// Gate (de)interleave for parameter upload / download: the reference block
+// w_q (rows, H) is column 4j+q of the engine's [rows][4H] layer matrix.
+// to_inter: plain -> interleaved (upload); else interleaved -> plain (download).
+__global__ void gate_copy_kernel(float* __restrict__ inter, float* __restrict__ plain, long long rows, int H,
+                                 int q, int to_inter) {
+  const long long n = rows * H;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / H, j = i - r * H;
+    float* d = inter + r * 4LL * H + 4 * j + q;
+    if (to_inter) *d = plain[i];
+    else plain[i] = *d;
+  }
+}
+
+// lanes: 4-bit gate mask; element i (from g) counts iff bit (i & 3) is set
+// (15 = every element; in a gate-interleaved LSTM region i & 3 is the gate)
+__global__ void sumsq_partial_kernel(const float* __restrict__ g, long long n, double* __restrict__ part,
+                                     int lanes) {
   __shared__ double red[32];
   float a = 0.f;
   double ad = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool l0 = lanes & 1, l1 = lanes & 2, l2 = lanes & 4, l3 = lanes & 8;
   int cnt = 0;
   if ((((uintptr_t)g) & 15) == 0) {
     const long long n4 = n >> 2;
@@ -931,24 +767,25 @@ __global__ void sumsq_partial_kernel(const float* __restrict__ g, long long n, d
       for (int u = 0; u < 4; ++u) v[u] = __ldcs(g4 + i + u * stride);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        a = fmaf(v[u].x, v[u].x, a);
-        a = fmaf(v[u].y, v[u].y, a);
-        a = fmaf(v[u].z, v[u].z, a);
-        a = fmaf(v[u].w, v[u].w, a);
+        a = fmaf(l0 ? v[u].x : 0.f, l0 ? v[u].x : 0.f, a);
+        a = fmaf(l1 ? v[u].y : 0.f, l1 ? v[u].y : 0.f, a);
+        a = fmaf(l2 ? v[u].z : 0.f, l2 ? v[u].z : 0.f, a);
+        a = fmaf(l3 ? v[u].w : 0.f, l3 ? v[u].w : 0.f, a);
       }
       if (++cnt == 16) { ad += a; a = 0.f; cnt = 0; }
     }
     for (; i < n4; i += stride) {
       const float4 v = g4[i];
-      a = fmaf(v.x, v.x, a);
-      a = fmaf(v.y, v.y, a);
-      a = fmaf(v.z, v.z, a);
-      a = fmaf(v.w, v.w, a);
+      a = fmaf(l0 ? v.x : 0.f, l0 ? v.x : 0.f, a);
+      a = fmaf(l1 ? v.y : 0.f, l1 ? v.y : 0.f, a);
+      a = fmaf(l2 ? v.z : 0.f, l2 ? v.z : 0.f, a);
+      a = fmaf(l3 ? v.w : 0.f, l3 ? v.w : 0.f, a);
     }
-    for (long long j = 4 * n4 + tid; j < n; j += stride) a = fmaf(g[j], g[j], a);
+    for (long long j = 4 * n4 + tid; j < n; j += stride)
+      if ((lanes >> (j & 3)) & 1) a = fmaf(g[j], g[j], a);
   } else {
     for (long long i = tid; i < n; i += stride) {
-      float v = g[i];
+      const float v = ((lanes >> (i & 3)) & 1) ? g[i] : 0.f;
       a = fmaf(v, v, a);
       if (++cnt == 256) { ad += a; a = 0.f; cnt = 0; }
     }
@@ -984,19 +821,47 @@ __global__ void clip_scale_kernel(const double* __restrict__ part, int nparts, d
   scal[1] = norm;
   if (!isfinite(norm)) atomicOr(status, ST_NORM);
   double scale = 1.0;
-  if (clip > 0.0 && norm > clip) scale = clip / norm;
+  if (clip >= 0.0 && norm > clip) scale = clip / norm;  // clip < 0 or NaN: None
   *s32 = (float)(lr * scale);
 }
 constexpr int CLIP_THREADS = 512;
 
-constexpr int ST_ABORT = ST_SCORES | ST_LOGITS | ST_LOSS | ST_NORM;
+constexpr int ST_ABORT = ST_SCORES | ST_LOGITS | ST_LOSS | ST_NORM | ST_HANG;
 
+// Data parallel: the ranks' status words are combined flag by flag.  A rank's
+// word is spread into one int per flag, the ints are max-reduced over ranks
+// (ncclMax) and the word is rebuilt, so k ranks raising the same flag give that
+// flag, never a carry into another one (status_combine is the host statement of
+// the same rule, exported for the CPU test).
+constexpr int ST_NFLAGS = 5;
+CMT_HD int status_spread(int s, int i) { return (s >> i) & 1; }
+CMT_HD int status_rebuild(const int* f) {
+  int s = 0;
+  for (int i = 0; i < ST_NFLAGS; ++i) s |= f[i] ? (1 << i) : 0;
+  return s;
+}
+inline int status_combine(const int* words, int n) {  // = spread, max over ranks, rebuild
+  int f[ST_NFLAGS] = {0, 0, 0, 0, 0};
+  for (int r = 0; r < n; ++r)
+    for (int i = 0; i < ST_NFLAGS; ++i) f[i] = f[i] > status_spread(words[r], i) ? f[i] : status_spread(words[r], i);
+  return status_rebuild(f);
+}
+__global__ void status_spread_kernel(const int* __restrict__ status, int* __restrict__ f) {
+  if (threadIdx.x < ST_NFLAGS) f[threadIdx.x] = status_spread(*status, threadIdx.x);
+}
+__global__ void status_gather_kernel(const int* __restrict__ f, int* __restrict__ status) {
+  if (threadIdx.x == 0) *status = status_rebuild(f);
+}
+
+// w -= fp32(lr * scale) * g over the elements whose gate bit (i & 3) is set in lanes
 __global__ void sgd_dense_kernel(float* __restrict__ w, const float* __restrict__ g, bf16* __restrict__ shadow,
-                                 long long n, const float* __restrict__ s32, const int* __restrict__ status) {
+                                 long long n, const float* __restrict__ s32, const int* __restrict__ status,
+                                 int lanes) {
   if (*status & ST_ABORT) return;
   const float s = *s32;
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool l0 = lanes & 1, l1 = lanes & 2, l2 = lanes & 4, l3 = lanes & 8;
   // 16-byte vectors over the (256-byte aligned) arena, scalar tail
   const long long n4 = n >> 2;
   float4* w4 = (float4*)w;
@@ -1004,10 +869,10 @@ __global__ void sgd_dense_kernel(float* __restrict__ w, const float* __restrict_
   for (long long i = tid; i < n4; i += stride) {
     const float4 wv = w4[i], gv = __ldcs(g4 + i);
     float4 nw;
-    nw.x = __fsub_rn(wv.x, __fmul_rn(s, gv.x));
-    nw.y = __fsub_rn(wv.y, __fmul_rn(s, gv.y));
-    nw.z = __fsub_rn(wv.z, __fmul_rn(s, gv.z));
-    nw.w = __fsub_rn(wv.w, __fmul_rn(s, gv.w));
+    nw.x = l0 ? __fsub_rn(wv.x, __fmul_rn(s, gv.x)) : wv.x;
+    nw.y = l1 ? __fsub_rn(wv.y, __fmul_rn(s, gv.y)) : wv.y;
+    nw.z = l2 ? __fsub_rn(wv.z, __fmul_rn(s, gv.z)) : wv.z;
+    nw.w = l3 ? __fsub_rn(wv.w, __fmul_rn(s, gv.w)) : wv.w;
     w4[i] = nw;
     if (shadow) {
       __align__(8) bf16 b4[4] = {__float2bfloat16_rn(nw.x), __float2bfloat16_rn(nw.y), __float2bfloat16_rn(nw.z),
@@ -1016,6 +881,7 @@ __global__ void sgd_dense_kernel(float* __restrict__ w, const float* __restrict_
     }
   }
   for (long long i = 4 * n4 + tid; i < n; i += stride) {
+    if (!((lanes >> (i & 3)) & 1)) continue;
     float nw = __fsub_rn(w[i], __fmul_rn(s, g[i]));
     w[i] = nw;
     if (shadow) shadow[i] = __float2bfloat16_rn(nw);

@@ -14,7 +14,7 @@
 // the batch over two CTAs (128 CTAs, the single-chain configuration).
 // Reference semantics: layers.py:344-363 (cell), layers.py:440-470 (scan).
 #pragma once
-#include "lstm_persistent.cuh"
+#include "lstm_common.cuh"
 
 namespace cmt {
 namespace mc {
@@ -112,12 +112,15 @@ __global__ void __launch_bounds__(mc::THREADS, 1)
       const int hrow = p.hrow0 + t * p.B + r0;
       const unsigned target = 4u * (unsigned)s;
       int issued = 0;
+      SpinGuard guard;
       while (issued < nst) {
         unsigned ready = 0xffffffffu;
         if (s > 0) {
           const bool ok = lane >= KB || ptx::ld_acquire(p.flag + lane * nh + half) >= target;
           ready = __ballot_sync(0xffffffffu, ok);
-          __syncwarp();  // order the lanes' acquire loads before lane 0's TMA issue
+          __syncwarp();
+          if (ready != 0xffffffffu && __shfl_sync(0xffffffffu, lane == 0 ? (int)guard.expired(p.status) : 0, 0))
+            ready = 0xffffffffu;  // wait budget exceeded: the step is reported failed  // order the lanes' acquire loads before lane 0's TMA issue
         }
         if (lane == 0) {
           if (s > 0) ptx::fence_proxy_async_global();
@@ -381,10 +384,13 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
       const int arow = time_of(p.steps - i) * p.B + r0;
       const unsigned target = (unsigned)i;
       int issued = 0;
+      SpinGuard guard;
       while (issued < nst) {
         const bool ok = lane >= KBL || ptx::ld_acquire(p.flag + (kb_base + lane) * nh + half) >= target;
-        const unsigned ready = __ballot_sync(0xffffffffu, ok);
+        unsigned ready = __ballot_sync(0xffffffffu, ok);
         __syncwarp();
+        if (ready != 0xffffffffu && __shfl_sync(0xffffffffu, lane == 0 ? (int)guard.expired(p.status) : 0, 0))
+          ready = 0xffffffffu;  // wait budget exceeded: the step is reported failed
         if (lane == 0) {
           ptx::fence_proxy_async_global();
           ptx::fence_proxy_async_shared();

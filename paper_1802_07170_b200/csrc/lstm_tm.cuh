@@ -190,12 +190,15 @@ __global__ void __launch_bounds__(tm::THREADS, 1)
       const int hrow = p.hrow0 + t * p.B + r0;
       const unsigned target = 2u * (unsigned)s;
       int issued = 0;
+      SpinGuard guard;
       while (issued < nst) {
         unsigned ready = 0xffffffffu;
         if (s > 0) {
           const bool ok = lane >= KB || ptx::ld_acquire(p.flag + lane * nh + half) >= target;
           ready = __ballot_sync(0xffffffffu, ok);
           __syncwarp();
+          if (ready != 0xffffffffu && __shfl_sync(0xffffffffu, lane == 0 ? (int)guard.expired(p.status) : 0, 0))
+            ready = 0xffffffffu;  // wait budget exceeded: the step is reported failed
         }
         if (lane == 0) {
           if (s > 0) ptx::fence_proxy_async_global();

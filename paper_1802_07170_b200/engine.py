@@ -124,6 +124,7 @@ class Engine:
             self._check(self.lib.cmt_block_info(h, i, name, 256, ctypes.byref(r), ctypes.byref(cc)))
             self.blocks.append((name.value.decode(), (r.value, cc.value)))
         self.index = {n: i for i, (n, _) in enumerate(self.blocks)}
+        self.learnable = [True] * len(self.blocks)
         self.last_draws = 0
 
     def close(self):
@@ -198,6 +199,18 @@ class Engine:
             raise ConfigError("restore needs a live snapshot of this engine")
         self._check(self.lib.cmt_snapshot_restore(self.h, snap.slot))
 
+    def set_learnable(self, flags):
+        """{name: bool} or a reference ModelParams: frozen blocks (ParamBlock.learnable
+        False, graph.py:20-31) are left out of the norm and the update
+        (training.py:128-139)."""
+        items = flags.items() if isinstance(flags, dict) else ((b.name, getattr(b, "learnable", True))
+                                                                for b in flags.blocks())
+        for n, on in items:
+            i = self.index[n]
+            if bool(on) != self.learnable[i]:
+                self._check(self.lib.cmt_set_learnable(self.h, i, int(bool(on))))
+                self.learnable[i] = bool(on)
+
     def download_into(self, params):
         for b in params.blocks():
             np.copyto(b.var.data, self._download(self.lib.cmt_download_param, b.name).astype(b.var.data.dtype))
@@ -221,7 +234,7 @@ class Engine:
         """One step on the staged batch.  Advances ``rng`` by the draws used.
         ``infer=True``: forward only in INFER mode (no dropout/backward/update)."""
         st = pcg_state(rng) if rng is not None else (0, 0, 0, 1)
-        a = _lib.StepArgs(float(lr), float(clip) if clip is not None else -1.0, float(eps),
+        a = _lib.StepArgs(float(lr), float(clip) if clip is not None else float("nan"), float(eps),
                           st[0], st[1], st[2], st[3], float(global_ntok),
                           (0 if update else _lib.FLAG_NO_UPDATE) | (_lib.FLAG_ASYNC if asynchronous else 0)
                           | (_lib.FLAG_INFER if infer else 0))
@@ -285,29 +298,47 @@ class Engine:
         if pending:
             yield self._finish()
 
-    # ---- translation (decode_begin / decode_step, include/cytonmt_b200.h) ----
-    def decode_begin(self, src_tokens):
-        """Encode one source sentence (INFER) and reset the decoder states to its finals."""
-        src = np.ascontiguousarray(np.asarray(src_tokens, dtype=np.int64).reshape(-1))
-        if src.size == 0:
-            raise ConfigError("cannot translate an empty source sentence")
-        self._check(self.lib.cmt_decode_begin(self.h, _llptr(src), int(src.size)))
+    # ---- translation: batched beam search on the device (cmt_beam_*, include/cytonmt_b200.h) ----
+    def beam_search(self, sources, beam, n_best, max_lens, lp_table, steps_per_call=16):
+        """Beam search for a list of non-empty id sequences at once.
 
-    def decode_step(self, prev_tokens, parent, k):
-        """One decoder step for the rows ``prev_tokens`` (parent: state row of the
-        previous step per row, or None for the encoder finals).  Returns the k
-        best (log-prob, token) of every row as arrays of shape (n, k)."""
-        prev = np.ascontiguousarray(np.asarray(prev_tokens, dtype=np.int64).reshape(-1))
-        n = int(prev.size)
-        vals = np.empty((n, k), dtype=np.float32)
-        toks = np.empty((n, k), dtype=np.int32)
-        par_p = None
-        if parent is not None:
-            par = np.ascontiguousarray(np.asarray(parent, dtype=np.int32).reshape(-1))
-            par_p = par.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
-        self._check(self.lib.cmt_decode_step(self.h, n, _llptr(prev), par_p, int(k), _fptr(vals),
-                                             toks.ctypes.data_as(ctypes.POINTER(ctypes.c_int))))
-        return vals, toks
+        ``max_lens[i]`` is sentence i's length cap, ``lp_table[n]`` the length
+        penalty of n tokens.  Returns, per sentence, the list of results
+        ``(tokens, score, log_prob, truncated)`` (score None when truncated)."""
+        B = len(sources)
+        S = max(len(x) for x in sources)
+        src = np.zeros((S, B), dtype=np.int64)
+        mask = np.zeros((S, B), dtype=np.float32)
+        for b, x in enumerate(sources):
+            src[:len(x), b] = np.asarray(x, dtype=np.int64)
+            mask[:len(x), b] = 1.0
+        ml = np.ascontiguousarray(max_lens, dtype=np.int32)
+        lpt = np.ascontiguousarray(lp_table, dtype=np.float64)
+        ip = ctypes.POINTER(ctypes.c_int)
+        dp = ctypes.POINTER(ctypes.c_double)
+        self._check(self.lib.cmt_beam_begin(self.h, _llptr(src), _fptr(mask), S, B, int(beam), int(n_best),
+                                            ml.ctypes.data_as(ip), lpt.ctypes.data_as(dp), int(lpt.size)))
+        active = ctypes.c_int(1)
+        while active.value:
+            self._check(self.lib.cmt_beam_step(self.h, int(steps_per_call), ctypes.byref(active)))
+        cap = int(ml.max()) + 1
+        toks = np.empty(cap, dtype=np.int32)
+        n_tok, n_res, trunc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        score, logp = ctypes.c_double(), ctypes.c_double()
+        out = []
+        for b in range(B):
+            res, rank = [], 0
+            while True:
+                self._check(self.lib.cmt_beam_result(self.h, b, rank, toks.ctypes.data_as(ip), cap, ctypes.byref(n_tok),
+                                                     ctypes.byref(score), ctypes.byref(logp), ctypes.byref(trunc),
+                                                     ctypes.byref(n_res)))
+                res.append(([int(t) for t in toks[:n_tok.value]], None if trunc.value else score.value, logp.value,
+                            bool(trunc.value)))
+                rank += 1
+                if rank >= n_res.value:
+                    break
+            out.append(res)
+        return out
 
     def _finish(self):
         r = self.wait()

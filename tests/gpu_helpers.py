@@ -39,3 +39,14 @@ def oracle_step(d, params, batch, eps, lr, clip, seed, update=True):
 def scaled_params(d, seed, scale):
     gen = np.random.Generator(np.random.PCG64(seed))
     return {n: gen.uniform(-scale, scale, size=s).astype(np.float32) for n, s in O.registry(d)}
+
+
+def step_close(new, old, ref_new, rel):
+    """The applied step w_new - w_old against the reference's, to `rel` of the
+    step's size plus one fp32 ulp of the weights: w - fp32(s*g) rounds to fp32,
+    so grads equal to ~1e-5 can still land one ulp apart, and one ulp of a 0.1
+    weight is ~1e-3 of a 1e-5 step."""
+    new, old, ref_new = (np.asarray(x, np.float64) for x in (new, old, ref_new))
+    ulp = float(np.spacing(np.float32(np.abs(ref_new).max())))
+    err = float(np.abs(new - ref_new).max())
+    return err <= rel * float(np.abs(ref_new - old).max()) + ulp, err

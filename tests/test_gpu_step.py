@@ -223,13 +223,10 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
     _, _, og, _, _ = oracle_step(d, params, (src, sm, tgt, tm), 0.1, 1.0, 5.0, 3, update=False)
     out = {}
     variants = {  # option settings per variant ("dual" = the default configuration)
-        "per_step": dict(persistent=0, dual=0, cluster=0),
-        "persistent": dict(persistent=1, dual=0, cluster=0),
-        "cluster": dict(persistent=1, dual=0, cluster=1, cluster_fwd=1),
+        "per_step": dict(persistent=0, dual=0),  # one tcgen05 GEMM per step, cell in the epilogue
+        "single": dict(dual=0),  # every scan alone: lstm_fwd_multi<64|128> / lstm_bwd_multi<64|128>
         "dual": dict(),  # default: paired forward scans in lstm_fwd_tm, paired BPTT in lstm_bwd_multi<128>
-        "dual_multi": dict(fwd_tm=0, bwd_tm=1),  # lstm_fwd_multi<128> / lstm_bwd_tm (W_h over smem + TMEM)
-        "tm_single": dict(fwd_tm=2, bwd_tm=2),  # single scans in the TMEM-split kernels too
-        "bg_dw": dict(bg_dw=1),  # BPTT weight grads on the background stream beside the next scans
+        "dual_multi": dict(fwd_tm=0),  # paired forward scans in lstm_fwd_multi<128>
     }
     for variant, opts in variants.items():
         eng = Engine(cfg_of(d), mode="bf16")
@@ -239,7 +236,7 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
         eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, np.random.Generator(np.random.PCG64(3)), update=False)
         out[variant] = eng.grads()
         eng.close()
-    for v in ("persistent", "cluster", "dual", "dual_multi", "tm_single", "bg_dw"):
+    for v in ("single", "dual", "dual_multi"):
         for n in og:
             assert O.norm_rel_err(out[v][n], out["per_step"][n]) < BF16_TOL, (v, n)
             assert O.norm_rel_err(out[v][n], og[n]) < BF16_TOL, (v, n)
@@ -434,8 +431,8 @@ def test_pipeline_matches_sequential_steps(mode):
 
 @pytest.mark.parametrize("tanh_", [True, False])
 def test_ce_variants_agree(tanh_):
-    """The three CE implementations (ce2=2 two-pass default, ce2=1 one-pass
-    persistent, ce2=0 per-row kernel + separate column sums) give the same loss
+    """The two CE implementations (ce2=2 two-pass default, ce2=0 per-row
+    kernel + separate column sums) give the same loss
     and gradients (including the output bias, a column sum of the CE
     gradient) within bf16 tolerance of the oracle, with and without the
     output tanh (training.py:96-120, layers.py:64-73)."""
@@ -446,7 +443,7 @@ def test_ce_variants_agree(tanh_):
     params = scaled_params(d, 8, 0.3)
     src, sm, tgt, tm = O.synthetic_batch(520, 7, 9, 20, seed=3, ragged=True)
     ol, _, og, _, _ = oracle_step(d, params, (src, sm, tgt, tm), 0.1, 1.0, 5.0, 1, update=False)
-    for ce2 in (2, 1, 0):
+    for ce2 in (2, 0):
         eng = Engine(cfg_of(d), mode="bf16")
         eng.set_option("ce2", ce2)
         eng.upload(params)

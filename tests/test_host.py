@@ -31,6 +31,26 @@ def test_library_loads_and_exports_all_header_symbols():
     assert isinstance(lib.cmt_launch_count(), int)
 
 
+def test_dp_status_combine_is_flagwise():
+    """The ranks' status words are combined flag by flag (engine.cu data-parallel
+    branch: spread, ncclMax, rebuild).  A SUM of the words would turn 4 ranks
+    raising ST_LOGITS (2) into 8 = ST_NORM and 16 ranks raising it into 32,
+    outside the abort mask; the flagwise rule keeps exactly the raised flags."""
+    import ctypes
+    lib = _lib.load()
+    ST_SCORES, ST_LOGITS, ST_LOSS, ST_NORM = 1, 2, 4, 8
+
+    def combine(words):
+        arr = (ctypes.c_int * len(words))(*words)
+        return lib.cmt_status_combine(arr, len(words))
+    for n in (1, 2, 4, 8, 16):
+        assert combine([ST_LOGITS] * n) == ST_LOGITS
+        assert combine([0] * (n - 1) + [ST_NORM]) == ST_NORM
+    assert combine([0, 0, 0]) == 0
+    assert combine([ST_SCORES, ST_LOSS, 0, ST_SCORES | ST_NORM]) == ST_SCORES | ST_LOSS | ST_NORM
+    assert sum([ST_LOGITS] * 4) == ST_NORM  # what the old SUM combine produced
+
+
 def test_create_without_gpu_fails_loudly():
     import torch
     if torch.cuda.is_available():
