@@ -30,6 +30,7 @@
 #include "lstm_multi.cuh"
 #include "lstm_tm.cuh"
 #include "attention.cuh"
+#include "attention_tc.cuh"
 #include "decode.cuh"
 
 namespace cmt {
@@ -383,6 +384,63 @@ class Engine {
   float* colpart2 = nullptr;  // column-sum scratch of the side stream
   float* dho32 = nullptr;   // fp32 split-K scratch of dH_o (bf16 mode)
   float *att_part = nullptr, *att_dsc = nullptr;  // split attention: score slices, d scores
+  bf16 *att_a16 = nullptr, *att_d16 = nullptr, *att_dc16 = nullptr;
+  int att_tc = 1;  // option: attention core as batched tcgen05 GEMMs (attention_tc.cuh)
+  bool att_tc_ok() const { return bf && att_tc && S <= 256 && H % 64 == 0; }
+  int s8() const { return (S + 7) / 8 * 8; }
+  // one operand of a batched GEMM as a 3-D TMA map (attention_tc.cuh)
+  struct BatOp {
+    const void* p;
+    long long d0, rows;       // contiguous extent, row extent
+    long long bstr, rstr;     // batch / row strides in bytes
+    int bpos;                 // 1: {d0, batch, rows}, 2: {d0, rows, batch}
+  };
+  void bat_map(CUtensorMap* m, const BatOp& o, int nb, int box0, int boxr) {
+    if (((uintptr_t)o.p & 15) || (o.bstr & 15) || (o.rstr & 15))
+      throw Error(CMT_ERR_SHAPE, "batched GEMM operand not 16-byte aligned");
+    const bool mid = o.bpos == 1;
+    cuuint64_t gdim[3] = {(cuuint64_t)o.d0, (cuuint64_t)(mid ? nb : o.rows), (cuuint64_t)(mid ? o.rows : nb)};
+    cuuint64_t gstr[2] = {(cuuint64_t)(mid ? o.bstr : o.rstr), (cuuint64_t)(mid ? o.rstr : o.bstr)};
+    cuuint32_t box[3] = {(cuuint32_t)box0, (cuuint32_t)(mid ? 1 : boxr), (cuuint32_t)(mid ? boxr : 1)};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = get_encode()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(o.p), gdim, gstr, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(CMT_ERR_CUDA, "cuTensorMapEncodeTiled (batched) failed: " + std::to_string((int)r));
+  }
+  // C_b = A_b B_b^T for every batch b (one work unit per (b, tile)); A_MN / B_MN as in gemm.cuh
+  template <int BN, int AMN, int BMN>
+  void bat_gemm(int M, int N, int K, int nb, const BatOp& A, const BatOp& Bo, const BatStore& e) {
+    using C = bat::Cfg<BN>;
+    auto kfn = gemm_bat_kernel<BN, AMN, BMN>;
+    static bool attr = false;
+    if (!attr) {
+      CMT_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+      attr = true;
+    }
+    CUtensorMap ta, tb;
+    bat_map(&ta, A, nb, 64, AMN ? 64 : bat::BM);
+    bat_map(&tb, Bo, nb, 64, BMN ? 64 : BN);
+    const int tiles = nb * ceil_div(M, bat::BM) * ceil_div(N, BN);
+    kfn<<<std::min(tiles, g_num_sms), bat::THREADS, C::SMEM, st>>>(ta, tb, M, N, K, nb, A.bpos, Bo.bpos, e);
+    CMT_LAUNCHED();
+    tl_mark(st, "attn_tc " + gemm_label(M, N, K, BN, 1));
+  }
+  // scores / dalpha: C_b[T][S] = X_b Hs_b^T with X = U or dC (rows t*B+b, K = H)
+  void att_tc_ts(const void* X, float* out) {
+    const void* Hs = (L == 1) ? top : views(L, false).ybase;
+    const BatOp xa{X, H, T, H * 2LL, (long long)B * H * 2, 1}, hb{Hs, H, S, H * 2LL, (long long)B * H * 2, 1};
+    const BatStore e{out, S, (long long)T * S, 0, 0};
+    if (S <= 64) bat_gemm<64, 0, 0>(T, S, H, B, xa, hb, e);
+    else if (S <= 128) bat_gemm<128, 0, 0>(T, S, H, B, xa, hb, e);
+    else bat_gemm<256, 0, 0>(T, S, H, B, xa, hb, e);
+  }
+  // [T x H] products: C_b = P_b Hs_b with P = alpha or dscores (bf16 [B][T][S8], K = S)
+  void att_tc_th(const bf16* P, void* out, long long ldc, long long bstride, int c_bf16) {
+    const void* Hs = (L == 1) ? top : views(L, false).ybase;
+    const BatOp pa{P, S, T, (long long)T * s8() * 2, s8() * 2LL, 2}, hb{Hs, H, S, H * 2LL, (long long)B * H * 2, 1};
+    bat_gemm<256, 0, 1>(T, H, S, B, pa, hb, BatStore{out, ldc, bstride, c_bf16, 0});
+  }
   int att_split = 2;  // option: 2 tiled split attention (S,T <= 128), 1 split (<= 64), 0 per-sentence
   int allow_empty_targets = 0;  // option: stage batches with no unmasked target (dev_entropy)
   bool last_infer = false;
@@ -1069,7 +1127,14 @@ class Engine {
     u_att = carve<char>(cur, NT * H * asz);
     alpha = carve<float>(cur, (long long)B * T * S * 4);
     att_dsc = carve<float>(cur, (long long)B * T * S * 4);
-    att_part = carve<float>(cur, (long long)B * att::nslices(H) * att2::tiles(T) * att2::tiles(S) * att2::P * att2::P * 4);
+    att_part = att_tc_ok() ? nullptr
+                           : carve<float>(cur, (long long)B * att::nslices(H) * att2::tiles(T) * att2::tiles(S) * att2::P *
+                                                   att2::P * 4);
+    if (att_tc_ok()) {  // bf16 alpha / dscores [B][T][S8] and dC [N_T][H] for the tcgen05 attention
+      att_a16 = carve<bf16>(cur, (long long)B * T * s8() * 2);
+      att_d16 = carve<bf16>(cur, (long long)B * T * s8() * 2);
+      att_dc16 = carve<bf16>(cur, NT * H * 2);
+    }
     cst_att = carve<char>(cur, NT * 2 * H * asz);
     ho = carve<float>(cur, NT * H * 4);
     hod = carve<char>(cur, NT * H * asz);
@@ -1531,14 +1596,21 @@ class Engine {
     const uint8_t* dx_keep;
     void* dUb;
   };
+  // BPTT cluster K-split: 4 CTAs per 64 units.  (A split of 8 halves each
+  // CTA's dU stream and doubles its TMA stages in flight, but only 15 clusters
+  // of 8 are co-resident on this B200 against the 16 a scan pair needs.)
+  static constexpr int BWD_KS = 4;
   template <int ROWS>
   bool bwd_multi_ok() const {
-    using F = mc::Bwd<ROWS>;
-    return bf && persistent && dual && H % mc::BWD_NU == 0 && (H / 64) % mc::BWD_KBOX == 0 && H / 64 <= 32 &&
-           (4 * H / 64) * ((B + ROWS - 1) / ROWS) <= FLAG_STRIDE && F::ctas(H, B) <= g_num_sms &&
-           F::stages(H) >= 2 && (size_t)F::stages(H) * F::STAGE >= F::xbuf_bytes();
+    using F = mc::Bwd<ROWS, BWD_KS>;
+    const int kbl = 4 * H / 64 / BWD_KS;
+    return bf && persistent && dual && H % mc::BWD_NU == 0 && (4 * H / 64) % BWD_KS == 0 &&
+           kbl % mc::BWD_KBOX == 0 && kbl <= 32 && (4 * H / 64) * ((B + ROWS - 1) / ROWS) <= FLAG_STRIDE &&
+           F::ctas(H, B) <= g_num_sms && F::stages(H) >= 2 && (size_t)F::stages(H) * F::STAGE >= F::xbuf_bytes();
   }
-  bool use_dual_bwd() const { return bwd_multi_ok<128>() && 2 * mc::Bwd<128>::ctas(H, B) <= g_num_sms; }
+  template <int ROWS>
+  int bwd_ctas() const { return mc::Bwd<ROWS, BWD_KS>::ctas(H, B); }
+  bool use_dual_bwd() const { return bwd_multi_ok<128>() && 2 * bwd_ctas<128>() <= g_num_sms; }
   // one scan over batch slices of ROWS rows (64: two halves of B<=128; 128: B<=256)
   int single_bwd_rows() const { return bwd_multi_ok<64>() ? 64 : bwd_multi_ok<128>() ? 128 : 0; }
   void bwd_single(const BwdScan& f, bool post = true) {
@@ -1546,7 +1618,7 @@ class Engine {
     else bwd_launch<128>(f, nullptr);
     if (post) bwd_post(f);
   }
-  template <int ROWS>
+  template <int ROWS, int KS>
   LstmBwdP bwd_params(const BwdScan& f, CUtensorMap* tmA, CUtensorMap* tmW) {
     const Layer& ly = layers[f.l];
     ScanViews v = views(f.l, f.reverse);
@@ -1560,31 +1632,31 @@ class Engine {
     prm.status = status_d;
     prm.steps = f.steps; prm.B = B; prm.H = H; prm.din = f.din; prm.reverse = f.reverse ? 1 : 0;
     prm.trace = (trace_layer == 100 + f.l) ? trace_d : nullptr;
-    prm.stages = mc::Bwd<ROWS>::stages(H);
+    prm.stages = mc::Bwd<ROWS, KS>::stages(H);
     return prm;
   }
-  template <int ROWS>
+  template <int ROWS, int KS = BWD_KS>
   void bwd_launch(const BwdScan& a, const BwdScan* b) {
     CUtensorMap tm[4];
     LstmBwdMulti m;
-    m.c[0] = bwd_params<ROWS>(a, &tm[0], &tm[1]);
-    if (b) m.c[1] = bwd_params<ROWS>(*b, &tm[2], &tm[3]);
+    m.c[0] = bwd_params<ROWS, KS>(a, &tm[0], &tm[1]);
+    if (b) m.c[1] = bwd_params<ROWS, KS>(*b, &tm[2], &tm[3]);
     else { m.c[1] = m.c[0]; tm[2] = tm[0]; tm[3] = tm[1]; }
-    const int g = mc::Bwd<ROWS>::ctas(H, B);
+    const int g = mc::Bwd<ROWS, KS>::ctas(H, B);
     m.split = g;
-    auto k = lstm_bwd_multi<ROWS>;
-    const size_t smem = mc::Bwd<ROWS>::smem(H);
+    auto k = lstm_bwd_multi<ROWS, KS>;
+    const size_t smem = mc::Bwd<ROWS, KS>::smem(H);
     CMT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t c = {};
     c.gridDim = dim3(b ? 2 * g : g);
-    c.blockDim = dim3(mc::BWD_THREADS);
+    c.blockDim = dim3(mc::Bwd<ROWS, KS>::THREADS);
     c.dynamicSmemBytes = smem;
     c.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = g_coop;
     at[1].id = cudaLaunchAttributeClusterDimension;
-    at[1].val.clusterDim.x = mc::BWD_KS;
+    at[1].val.clusterDim.x = KS;
     at[1].val.clusterDim.y = 1;
     at[1].val.clusterDim.z = 1;
     c.attrs = at;
@@ -1873,7 +1945,14 @@ class Engine {
     // attention (attention.py:146-173)
     copy_act(Ht, H, (char*)cst_att + (size_t)H * asz, 2LL * H, (int)NT, H);
     gemm((int)NT, H, H, Mat{Ht, H, 0}, Mat{wv(off_wa), H, 1}, store(u_att, H, true));
-    if (S <= att2::MAXL && T <= att2::MAXL && att_split == 2) {
+    if (att_tc_ok()) {
+      // tcgen05: scores = U Hs^T, masked softmax, C_s = alpha Hs (attention_tc.cuh)
+      att_tc_ts(u_att, att_dsc);
+      att_softmax_fwd_kernel<<<ceil_div(B * T, 8), 256, 0, st>>>(att_dsc, src_mask_d, S, T, B, s8(), alpha, att_a16,
+                                                                 status_d);
+      CMT_LAUNCHED(); tl_mark(st, "attn_tc_softmax");
+      att_tc_th(att_a16, cst_att, (long long)B * 2 * H, 2LL * H, 1);
+    } else if (S <= att2::MAXL && T <= att2::MAXL && att_split == 2) {
       const int nsp = att::nslices(H), tt = att2::tiles(T), ts = att2::tiles(S);
       dim3 gs(B, nsp, tt * ts), gc(B, ceil_div(H, att::HC), tt);
       if (bf) attn2_scores_part<bf16, bf16><<<gs, att::THREADS, 0, st>>>((const bf16*)u_att, H, (const bf16*)Hs, S, T, B,
@@ -2037,6 +2116,21 @@ class Engine {
     gemm((int)NT, 2 * H, H, Mat{dhpre, H, 0}, Mat{wv(off_wc), H, 0}, store(dcst, 2LL * H, false));
     // attention core backward
     float* dHs = (L == 1) ? dtop : lw[L].dy;
+    if (att_tc_ok()) {
+      // tcgen05 (attention_tc.cuh): dalpha = dC Hs^T, softmax backward,
+      // dU = dsc Hs, dHs = alpha^T dC + dsc^T U (every row of dHs written)
+      copy2d_kernel<float, bf16><<<grid_for(NT * H), 256, 0, st>>>(dcst, 2LL * H, att_dc16, H, (int)NT, H);
+      CMT_LAUNCHED(); tl_mark(st, "attn_tc_dc16");
+      att_tc_ts(att_dc16, att_dsc);
+      att_softmax_bwd_kernel<<<ceil_div(B * T, 8), 256, 0, st>>>(alpha, att_dsc, S, T, B, s8(), att_d16);
+      CMT_LAUNCHED(); tl_mark(st, "attn_tc_softmax_bwd");
+      att_tc_th(att_d16, du_att, (long long)B * H, H, 1);
+      const BatOp aT{att_a16, S, T, (long long)T * s8() * 2, s8() * 2LL, 2},
+          dT{att_d16, S, T, (long long)T * s8() * 2, s8() * 2LL, 2},
+          dcb{att_dc16, H, T, H * 2LL, (long long)B * H * 2, 1}, ub{u_att, H, T, H * 2LL, (long long)B * H * 2, 1};
+      bat_gemm<256, 1, 1>(S, H, T, B, aT, dcb, BatStore{dHs, (long long)B * H, H, 0, 0});
+      bat_gemm<256, 1, 1>(S, H, T, B, dT, ub, BatStore{dHs, (long long)B * H, H, 0, 1});
+    } else {
     CMT_CUDA(cudaMemsetAsync(dHs, 0, NS * H * 4, st));
     if (S <= att2::MAXL && T <= att2::MAXL && att_split == 2) {
       const int nsp = att::nslices(H), tt = att2::tiles(T), ts = att2::tiles(S);
@@ -2113,6 +2207,7 @@ class Engine {
       }
       CMT_LAUNCHED(); tl_mark(st, "attn_bwd_kernel");
       CMT_CUDA(cudaGetLastError());
+    }
     }
     // W_a (attention.py:166): dW_a and dH_t = du W_a^T + dC_st[:, H:]
     gemm(H, H, (int)NT, Mat{Ht, H, 1}, Mat{du_att, H, 1}, store(dg + off_wa, H, false));
@@ -2567,6 +2662,10 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
   return guard(e, [&] {
     std::string k(key);
     if (k == "time_dominant") e->eng->time_dominant = (int)value;
+    else if (k == "att_tc") {
+      if (e->eng->staged) throw Error(cmt::CMT_ERR_CONFIG, "set att_tc before staging a batch");
+      e->eng->att_tc = (int)value;
+    }
     else if (k == "persistent") e->eng->persistent = (int)value;
     else if (k == "cg2") e->eng->cg2 = (int)value;
     else if (k == "dual") e->eng->dual = (int)value;

@@ -275,41 +275,49 @@ __global__ void __launch_bounds__(mc::THREADS, 1)
 // enc.l1 bwd with enc.l1 fwd).  Reference: layers.py:366-395, 472-493.
 // ---------------------------------------------------------------------------
 namespace mc {
-constexpr int BWD_THREADS = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 cell epilogue
-constexpr int BWD_KS = 4;         // cluster size = K quarters of the 4H gate columns
 constexpr int BWD_NU = 64;        // units per cluster
 constexpr int BWD_UPT = 8;        // units per epilogue thread
 constexpr int BWD_KBOX = 2;       // k-blocks per TMA / stage
-inline size_t bwd_w_bytes(int H) { return (size_t)(H / 64) * BWD_NU * 128; }
 // ROWS = batch rows per CTA: 128 (paired scans) or 64 (one scan split over two
 // batch halves, 128 CTAs; the M=128 MMA reads a padding tile past the stage).
-template <int ROWS>
+// KS = cluster size = K slices of the 4H gate columns (4 or 8): each CTA holds
+// a (4H/KS) x 64-unit W_h slice and streams 1/KS of dU per step; a larger KS
+// halves both, leaving room for twice the TMA stages in flight, at the price
+// of more (smaller) partial sums in the exchange.
+template <int ROWS, int KS>
 struct Bwd {
+  static constexpr int UPC = BWD_NU / KS;          // units per CTA (16 or 8)
+  static constexpr int NG = UPC / BWD_UPT;         // 8-unit groups per CTA (2 or 1)
+  static constexpr int EPI_WARPS = 4 * NG;       // warp w: TMEM lane quarter w & 3, unit group (w - 4) >> 2
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;  // w0 TMA, w1 MMA, w2 TMEM, w3 idle, epilogue
   static constexpr int KBLK = ROWS * 128;  // [ROWS rows][64] bf16
   static constexpr int STAGE = BWD_KBOX * KBLK;
   static constexpr int PAD = ROWS < 128 ? KBLK : 0;
+  static constexpr int PROD = 16 / UPC;            // CTAs producing one 64-column k-block of dU
+  static size_t w_bytes(int H) { return (size_t)(4 * H / 64 / KS) * BWD_NU * 128; }
   static int stages(int H) {
-    long long room = (long long)SMEM_LIMIT - 1024 - 512 - PAD - (long long)bwd_w_bytes(H);
+    long long room = (long long)SMEM_LIMIT - 1024 - 512 - PAD - (long long)w_bytes(H);
     long long s = room / STAGE;
     return (int)(s > MAX_STAGES ? MAX_STAGES : s);
   }
-  static size_t smem(int H) { return 1024 + bwd_w_bytes(H) + (size_t)stages(H) * STAGE + PAD + 512; }
-  static int ctas(int H, int B) { return (H / BWD_NU) * BWD_KS * ((B + ROWS - 1) / ROWS); }
-  static size_t xbuf_bytes() { return (size_t)BWD_KS * 2 * ROWS * 32; }
+  static size_t smem(int H) { return 1024 + w_bytes(H) + (size_t)stages(H) * STAGE + PAD + 512; }
+  static int ctas(int H, int B) { return (H / BWD_NU) * KS * ((B + ROWS - 1) / ROWS); }
+  static size_t xbuf_bytes() { return (size_t)KS * NG * ROWS * 32; }
 };
 }  // namespace mc
 
 struct LstmBwdMulti {
   LstmBwdP c[2];
-  int split;  // multiple of BWD_KS
+  int split;  // multiple of the cluster size
 };
 
-template <int ROWS>
-__global__ void __launch_bounds__(mc::BWD_THREADS, 1)
+template <int ROWS, int KS>
+__global__ void __launch_bounds__(mc::Bwd<ROWS, KS>::THREADS, 1)
     lstm_bwd_multi(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmW0,
                    const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmW1,
                    const LstmBwdMulti m) {
-  using F = mc::Bwd<ROWS>;
+  using F = mc::Bwd<ROWS, KS>;
+  constexpr int UPC = F::UPC, NG = F::NG, EPI_WARPS = F::EPI_WARPS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int ch = (int)blockIdx.x >= m.split ? 1 : 0;
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
   const void* tmA = ch ? (const void*)&tmA1 : (const void*)&tmA0;
   const void* tmW = ch ? (const void*)&tmW1 : (const void*)&tmW0;
 
-  const int KBL = p.H / 64;  // k-blocks of this CTA's gate-column quarter
+  const int KBL = 4 * p.H / 64 / KS;  // k-blocks of this CTA's gate-column slice
   uint8_t* sW = smem;                                    // KBL x [64 units][64] (K-major)
   uint8_t* sA = smem + (size_t)KBL * (mc::BWD_NU * 128);  // stage ring; also the parked partials
   uint64_t* full = (uint64_t*)(sA + (size_t)p.stages * F::STAGE + F::PAD);
@@ -335,8 +343,8 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kq = (int)ptx::cluster_rank();
   const int nh = (p.B + ROWS - 1) / ROWS;
-  const int half = (bid / mc::BWD_KS) % nh;                  // batch half of this cluster
-  const int ug = (bid / mc::BWD_KS / nh) * mc::BWD_NU;       // cluster's first unit
+  const int half = (bid / KS) % nh;                  // batch half of this cluster
+  const int ug = (bid / KS / nh) * mc::BWD_NU;       // cluster's first unit
   const int r0 = half * ROWS;
   const int kb_base = kq * KBL;
   const int rounds = p.steps + (p.dh0 ? 1 : 0);
@@ -350,10 +358,10 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
     }
     ptx::mbar_init(wfull, 1);
     ptx::mbar_init(tfull, 1);
-    ptx::mbar_init(tempty, 8);
-    ptx::mbar_init(rfree, mc::BWD_KS - 1);
+    ptx::mbar_init(tempty, EPI_WARPS);
+    ptx::mbar_init(rfree, KS - 1);
     ptx::mbar_init(xfull, 1);  // my expect_tx; the partners' st.async bytes complete it
-    ptx::mbar_init(xdone, 8);  // the 8 epilogue warps
+    ptx::mbar_init(xdone, EPI_WARPS);  // the epilogue warps
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 64);
@@ -382,7 +390,7 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
       if (i >= 2) ptx::mbar_wait(xdone, (i - 2) & 1);
       if (p.trace && bid == 0 && lane == 0) p.trace[i * 8 + 0] = gtimer();
       const int arow = time_of(p.steps - i) * p.B + r0;
-      const unsigned target = (unsigned)i;
+      const unsigned target = (unsigned)(i * F::PROD);
       int issued = 0;
       SpinGuard guard;
       while (issued < nst) {
@@ -440,18 +448,18 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
-    const int uh = (warp - 4) >> 2;  // unit half of this CTA's 16 units
+    const int uh = (warp - 4) >> 2;  // 8-unit group of this CTA's units
     const int b = q * 32 + lane;               // row within this CTA's batch slice
     const bool inrow = b < ROWS;
     const bool valid = inrow && r0 + b < p.B;
     const long long gb = r0 + b;                // batch column
     const long long H = p.H;
-    const int u0 = ug + kq * 16 + uh * 8;  // my 8 units
+    const int u0 = ug + kq * UPC + uh * 8;  // my 8 units
     // partials parked in the receiver's stage ring: xbuf[sender][uh][row][8] floats
-    const uint32_t xslot = ptx::smem_u32(sA) + (uint32_t)((kq * 2 + uh) * ROWS + (inrow ? b : 0)) * 32;
-    uint32_t rx[mc::BWD_KS], rxf[mc::BWD_KS], rrf[mc::BWD_KS];
+    const uint32_t xslot = ptx::smem_u32(sA) + (uint32_t)((kq * NG + uh) * ROWS + (inrow ? b : 0)) * 32;
+    uint32_t rx[KS], rxf[KS], rrf[KS];
 #pragma unroll
-    for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
+    for (int pr_ = 0; pr_ < KS; ++pr_) {
       rx[pr_] = ptx::mapa(xslot, pr_);
       rxf[pr_] = ptx::mapa(ptx::smem_u32(xfull), pr_);
       rrf[pr_] = ptx::mapa(ptx::smem_u32(rfree), pr_);
@@ -490,22 +498,22 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
         if (p.trace && bid == 0 && threadIdx.x == 128) p.trace[i * 8 + 1] = gtimer();
         if (p.trace && bid < 8 && threadIdx.x == 128) p.trace[1024 + i * 8 + bid] = gtimer();
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-        float v[mc::BWD_KS][mc::BWD_UPT];
+        float v[KS][mc::BWD_UPT];
 #pragma unroll
-        for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) ptx::tmem_ld8(tl + pr_ * 16 + uh * 8, v[pr_]);
+        for (int pr_ = 0; pr_ < KS; ++pr_) ptx::tmem_ld8(tl + pr_ * UPC + uh * 8, v[pr_]);
         ptx::tmem_wait_ld();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(tempty);
         // my MMA is done: my ring may now receive the partners' partials
         if (threadIdx.x == 128) {
-          ptx::mbar_expect_tx(xfull, (mc::BWD_KS - 1) * 2 * ROWS * 32);
+          ptx::mbar_expect_tx(xfull, (KS - 1) * NG * ROWS * 32);
 #pragma unroll
-          for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_)
+          for (int pr_ = 0; pr_ < KS; ++pr_)
             if (pr_ != kq) ptx::mbar_arrive_remote_relaxed(rrf[pr_]);
         }
 #pragma unroll
-        for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_)
+        for (int pr_ = 0; pr_ < KS; ++pr_)
           if (pr_ == kq) {
 #pragma unroll
             for (int u = 0; u < mc::BWD_UPT; ++u) acc[u] = v[pr_][u];
@@ -513,16 +521,16 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
         // push each partner its 8 columns (async remote stores completing its xfull)
         ptx::mbar_wait_cluster(rfree, (i - 1) & 1);
 #pragma unroll
-        for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
+        for (int pr_ = 0; pr_ < KS; ++pr_) {
           if (pr_ == kq || !inrow) continue;
           ptx::st_async_v4(rx[pr_], v[pr_][0], v[pr_][1], v[pr_][2], v[pr_][3], rxf[pr_]);
           ptx::st_async_v4(rx[pr_] + 16, v[pr_][4], v[pr_][5], v[pr_][6], v[pr_][7], rxf[pr_]);
         }
         ptx::mbar_wait_cluster(xfull, (i - 1) & 1);
 #pragma unroll
-        for (int pr_ = 0; pr_ < mc::BWD_KS; ++pr_) {
+        for (int pr_ = 0; pr_ < KS; ++pr_) {
           if (pr_ == kq || !inrow) continue;
-          const float4* xr = (const float4*)(sA + ((pr_ * 2 + uh) * ROWS + b) * 32);
+          const float4* xr = (const float4*)(sA + ((pr_ * NG + uh) * ROWS + b) * 32);
           const float4 z0 = xr[0], z1 = xr[1];
           acc[0] += z0.x; acc[1] += z0.y; acc[2] += z0.z; acc[3] += z0.w;
           acc[4] += z1.x; acc[5] += z1.y; acc[6] += z1.z; acc[7] += z1.w;
@@ -574,10 +582,11 @@ __global__ void __launch_bounds__(mc::BWD_THREADS, 1)
         }
       }
       if (p.trace && bid == 0 && threadIdx.x == 128) p.trace[i * 8 + 3] = gtimer();
-      ptx::named_bar_sync(1, 256);
+      ptx::named_bar_sync(1, 32 * EPI_WARPS);
       if (threadIdx.x == 128) {
-        // my k-block (gate columns 4*(ug+16kq) ..) of this batch half
-        ptx::red_release_add(p.flag + ((ug + kq * 16) >> 4) * nh + half, 1u);
+        // my units' gate columns 4*(ug + UPC kq) .. lie in k-block (ug + UPC kq) / 16 of
+        // this batch half (shared by PROD = 16 / UPC CTAs)
+        ptx::red_release_add(p.flag + ((ug + kq * UPC) >> 4) * nh + half, 1u);
         if (p.trace && bid == 0) p.trace[i * 8 + 4] = gtimer();
       }
     }

@@ -272,10 +272,12 @@ def test_dp_path_single_rank_nccl_matches_plain(mode):
 
 
 @pytest.mark.parametrize("case", [(304, 64, 128, 2, 24, 17, 13, True), (256, 128, 256, 1, 8, 64, 64, False),
-                                  (256, 64, 128, 1, 12, 80, 72, True), (256, 64, 128, 1, 4, 128, 100, False)])
+                                  (256, 64, 128, 1, 12, 80, 72, True), (256, 64, 128, 1, 4, 128, 100, False),
+                                  (256, 64, 128, 1, 3, 200, 150, True)])
 def test_attention_variants_agree(case):
-    """Split attention kernels (many CTAs per sentence, default) against the
-    one-CTA-per-sentence tiled kernels and the oracle (bf16 step)."""
+    """The tcgen05 attention core (batched per-sentence GEMMs + softmax
+    kernels, the bf16 default for S <= 256) against the SIMT kernels (split
+    many-CTA, per-sentence tiled) and the oracle (bf16 step)."""
     from paper_1802_07170_b200.engine import Engine
     from paper_1802_07170_b200.model import Batch
     from tests.gpu_helpers import cfg_of
@@ -285,17 +287,23 @@ def test_attention_variants_agree(case):
     src, sm, tgt, tm = O.synthetic_batch(V, S, T, B, seed=8, ragged=ragged)
     _, _, og, _, _ = oracle_step(d, params, (src, sm, tgt, tm), 0.1, 1.0, 5.0, 3, update=False)
     out = {}
-    for split in (0, 1, 2):
+    variants = {"tc": dict(), "split2": dict(att_tc=0, att_split=2), "split1": dict(att_tc=0, att_split=1),
+                "tiled": dict(att_tc=0, att_split=0)}
+    if S > 128:  # beyond the SIMT kernels' tiles: the tcgen05 core alone against the oracle
+        variants = {"tc": dict()}
+    for name, opts in variants.items():
         eng = Engine(cfg_of(d), mode="bf16")
-        eng.set_option("att_split", split)
+        for k, v in opts.items():
+            eng.set_option(k, v)
         eng.upload(params)
         eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, np.random.Generator(np.random.PCG64(3)), update=False)
-        out[split] = eng.grads()
+        out[name] = eng.grads()
         eng.close()
-    for v in (1, 2):
+    for v in variants:
         for n in og:
-            assert O.norm_rel_err(out[v][n], out[0][n]) < 1e-3, (v, n)
             assert O.norm_rel_err(out[v][n], og[n]) < BF16_TOL, (v, n)
+            if v != "tc":
+                assert O.norm_rel_err(out[v][n], out["split2" if v != "split2" else "tiled"][n]) < 1e-3, (v, n)
 
 
 @pytest.mark.parametrize("mode,tol", [("fp32", FP32_TOL), ("bf16", BF16_TOL)])
