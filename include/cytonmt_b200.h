@@ -142,6 +142,15 @@ int cmt_wait(cmt_engine* e, cmt_step_result* res);
 /* data parallel: NCCL communicator from a 128-byte ncclUniqueId (from cmt_nccl_unique_id on rank 0).
    Grads, loss and status are summed over ranks inside every step; pass global_ntok in cmt_step_args. */
 int cmt_set_comm(cmt_engine* e, const void* nccl_unique_id, int rank, int world);
+/* data parallel, embedding rows: the ids (ascending) of table `table` (0 src,
+ * 1 tgt; one table when embeddings are shared) that the staged batch touches,
+ * *n of them (ids may be NULL to query the count); and, before cmt_run_step,
+ * the union of every rank's ids (ascending, unique).  The step all-reduces the
+ * embedding grads as rows of that union and updates only those rows (the
+ * reference's update touches every row, but rows outside the union have zero
+ * gradient: w - s*0 = w).  With one rank the union defaults to the rank's ids. */
+int cmt_staged_rows(cmt_engine* e, int table, int* ids, int cap, int* n);
+int cmt_set_union(cmt_engine* e, int table, const int* ids, int n);
 /* the rule that combines the ranks' status words inside a data-parallel step
  * (flag by flag: a flag is raised iff some rank raised it); host-only, no GPU */
 int cmt_status_combine(const int* words, int n);

@@ -38,6 +38,7 @@ EXPORTS = [
     "cmt_event_elapsed", "cmt_launch_count", "cmt_set_option", "cmt_get_stat", "cmt_debug_buffer", "cmt_test_gemm", "cmt_test_dropout", "cmt_timeline",
     "cmt_snapshot_save", "cmt_snapshot_restore", "cmt_snapshot_download", "cmt_snapshot_free",
     "cmt_beam_begin", "cmt_beam_step", "cmt_beam_result", "cmt_set_learnable", "cmt_status_combine",
+    "cmt_staged_rows", "cmt_set_union",
 ]
 
 
@@ -99,6 +100,8 @@ def load(path=LIB_PATH):
     lib.cmt_set_comm.argtypes = [VP, VP, I, I]
     lib.cmt_set_learnable.argtypes = [VP, I, I]
     lib.cmt_status_combine.argtypes = [P(I), I]
+    lib.cmt_staged_rows.argtypes = [VP, I, P(I), I, P(I)]
+    lib.cmt_set_union.argtypes = [VP, I, P(I), I]
     lib.cmt_nccl_unique_id.argtypes = [VP]
     lib.cmt_event_record.argtypes = [VP, I]
     lib.cmt_event_elapsed.argtypes = [VP, I, I, P(ctypes.c_float)]

@@ -13,6 +13,7 @@
 //   passes; embedding grads are row-compact (only touched rows exist).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_profiler_api.h>
 #include <dlfcn.h>
 #include <algorithm>
 #include <cmath>
@@ -512,7 +513,42 @@ class Engine {
   // data parallel (NCCL): dense all-reduce of grads, loss and status
   void* comm = nullptr;
   int rank = 0, world = 1;
-  float* demb[2] = {nullptr, nullptr};  // dense embedding grads (DP only)
+  // data parallel: the embedding grads are exchanged as rows of the UNION of all
+  // ranks' touched ids (cmt_set_union, computed by the host from every rank's
+  // staged ids): ubuf[t] [U][E] holds this rank's rows at their union index
+  // (zeros elsewhere) and is all-reduced; the norm and the update then run
+  // over the U union rows on every rank (identical results everywhere).
+  float* ubuf[2] = {nullptr, nullptr};
+  int *umap_d[2] = {nullptr, nullptr}, *uids_d[2] = {nullptr, nullptr};
+  size_t ucap[2] = {0, 0};
+  int nunion[2] = {0, 0};
+  bool union_set[2] = {false, false};
+  bool emb_sent[2] = {false, false};
+  void set_union(int t, const int* ids, int n) {
+    if (t < 0 || t >= n_tables) throw Error(CMT_ERR_SHAPE, "table index out of range");
+    if (!staged) throw Error(CMT_ERR_CONFIG, "stage the batch before setting its rows union");
+    std::vector<int> map((size_t)nuniq[t]);
+    int j = 0;
+    for (int i = 0; i < n; ++i) {
+      if (ids[i] < 0 || ids[i] >= V || (i && ids[i] <= ids[i - 1]))
+        throw Error(CMT_ERR_CONFIG, "rows union must be ascending unique ids in [0, V)");
+      if (j < nuniq[t] && uniq_h[t][j] == ids[i]) map[j++] = i;
+    }
+    if (j != nuniq[t]) throw Error(CMT_ERR_CONFIG, "rows union does not contain this rank's ids");
+    if ((size_t)n > ucap[t]) {
+      for (void* q : {(void*)ubuf[t], (void*)umap_d[t], (void*)uids_d[t]}) if (q) CMT_CUDA(cudaFree(q));
+      CMT_CUDA(cudaMalloc(&ubuf[t], (size_t)n * E * 4));
+      CMT_CUDA(cudaMalloc(&umap_d[t], (size_t)std::max(n, 1) * 4));  // >= this rank's rows
+      CMT_CUDA(cudaMalloc(&uids_d[t], (size_t)n * 4));
+      ucap[t] = n;
+    }
+    CMT_CUDA(cudaStreamSynchronize(st));
+    if (nuniq[t]) CMT_CUDA(cudaMemcpy(umap_d[t], map.data(), map.size() * 4, cudaMemcpyHostToDevice));
+    if (n) CMT_CUDA(cudaMemcpy(uids_d[t], ids, (size_t)n * 4, cudaMemcpyHostToDevice));
+    nunion[t] = n;
+    union_set[t] = true;
+  }
+
   void nccl_check(int r, const char* what) {
     if (r != 0)
       throw Error(CMT_ERR_CUDA, std::string(what) + ": " + (g_nccl.get_error ? g_nccl.get_error(r) : "nccl error"));
@@ -529,7 +565,6 @@ class Engine {
     nccl_check(init(&comm, world_, u, rank_), "ncclCommInitRank");
     rank = rank_;
     world = world_;
-    for (int t = 0; t < n_tables; ++t) CMT_CUDA(cudaMalloc(&demb[t], (size_t)V * E * 4));
     CMT_CUDA(cudaStreamCreateWithFlags(&stc, cudaStreamNonBlocking));
     for (auto& e : ev_ar) CMT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
@@ -626,7 +661,8 @@ class Engine {
     }
     beam_free();
     if (jump_d) cudaFree(jump_d);
-    for (int t = 0; t < 2; ++t) if (demb[t]) cudaFree(demb[t]);
+    for (int t = 0; t < 2; ++t)
+      for (void* q : {(void*)ubuf[t], (void*)umap_d[t], (void*)uids_d[t]}) if (q) cudaFree(q);
     if (comm && g_nccl.comm_destroy) g_nccl.comm_destroy(comm);
     if (stc) {
       cudaStreamDestroy(stc);
@@ -1285,6 +1321,7 @@ class Engine {
     }
     CMT_CUDA(cudaEventRecord(pin_ev[k], st));
     staged = true;
+    union_set[0] = union_set[1] = false;  // a new batch: its rows union comes with it
   }
 
   // ---- launch helpers ----
@@ -1374,8 +1411,10 @@ class Engine {
     dim3 blk(32, 8);
     dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, DROP4_DPT), 8));
     float scale = 1.0f / (float)(1.0 - cfg.dropout);
+    ncu_begin(8);
     dropout_fwd_kernel4<TI, TO><<<grid, blk, 0, st>>>((const TI*)x, (TO*)y, keep, N, H, pcg, jump_d, base,
                                                       dropout_threshold(cfg.dropout), scale, (const TI*)x2);
+    ncu_end();
     CMT_LAUNCHED(); tl_mark(st, "dropout_fwd_kernel4");
   }
 
@@ -1426,7 +1465,9 @@ class Engine {
     const Layer& ly = layers[f.l];
     EpiStore e = store(f.uxb, 4LL * H, false);
     e.bias = dw + ly.b_off;
+    ncu_begin(3);
     gemm(f.steps * B, 4 * H, f.din, Mat{f.X, f.din, 0}, Mat{wv(ly.w_off), 4LL * H, 1}, e);
+    ncu_end();
   }
   template <int ROWS>
   LstmFwdP fwd_params(const FwdScan& f, CUtensorMap* tmH, CUtensorMap* tmW) {
@@ -1679,7 +1720,9 @@ class Engine {
     ScanViews v = views(f.l, f.reverse);
     long long N = (long long)f.steps * B;
     // dW[0:din] = X^T dU, dW[din:] = Hprev^T dU  (layers.py:389-391, batched; K6)
+    ncu_begin(5);
     gemm(f.din, 4 * H, (int)N, Mat{f.X, f.din, 1}, Mat{f.dUb, 4LL * H, 1}, store(dg + ly.w_off, 4LL * H, false));
+    ncu_end();
     gemm(H, 4 * H, (int)N, Mat{v.hprev, H, 1}, Mat{f.dUb, 4LL * H, 1},
          store(dg + ly.w_off + (size_t)f.din * 4 * H, 4LL * H, false));
     colsum(f.dUb, true, N, 4 * H, dg + ly.b_off);
@@ -1692,7 +1735,9 @@ class Engine {
     EpiStore e = store(f.dX, f.din, false);
     e.beta = f.dx_beta;
     if (f.dx_keep) { e.dmask = f.dx_keep; e.ld_dmask = f.din; e.dscale = 1.0f / (float)(1.0 - cfg.dropout); }
+    ncu_begin(4);
     gemm((int)N, f.din, 4 * H, Mat{f.dUb, 4LL * H, 0}, Mat{wv(ly.w_off), 4LL * H, 0}, e);
+    ncu_end();
   }
 
   void scan_bwd(int l, const void* X, int din, int steps, bool reverse, const float* mask, const float* dy,
@@ -1788,9 +1833,43 @@ class Engine {
     else copy2d<float>(s, lds, d, ldd, rows, cols);
   }
 
+  // embedding grads of table t: deterministic segmented scatter of the dX rows
+  // (tensor.py:208-216; np.add.at order) into compact rows, and in data
+  // parallel the rows-union exchange (each table once per step)
+  void embed_grads(int t, bool dp) {
+    if (emb_sent[t]) return;
+    emb_sent[t] = true;
+    if (nuniq[t]) {
+      if (E % 4 == 0) {
+        ncu_begin(12);
+        scatter_compact_v4_kernel<<<nuniq[t], SCAT_THREADS, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t],
+                                                                       gcomp[t]);
+        ncu_end();
+        CMT_LAUNCHED(); tl_mark(st, "scatter_compact_v4_kernel");
+      } else {
+        scatter_compact_kernel<<<nuniq[t], 128, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t], gcomp[t]);
+        CMT_LAUNCHED(); tl_mark(st, "scatter_compact_kernel");
+      }
+    }
+    if (!dp) return;
+    if (!union_set[t]) {
+      if (world > 1) throw Error(CMT_ERR_CONFIG, "a data-parallel step needs the embedding rows union (cmt_set_union)");
+      set_union(t, uniq_h[t].data(), nuniq[t]);  // one rank: the union is its own rows
+    }
+    if (!nunion[t]) return;
+    CMT_CUDA(cudaMemsetAsync(ubuf[t], 0, (size_t)nunion[t] * E * 4, st));
+    if (nuniq[t]) {
+      scatter_rows_kernel<<<nuniq[t], 128, 0, st>>>(gcomp[t], E, umap_d[t], nuniq[t], ubuf[t]);
+      CMT_LAUNCHED(); tl_mark(st, "scatter_rows_kernel");
+    }
+    allreduce(ubuf[t], (size_t)nunion[t] * E, NCCL_FLOAT32);
+  }
+
   // ---- the step ----
   void run(const cmt_step_args& a, cmt_step_result* res) {
     if (!staged) throw Error(CMT_ERR_INTERNAL, "no batch staged");
+    const bool dp = comm != nullptr;  // (a 1-rank communicator exercises the same path)
+    emb_sent[0] = emb_sent[1] = false;
     const long long NS = (long long)S * B, NT = (long long)T * B, BH = (long long)B * H;
     const bool infer = (a.flags & CMT_FLAG_INFER) != 0;  // dev_entropy pass (training.py:162-182)
     const bool drop = cfg.dropout > 0.0 && !infer;        // INFER mode: dropout is the identity
@@ -1947,7 +2026,9 @@ class Engine {
     gemm((int)NT, H, H, Mat{Ht, H, 0}, Mat{wv(off_wa), H, 1}, store(u_att, H, true));
     if (att_tc_ok()) {
       // tcgen05: scores = U Hs^T, masked softmax, C_s = alpha Hs (attention_tc.cuh)
+      ncu_begin(9);
       att_tc_ts(u_att, att_dsc);
+      ncu_end();
       att_softmax_fwd_kernel<<<ceil_div(B * T, 8), 256, 0, st>>>(att_dsc, src_mask_d, S, T, B, s8(), alpha, att_a16,
                                                                  status_d);
       CMT_LAUNCHED(); tl_mark(st, "attn_tc_softmax");
@@ -2045,13 +2126,17 @@ class Engine {
     // fused log-softmax + smoothed CE + grad (training.py:96-120, tensor.py:146-151)
     const bool fused_ce = use_ce2() && cepart;
     if (fused_ce) {
+      ncu_begin(6);
       ce_stats_kernel<<<(int)NT, CES_THREADS, 0, st>>>((const bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon,
                                                        inv_ntok, cfg.output_tanh, losstok, status_d, cerow);
+      ncu_end();
       CMT_LAUNCHED(); tl_mark(st, "ce_stats_kernel");
       const int chunks = (int)ceil_div(NT, CEG_ROWS);
+      ncu_begin(7);
       ce_grad_kernel<<<dim3(ceil_div(V, CEG_COLS), chunks), CEG_THREADS, 0, st>>>((bf16*)Y, V, (int)NT, tgt_out_d,
                                                                                   cerow, (float)a.epsilon,
                                                                                   cfg.output_tanh, cepart);
+      ncu_end();
       CMT_LAUNCHED(); tl_mark(st, "ce_grad_kernel");
       colsum_final_kernel<<<ceil_div(V, 256), 256, 0, st>>>(cepart, chunks, V, dg + off_bo);
       CMT_LAUNCHED(); tl_mark(st, "colsum_final_kernel");
@@ -2088,7 +2173,9 @@ class Engine {
     if (ov_wo) {
       fork();
       on_side_stream([&]() {
+        ncu_begin(11);
         gemm(H, V, (int)NT, Mat{hin, H, 1}, Mat{Y, V, 1}, store(dg + off_wo, V, false));
+        ncu_end();
         if (!fused_ce) colsum(Y, true, NT, V, dg + off_bo);
         allreduce_region((int)layers.size() + 1);
       });
@@ -2264,6 +2351,9 @@ class Engine {
           bwd_post(e);
         }
       }
+      // the target table's rows are final once dec.l1's input grads are: in
+      // data parallel their exchange overlaps the enc.l1 scans
+      if (dp && n_tables == 2) embed_grads(1, dp);
       BwdScan b1 = l1_scan(true, dU), f1 = l1_scan(false, dU2);
       bwd_pair(b1, f1);
       if (use_overlap()) {
@@ -2286,34 +2376,14 @@ class Engine {
       single(l1_scan(true, dU));
       single(l1_scan(false, dU));
     }
-    // embedding grads: deterministic segmented scatter (tensor.py:208-216)
-    for (int t = 0; t < n_tables; ++t) {
-      if (nuniq[t] == 0) continue;
-      if (E % 4 == 0) {
-        scatter_compact_v4_kernel<<<nuniq[t], SCAT_THREADS, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t],
-                                                                       gcomp[t]);
-        CMT_LAUNCHED(); tl_mark(st, "scatter_compact_v4_kernel");
-      } else {
-        scatter_compact_kernel<<<nuniq[t], 128, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t], gcomp[t]);
-        CMT_LAUNCHED(); tl_mark(st, "scatter_compact_kernel");
-      }
-    }
+    for (int t = 0; t < n_tables; ++t) embed_grads(t, dp);
 
     // ===== data parallel: sum grads / loss / status over ranks (NCCL) =====
-    const bool dp = comm != nullptr;  // (a 1-rank communicator exercises the same path)
     if (dp) {
       if (ar_buckets) {
         for (int id = 0; id < (int)layers.size() + 2; ++id) allreduce_region(id);  // any not yet issued
       } else {
         allreduce(dg, dense_n, NCCL_FLOAT32);
-      }
-      for (int t = 0; t < n_tables; ++t) {
-        CMT_CUDA(cudaMemsetAsync(demb[t], 0, (size_t)V * E * 4, st));
-        if (nuniq[t]) {
-          scatter_rows_kernel<<<nuniq[t], 128, 0, st>>>(gcomp[t], E, uniq_d[t], nuniq[t], demb[t]);
-          CMT_LAUNCHED(); tl_mark(st, "scatter_rows_kernel");
-        }
-        allreduce(demb[t], (size_t)V * E, NCCL_FLOAT32);
       }
       allreduce(losssum_d, 1, NCCL_FLOAT64);
       // the status word is a set of flags: spread it one flag per int, take the
@@ -2333,9 +2403,10 @@ class Engine {
       nparts += NORM_BLOCKS;
     }
     for (int t = 0; t < n_tables; ++t) {
-      if (!table_learn[t] || (!dp && nuniq[t] == 0)) continue;
-      const float* gsrc = dp ? demb[t] : gcomp[t];
-      long long gn = dp ? (long long)V * E : (long long)nuniq[t] * E;
+      const int rows = dp ? nunion[t] : nuniq[t];
+      if (!table_learn[t] || rows == 0) continue;
+      const float* gsrc = dp ? ubuf[t] : gcomp[t];
+      long long gn = (long long)rows * E;
       sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(gsrc, gn, normpart + nparts, 15);
       CMT_LAUNCHED(); tl_mark(st, "sumsq_partial_kernel");
       nparts += NORM_BLOCKS;
@@ -2344,17 +2415,20 @@ class Engine {
     CMT_LAUNCHED(); tl_mark(st, "clip_scale_kernel");
     if (!(a.flags & CMT_FLAG_NO_UPDATE)) {
       for (const GradSeg& sg : segs) {
+        ncu_begin(10);
         sgd_dense_kernel<<<grid_for((long long)sg.n), 256, 0, st>>>(dw + sg.off, dg + sg.off,
                                                                     bf ? dsh + sg.off : nullptr, (long long)sg.n,
                                                                     s32_d, status_d, sg.lanes);
+        ncu_end();
         CMT_LAUNCHED(); tl_mark(st, "sgd_dense_kernel");
       }
       for (int t = 0; t < n_tables; ++t) {
         if (!table_learn[t]) continue;
-        if (dp) {  // union of all ranks' rows: dense update (zero rows are exact no-ops)
-          sgd_dense_kernel<<<grid_for((long long)V * E), 256, 0, st>>>(emb_w[t], demb[t], bf ? emb_sh[t] : nullptr,
-                                                                      (long long)V * E, s32_d, status_d, 15);
-          CMT_LAUNCHED(); tl_mark(st, "sgd_dense_kernel");
+        if (dp) {  // the union rows, identical on every rank
+          if (nunion[t] == 0) continue;
+          sgd_rows_kernel<<<nunion[t], 128, 0, st>>>(emb_w[t], bf ? emb_sh[t] : nullptr, E, uids_d[t], nunion[t],
+                                                      ubuf[t], s32_d, status_d);
+          CMT_LAUNCHED(); tl_mark(st, "sgd_rows_kernel");
           continue;
         }
         if (nuniq[t] == 0) continue;
@@ -2417,7 +2491,30 @@ class Engine {
   // probes (bench.py's roofline, timed inside the timed steps on the launching
   // stream): class 0 the logits GEMM, 1 the BPTT scan launches, 2 the forward scan launches
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> probe_ev[3];
+  // ncu_class >= 0: the first launch of that class runs inside
+  // cudaProfilerStart/Stop, so `ncu --profile-from-start off -c 1` captures it
+  // (scripts/ncu_step.py): 0 logits GEMM, 1 BPTT scan, 2 forward scan, 3 Ux GEMM,
+  // 4 dX GEMM, 5 dW GEMM, 6 ce_stats, 7 ce_grad, 8 dropout, 9 attention scores
+  // GEMM, 10 dense SGD, 11 dW_o GEMM, 12 embedding scatter
+  int ncu_class = -1, ncu_skip = 0;  // ncu_skip: launches of the class to pass over first
+  bool ncu_on = false, ncu_done = false;
+  void ncu_begin(int cls) {
+    if (cls != ncu_class || ncu_done) return;
+    if (ncu_skip > 0) {
+      --ncu_skip;
+      return;
+    }
+    CMT_CUDA(cudaProfilerStart());
+    ncu_on = true;
+  }
+  void ncu_end() {
+    if (!ncu_on) return;
+    CMT_CUDA(cudaProfilerStop());
+    ncu_on = false;
+    ncu_done = true;
+  }
   cudaEvent_t probe_begin(int cls) {
+    ncu_begin(cls);
     if (!((time_dominant >> cls) & 1)) return nullptr;
     cudaEvent_t e0;
     CMT_CUDA(cudaEventCreate(&e0));
@@ -2425,6 +2522,7 @@ class Engine {
     return e0;
   }
   void probe_end(int cls, cudaEvent_t e0) {
+    ncu_end();
     if (!e0) return;
     cudaEvent_t e1;
     CMT_CUDA(cudaEventCreate(&e1));
@@ -2561,6 +2659,20 @@ int cmt_set_learnable(cmt_engine* e, int idx, int learnable) {
   return guard(e, [&]() { e->eng->set_learnable(idx, learnable != 0); });
 }
 int cmt_status_combine(const int* words, int n) { return cmt::status_combine(words, n); }
+int cmt_staged_rows(cmt_engine* e, int table, int* ids, int cap, int* n) {
+  return guard(e, [&] {
+    cmt::Engine& g = *e->eng;
+    if (table < 0 || table >= g.n_tables) throw Error(cmt::CMT_ERR_SHAPE, "table index out of range");
+    *n = (int)g.uniq_h[table].size();
+    if (ids) {
+      if (cap < *n) throw Error(cmt::CMT_ERR_SHAPE, "id buffer too small");
+      std::memcpy(ids, g.uniq_h[table].data(), g.uniq_h[table].size() * 4);
+    }
+  });
+}
+int cmt_set_union(cmt_engine* e, int table, const int* ids, int n) {
+  return guard(e, [&] { e->eng->set_union(table, ids, n); });
+}
 int cmt_download_grad(cmt_engine* e, int idx, float* h, long long rows, long long cols) {
   return guard(e, [&] { e->eng->download(idx, h, rows, cols, true); });
 }
@@ -2662,7 +2774,11 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
   return guard(e, [&] {
     std::string k(key);
     if (k == "time_dominant") e->eng->time_dominant = (int)value;
-    else if (k == "att_tc") {
+    else if (k == "ncu_skip") e->eng->ncu_skip = (int)value;
+    else if (k == "ncu_class") {
+      e->eng->ncu_class = (int)value;
+      e->eng->ncu_done = false;
+    } else if (k == "att_tc") {
       if (e->eng->staged) throw Error(cmt::CMT_ERR_CONFIG, "set att_tc before staging a batch");
       e->eng->att_tc = (int)value;
     }

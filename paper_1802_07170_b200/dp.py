@@ -9,7 +9,11 @@ of shard gradients equal the reference gradient of the concatenated batch:
   the batch's token count), and
 * the engine all-reduces (NCCL, sum) the dense gradients, the loss sum and the
   error status inside the step, before the global-norm clip and the update,
-  so every rank applies the identical update (training.py:123-142).
+  so every rank applies the identical update (training.py:123-142);
+* the embedding gradients are row-sparse: each rank stages only the rows its
+  shard touches, the ranks agree on the union of those ids on the host
+  (``exchange_rows``, before the step) and the engine all-reduces and updates
+  just the union rows (rows outside it have zero gradient in every rank).
 
 Dropout draws are per rank (each rank's own PCG64 stream); the single-process
 reference equality holds at dropout 0.
@@ -61,3 +65,31 @@ def attach(engine, dist, rank, world):
         dist.broadcast_object_list(obj, src=0)
     uid = ctypes.create_string_buffer(obj[0], 128)
     engine._check(engine.lib.cmt_set_comm(engine.h, uid, rank, world))
+
+
+def union_rows(id_lists):
+    """Ascending union of several ascending id arrays (the rows any rank touches)."""
+    if not id_lists:
+        return np.empty(0, dtype=np.int32)
+    return np.unique(np.concatenate([np.asarray(x, dtype=np.int32) for x in id_lists])).astype(np.int32)
+
+
+def gather_ids(ids, dist):
+    """All ranks' id arrays (variable lengths) via torch.distributed all_gather."""
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    n = torch.tensor([len(ids)], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros_like(n) for _ in range(dist.get_world_size())]
+    dist.all_gather(sizes, n)
+    mx = int(max(int(x.item()) for x in sizes))
+    buf = torch.full((max(mx, 1),), -1, dtype=torch.int32, device=dev)
+    buf[:len(ids)] = torch.as_tensor(np.asarray(ids, dtype=np.int32), device=dev)
+    out = [torch.empty_like(buf) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, buf)
+    return [o[:int(s.item())].cpu().numpy() for o, s in zip(out, sizes)]
+
+
+def exchange_rows(engine, dist):
+    """Give the engine the union of every rank's staged embedding rows (per table)."""
+    for t in range(engine.n_tables):
+        engine.set_union(t, union_rows(gather_ids(engine.staged_rows(t), dist)))

@@ -256,6 +256,9 @@ class Engine:
         src, tgt = batch.src_ids, batch.tgt_ids
         try:
             self.stage(src, batch.src_mask, tgt, batch.tgt_mask)
+            if getattr(self, "_dp", None) is not None:
+                from . import dp
+                dp.exchange_rows(self, self._dp)
         except ConfigError as e:
             # the reference raises the empty-target ConfigError after its forward
             # pass, so the dropout draws are consumed (training.py:149-153)
@@ -372,6 +375,26 @@ class Engine:
     def set_dp(self, dist, rank, world):
         from . import dp
         dp.attach(self, dist, rank, world)
+        self._dp = dist if world > 1 else None
+
+    @property
+    def n_tables(self):
+        return 1 if self.config.shared_embeddings else 2
+
+    def staged_rows(self, table):
+        """Ascending ids of embedding table ``table`` the staged batch touches."""
+        n = ctypes.c_int()
+        self._check(self.lib.cmt_staged_rows(self.h, int(table), None, 0, ctypes.byref(n)))
+        out = np.empty(n.value, dtype=np.int32)
+        self._check(self.lib.cmt_staged_rows(self.h, int(table), out.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                             n.value, ctypes.byref(n)))
+        return out
+
+    def set_union(self, table, ids):
+        """Rows union (ascending ids over all ranks) of table ``table`` for the next step."""
+        u = np.ascontiguousarray(ids, dtype=np.int32)
+        self._check(self.lib.cmt_set_union(self.h, int(table), u.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                           int(u.size)))
 
     # ---- timing ----
     def set_option(self, key, value):

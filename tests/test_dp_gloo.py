@@ -102,3 +102,39 @@ def test_shard_columns_and_errors():
     with pytest.raises(ValueError):
         dp.shard_columns([a], 0, 3)
     assert dp.global_ntok(np.ones((3, 2), np.float32)) == 6.0
+
+
+def _rows_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_1802_07170_b200 import dp
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        # each rank's staged rows: the ascending unique ids of its shard (the
+        # engine's cmt_staged_rows), different lengths per rank
+        src, sm, tgt, tm = dp.shard_columns(_batch(), rank, world)
+        mine = np.unique(src[sm > 0]).astype(np.int32) if rank == 0 else np.array([0, 5, 52], np.int32)
+        got = dp.union_rows(dp.gather_ids(mine, dist))
+        q.put((rank, mine, got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dp_rows_union_exchange_two_ranks():
+    """dp.exchange_rows' host side (gather_ids + union_rows) on a real 2-rank
+    gloo group: every rank obtains the same ascending union of all ranks'
+    staged embedding rows (what the engine all-reduces and updates)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rows_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    expect = np.unique(np.concatenate([res[0][1], res[1][1]]))
+    for r in res:
+        assert r[2].dtype == np.int32 and np.array_equal(r[2], expect)
+    assert np.all(np.diff(expect) > 0)
