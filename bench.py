@@ -37,6 +37,9 @@ CONFIGS = {
 }
 METRIC = "train target tokens/sec (fwd+bwd+update)"
 CPU_SAMPLE_B = 16  # sentences per CPU-baseline step (bounded sample of the B=128 batch)
+# the real reference (minmt.training.train_step) on the FULL c3 batch, measured
+# in the survey container (8-core Xeon, numpy/OpenBLAS): BASELINE.md §2.2
+REF_FULL = "163-180 tgt tok/s: minmt.train_step itself, full c3 batch (B=128, S=T=50), 8 cores, BASELINE.md 2.2"
 
 
 def flops_per_step(V, E, H, L, B, S, T):
@@ -211,12 +214,16 @@ def run_reference(args, cfg_t):
     sample = f"{CPU_SAMPLE_B} of {B} sentences (S=T={S}) per step, {args.steps} steps after {args.warmup} warm-up"
     out = {
         "metric": METRIC, "value": rate, "unit": "tgt_tok/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times) * B / CPU_SAMPLE_B,
+        # the measured step of the sample (what the timed loop ran); the full
+        # c3 batch would take B / sample times longer
+        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+        "ms_per_step_full_batch_est": 1e3 * statistics.median(times) * B / CPU_SAMPLE_B,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": args.config, "vocab": V, "emb": E, "hidden": H, "depth": L, "batch": B,
                    "src_len": S, "tgt_len": T},
-        "cpu_baseline": {"value": rate, "unit": "tgt_tok/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": rate, "unit": "tgt_tok/s", "cores": cores, "kind": "port", "sample": sample,
+                         "reference_full_batch": REF_FULL},
         "e2e": {"value": rate, "unit": "tgt_tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -412,7 +419,8 @@ def main():
         rate, times = cpu_oracle_rate(cfg_t, params, 2, 0)
         out["cpu_baseline"] = {"value": rate, "unit": "tgt_tok/s", "cores": os.cpu_count(), "kind": "port",
                                "sample": f"numpy oracle, {CPU_SAMPLE_B} of {B} sentences (S=T={S}), "
-                                         f"median of 2 steps ({sum(times):.1f} s)"}
+                                         f"median of 2 steps ({sum(times):.1f} s)",
+                               "reference_full_batch": REF_FULL if args.config == "c3" else None}
     print(json.dumps(out), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -383,6 +383,7 @@ class Engine {
   float* cepart = nullptr;  // per-CTA dY column sums of the fused CE kernel
   float2* cerow = nullptr;  // per-token (lse * log2e, mask / ntok) between the two CE passes
   float* colpart2 = nullptr;  // column-sum scratch of the side stream
+  unsigned *colticket = nullptr, *colticket2 = nullptr;  // colsum_partial_v8 tickets (self-resetting)
   float* dho32 = nullptr;   // fp32 split-K scratch of dH_o (bf16 mode)
   float *att_part = nullptr, *att_dsc = nullptr;  // split attention: score slices, d scores
   bf16 *att_a16 = nullptr, *att_d16 = nullptr, *att_dc16 = nullptr;
@@ -1193,6 +1194,9 @@ class Engine {
     long long colmax = std::max<long long>(V, 4LL * H);
     colpart = carve<float>(cur, 64 * colmax * 4);
     colpart2 = carve<float>(cur, 64 * colmax * 4);
+    colticket = carve<unsigned>(cur, 2 * 1024 * 4);
+    colticket2 = colticket + 1024;
+    if (base) CMT_CUDA(cudaMemsetAsync(colticket, 0, 2 * 1024 * 4, st));
     cepart = use_ce2() ? carve<float>(cur, std::max<long long>(g_num_sms, ceil_div(NT, CEG_ROWS)) * V * 4) : nullptr;
     cerow = carve<float2>(cur, (size_t)NT * 8);
     for (int t = 0; t < 2; ++t) {
@@ -1812,12 +1816,21 @@ class Engine {
 
   void colsum(const void* D, bool is_act, long long rows, int cols, float* out) {
     float* colpart = on_side ? colpart2 : this->colpart;
+    unsigned* ticket = on_side ? colticket2 : colticket;
     int chunks = (int)std::min<long long>(64, std::max<long long>(1, rows / 64));
     int rows_per = ceil_div(rows, chunks);
     chunks = ceil_div(rows, rows_per);
-    dim3 grid(ceil_div(cols, 256), chunks);
-    if (is_act && bf) colsum_partial_kernel<bf16><<<grid, 256, 0, st>>>((const bf16*)D, cols, (int)rows, cols, rows_per, colpart);
-    else colsum_partial_kernel<float><<<grid, 256, 0, st>>>((const float*)D, cols, (int)rows, cols, rows_per, colpart);
+    if (is_act && bf && cols % 8 == 0 && ceil_div(cols, 256) <= 1024) {  // 16-byte rows, fused final sum
+      dim3 grid(ceil_div(cols, 256), chunks);
+      colsum_partial_v8_kernel<<<grid, dim3(32, 8), 0, st>>>((const bf16*)D, cols, (int)rows, cols, rows_per, colpart,
+                                                             ticket, out);
+      CMT_LAUNCHED(); tl_mark(st, "colsum_v8_kernel");
+      return;
+    } else {
+      dim3 grid(ceil_div(cols, 256), chunks);
+      if (is_act && bf) colsum_partial_kernel<bf16><<<grid, 256, 0, st>>>((const bf16*)D, cols, (int)rows, cols, rows_per, colpart);
+      else colsum_partial_kernel<float><<<grid, 256, 0, st>>>((const float*)D, cols, (int)rows, cols, rows_per, colpart);
+    }
     CMT_LAUNCHED(); tl_mark(st, "colsum_partial_kernel");
     colsum_final_kernel<<<ceil_div(cols, 256), 256, 0, st>>>(colpart, chunks, cols, out);
     CMT_LAUNCHED(); tl_mark(st, "colsum_final_kernel");
@@ -2140,11 +2153,13 @@ class Engine {
       CMT_LAUNCHED(); tl_mark(st, "ce_grad_kernel");
       colsum_final_kernel<<<ceil_div(V, 256), 256, 0, st>>>(cepart, chunks, V, dg + off_bo);
       CMT_LAUNCHED(); tl_mark(st, "colsum_final_kernel");
-    } else if (bf) ce_kernel<bf16><<<(int)NT, CE_THREADS, 0, st>>>((bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon, inv_ntok,
-                                                           cfg.output_tanh, losstok, status_d);
-    else ce_kernel<float><<<(int)NT, CE_THREADS, 0, st>>>((float*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon, inv_ntok,
-                                                         cfg.output_tanh, losstok, status_d);
-    CMT_LAUNCHED(); tl_mark(st, "ce_kernel");
+    } else {
+      if (bf) ce_kernel<bf16><<<(int)NT, CE_THREADS, 0, st>>>((bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon,
+                                                              inv_ntok, cfg.output_tanh, losstok, status_d);
+      else ce_kernel<float><<<(int)NT, CE_THREADS, 0, st>>>((float*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon,
+                                                            inv_ntok, cfg.output_tanh, losstok, status_d);
+      CMT_LAUNCHED(); tl_mark(st, "ce_kernel");
+    }
     sum_to_double_kernel<<<1, 1024, 0, st>>>(losstok, (int)NT, losssum_d);
     CMT_LAUNCHED(); tl_mark(st, "sum_to_double_kernel");
 

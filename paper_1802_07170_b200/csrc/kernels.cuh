@@ -265,7 +265,10 @@ inline unsigned long long dropout_threshold(double p) { return (unsigned long lo
 // against the constant PCG64 multiplier (one umulhi, three low products, one
 // carry), the keep test on the state halves directly, and the element index
 // advanced incrementally: about half the instructions per draw.
-constexpr int DROP4_DPT = 32;
+#ifndef CMT_DROP_DPT
+#define CMT_DROP_DPT 64
+#endif
+constexpr int DROP4_DPT = CMT_DROP_DPT;  // draws per thread: one jump-ahead amortised over them
 template <typename TI, typename TO>
 __global__ void dropout_fwd_kernel4(const TI* __restrict__ x, TO* __restrict__ y, uint8_t* __restrict__ keep, int N,
                                     int H, Pcg pcg, const PcgJump* __restrict__ jt, unsigned long long base,
@@ -719,6 +722,70 @@ __global__ void colsum_partial_kernel(const T* __restrict__ D, long long ld, int
   }
   for (; r < r1; ++r) a[0] += to_f<T>(D[(long long)r * ld + c]);
   part[(long long)blockIdx.y * cols + c] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+}
+// bf16 rows: a CTA covers 256 columns (threadIdx.x: 8 columns via 16-byte
+// loads, a warp reads 512 contiguous bytes of a row) and 8 row lanes
+// (threadIdx.y: rows r0 + y, r0 + y + 8, ...; 2 rows in flight); the 8 lanes'
+// sums are combined in shared memory in lane order, so the partial of a chunk
+// is deterministic.
+// The last CTA of a column block to finish (a self-resetting ticket per column
+// block) adds the chunks' partials in chunk order and writes out[col]: one
+// launch, deterministic.
+__global__ void __launch_bounds__(256) colsum_partial_v8_kernel(const bf16* __restrict__ D, long long ld, int rows,
+                                                                int cols, int rows_per, float* __restrict__ part,
+                                                                unsigned* __restrict__ ticket, float* __restrict__ out) {
+  __shared__ float red[8][256 + 4];
+  const int cx = threadIdx.x * 8, c = blockIdx.x * 256 + cx;
+  const int r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
+  float a[2][8];
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[k][j] = 0.f;
+  if (c < cols) {
+    int r = r0 + threadIdx.y;
+    for (; r + 8 < r1; r += 16) {
+      const uint4 q0 = __ldcs((const uint4*)(D + (long long)r * ld + c));
+      const uint4 q1 = __ldcs((const uint4*)(D + (long long)(r + 8) * ld + c));
+      const bf16* e0 = (const bf16*)&q0;
+      const bf16* e1 = (const bf16*)&q1;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        a[0][j] += __bfloat162float(e0[j]);
+        a[1][j] += __bfloat162float(e1[j]);
+      }
+    }
+    if (r < r1) {
+      const uint4 q0 = __ldcs((const uint4*)(D + (long long)r * ld + c));
+      const bf16* e0 = (const bf16*)&q0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[0][j] += __bfloat162float(e0[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[threadIdx.y][cx + j] = a[0][j] + a[1][j];
+  __syncthreads();
+  // 256 threads, one column each: sum the 8 row lanes in order
+  const int t = threadIdx.y * 32 + threadIdx.x, col = blockIdx.x * 256 + t;
+  if (col < cols) {
+    float o = 0.f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) o += red[y][t];
+    part[(long long)blockIdx.y * cols + col] = o;
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ bool last;
+  if (t == 0) last = atomicAdd(ticket + blockIdx.x, 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (col < cols) {
+    float a = 0.f;
+    for (int k = 0; k < (int)gridDim.y; ++k) a += __ldcg(part + (long long)k * cols + col);
+    out[col] = a;
+  }
+  if (t == 0) ticket[blockIdx.x] = 0;  // ready for the next launch
 }
 __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, int cols, float* __restrict__ out) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
