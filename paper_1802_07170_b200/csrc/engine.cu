@@ -345,6 +345,13 @@ class Engine {
   int n_ev_ar = 0;
   int ar_overlap = 1;  // option: bucketed all-reduce overlapped with the backward (0: one all-reduce at the end)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // background stream: the first columns of a BPTT level's weight grads run
+  // here, grid-capped to the SMs the next level's scans leave idle
+  cudaStream_t stb = nullptr;
+  cudaEvent_t ev_bg = nullptr, ev_bgj = nullptr;
+  bool bg_pending = false;
+  int bwd_bg = 25;  // option (A/B: 0 9.556, 15 9.531, 25 9.457, 30 9.466, 40 9.68 ms/step at c3): percent of a BPTT level's dW columns computed beside the next scan (0: off)
+  std::vector<void*> dUl;  // per-layer dU buffers while the split is on (a deferred GEMM still reads its level's dU)
   int overlap = 1;      // option
   bool on_side = false;
   cudaEvent_t ev[16];
@@ -638,6 +645,9 @@ class Engine {
     asz = bf ? 2 : 4;
     CMT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     CMT_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+    CMT_CUDA(cudaStreamCreateWithFlags(&stb, cudaStreamNonBlocking));
+    CMT_CUDA(cudaEventCreateWithFlags(&ev_bg, cudaEventDisableTiming));
+    CMT_CUDA(cudaEventCreateWithFlags(&ev_bgj, cudaEventDisableTiming));
     CMT_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     CMT_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     for (auto& e : pin_ev) CMT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -672,6 +682,9 @@ class Engine {
     for (auto& e : ev) cudaEventDestroy(e);
     cudaStreamDestroy(st);
     cudaStreamDestroy(st2);
+    cudaStreamDestroy(stb);
+    cudaEventDestroy(ev_bg);
+    cudaEventDestroy(ev_bgj);
     cudaEventDestroy(ev_fork);
     cudaEventDestroy(ev_join);
     for (auto& e : pin_ev) cudaEventDestroy(e);
@@ -1153,6 +1166,9 @@ class Engine {
     ux3 = carve<float>(cur, NT * 4 * H * 4);  // dec.l1 input projection, computed early (see run())
     dU = carve<char>(cur, Nmax * 4 * H * asz);
     dU2 = carve<char>(cur, Nmax * 4 * H * asz);
+    dUl.assign(layers.size(), nullptr);
+    if (bwd_split_mem())
+      for (size_t l = 0; l < layers.size(); ++l) dUl[l] = carve<char>(cur, (long long)(l <= (size_t)L ? NS : NT) * 4 * H * asz);
     drop_enc.assign(L + 1, nullptr); keep_enc.assign(L + 1, nullptr);
     drop_dec.assign(L + 1, nullptr); keep_dec.assign(L + 1, nullptr);
     for (int k = 2; k <= L; ++k) {
@@ -1714,21 +1730,62 @@ class Engine {
   }
   void bwd_pair(const BwdScan& a, const BwdScan& b) { bwd_launch<128>(a, &b); }
   // weight grads, bias grads and input grads of a finished BPTT scan
-  void bwd_post(const BwdScan& f) {
-    bwd_post_w(f);
+  void bwd_post(const BwdScan& f, int c0 = 0) {
+    bwd_post_w(f, c0);
     if (f.dX) bwd_post_dx(f);
   }
   // weight and bias grads of a finished BPTT scan
-  void bwd_post_w(const BwdScan& f) {
+  // dW[0:din] = X^T dU, dW[din:] = Hprev^T dU  (layers.py:389-391, batched; K6),
+  // gate columns [c0, c1) of both halves
+  void bwd_dw_cols(const BwdScan& f, int c0, int c1) {
+    if (c1 <= c0) return;
     const Layer& ly = layers[f.l];
     ScanViews v = views(f.l, f.reverse);
-    long long N = (long long)f.steps * B;
-    // dW[0:din] = X^T dU, dW[din:] = Hprev^T dU  (layers.py:389-391, batched; K6)
+    const long long N = (long long)f.steps * B;
+    const void* du = (const char*)f.dUb + (size_t)c0 * asz;
     ncu_begin(5);
-    gemm(f.din, 4 * H, (int)N, Mat{f.X, f.din, 1}, Mat{f.dUb, 4LL * H, 1}, store(dg + ly.w_off, 4LL * H, false));
+    gemm(f.din, c1 - c0, (int)N, Mat{f.X, f.din, 1}, Mat{du, 4LL * H, 1}, store(dg + ly.w_off + c0, 4LL * H, false));
     ncu_end();
-    gemm(H, 4 * H, (int)N, Mat{v.hprev, H, 1}, Mat{f.dUb, 4LL * H, 1},
-         store(dg + ly.w_off + (size_t)f.din * 4 * H, 4LL * H, false));
+    gemm(H, c1 - c0, (int)N, Mat{v.hprev, H, 1}, Mat{du, 4LL * H, 1},
+         store(dg + ly.w_off + (size_t)f.din * 4 * H + c0, 4LL * H, false));
+  }
+  // the BPTT weight-gradient split: the first bg_cols() gate columns of a
+  // level's dW run on the background stream beside the NEXT level's scans (on
+  // the SMs those leave idle), the rest here at full width.  Off in data
+  // parallel (the gradient buckets are all-reduced as levels finish) and in
+  // the single-stream timeline.
+  bool bwd_split_mem() const { return bf && bwd_bg > 0 && comm == nullptr && use_dual_bwd(); }
+  bool bwd_split_ok() const { return bwd_split_mem() && !g_tl.on && !dUl.empty() && dUl[0] != nullptr; }
+  int bg_cols() const { return bwd_split_ok() ? (4 * H * bwd_bg / 100) / 256 * 256 : 0; }
+  int idle_sms() const { return g_num_sms - 2 * bwd_ctas<128>(); }
+  void bwd_dw_bg(const BwdScan& f) {  // issue this level's deferred columns on the background stream
+    const int nb = bg_cols();
+    if (!nb || idle_sms() < 8) return;
+    CMT_CUDA(cudaEventRecord(ev_bg, st));
+    CMT_CUDA(cudaStreamWaitEvent(stb, ev_bg, 0));
+    std::swap(st, stb);
+    g_grid_cap = idle_sms() / 2 * 2;
+    try {
+      bwd_dw_cols(f, 0, nb);
+    } catch (...) {
+      std::swap(st, stb);
+      g_grid_cap = 0;
+      throw;
+    }
+    std::swap(st, stb);
+    g_grid_cap = 0;
+    bg_pending = true;
+  }
+  void bg_join() {
+    if (!bg_pending) return;
+    CMT_CUDA(cudaEventRecord(ev_bgj, stb));
+    CMT_CUDA(cudaStreamWaitEvent(st, ev_bgj, 0));
+    bg_pending = false;
+  }
+  void bwd_post_w(const BwdScan& f, int c0 = 0) {
+    const Layer& ly = layers[f.l];
+    long long N = (long long)f.steps * B;
+    bwd_dw_cols(f, c0, 4 * H);
     colsum(f.dUb, true, N, 4 * H, dg + ly.b_off);
     allreduce_region(f.l);
   }
@@ -2351,25 +2408,35 @@ class Engine {
                f.dx_beta, f.dx_keep);
     };
     if (use_dual_bwd()) {
-      // pairs of independent scans: dL alone, then (d(k), e(k+1)) for k = L-1..1, then (e1 bwd, e1 fwd)
-      single(dec_scan(L, dU));
+      // pairs of independent scans: dL alone, then (d(k), e(k+1)) for k = L-1..1, then (e1 bwd, e1 fwd);
+      // with the dW split, each level's scans write their own dU (the deferred
+      // columns are read while the next level runs) and every level but the
+      // last leaves its first bg_cols() dW columns to the background stream
+      const int nb = bg_cols();
+      auto dub = [&](int l, void* fb) { return nb ? dUl[l] : fb; };
+      BwdScan dl = dec_scan(L, dub(2 * L, dU));
+      bwd_single(dl, false);
+      bwd_post(dl, nb);
+      bwd_dw_bg(dl);
       for (int k = L - 1; k >= 1; --k) {
-        BwdScan d = dec_scan(k, dU), e = enc_scan(k + 1, dU2);
+        BwdScan d = dec_scan(k, dub(L + k, dU)), e = enc_scan(k + 1, dub(k + 1, dU2));
         bwd_pair(d, e);
         if (use_overlap()) {  // disjoint outputs: the encoder scan's GEMMs on the side stream
           fork();
-          bwd_post(d);
-          on_side_stream([&]() { bwd_post(e); });
+          bwd_post(d, nb);
+          on_side_stream([&]() { bwd_post(e, nb); });
           join();
         } else {
-          bwd_post(d);
-          bwd_post(e);
+          bwd_post(d, nb);
+          bwd_post(e, nb);
         }
+        bwd_dw_bg(d);
+        bwd_dw_bg(e);
       }
       // the target table's rows are final once dec.l1's input grads are: in
       // data parallel their exchange overlaps the enc.l1 scans
       if (dp && n_tables == 2) embed_grads(1, dp);
-      BwdScan b1 = l1_scan(true, dU), f1 = l1_scan(false, dU2);
+      BwdScan b1 = l1_scan(true, dub(1, dU)), f1 = l1_scan(false, dub(0, dU2));
       bwd_pair(b1, f1);
       if (use_overlap()) {
         // weight grads of both directions overlap; the two dX GEMMs stay ordered
@@ -2392,6 +2459,7 @@ class Engine {
       single(l1_scan(false, dU));
     }
     for (int t = 0; t < n_tables; ++t) embed_grads(t, dp);
+    bg_join();  // the deferred weight-gradient columns, before the norm
 
     // ===== data parallel: sum grads / loss / status over ranks (NCCL) =====
     if (dp) {
@@ -2790,6 +2858,10 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     std::string k(key);
     if (k == "time_dominant") e->eng->time_dominant = (int)value;
     else if (k == "ncu_skip") e->eng->ncu_skip = (int)value;
+    else if (k == "bwd_bg") {
+      if (e->eng->staged) throw Error(cmt::CMT_ERR_CONFIG, "set bwd_bg before staging a batch");
+      e->eng->bwd_bg = (int)value;
+    }
     else if (k == "ncu_class") {
       e->eng->ncu_class = (int)value;
       e->eng->ncu_done = false;

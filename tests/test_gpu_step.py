@@ -227,6 +227,7 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
         "single": dict(dual=0),  # every scan alone: lstm_fwd_multi<64|128> / lstm_bwd_multi<64|128>
         "dual": dict(),  # default: paired forward scans in lstm_fwd_tm, paired BPTT in lstm_bwd_multi<128>
         "dual_multi": dict(fwd_tm=0),  # paired forward scans in lstm_fwd_multi<128>
+        "no_bg": dict(bwd_bg=0),  # every BPTT weight-gradient column on the main streams
     }
     for variant, opts in variants.items():
         eng = Engine(cfg_of(d), mode="bf16")
@@ -236,7 +237,7 @@ def test_persistent_recurrence_matches_per_step_and_oracle(case):
         eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, np.random.Generator(np.random.PCG64(3)), update=False)
         out[variant] = eng.grads()
         eng.close()
-    for v in ("single", "dual", "dual_multi"):
+    for v in ("single", "dual", "dual_multi", "no_bg"):
         for n in og:
             assert O.norm_rel_err(out[v][n], out["per_step"][n]) < BF16_TOL, (v, n)
             assert O.norm_rel_err(out[v][n], og[n]) < BF16_TOL, (v, n)
