@@ -26,6 +26,14 @@ SHAPES = {
     "ux": (6400, 4096, 1024, 0, 1, 0),                 # X W_x + b (hoisted input projection)
     "dWx": (1024, 4096, 6400, 1, 1, 0),                # X^T dU
     "dX": (6400, 1024, 4096, 0, 0, 0),                 # dU W_x^T
+    # c2 (2x512, V=30k, B=64, S=T=50): K = 512 products
+    "logits_c2": (3200, 30000, 512, 0, 1, 2 | 4),
+    "logits_c2_plain": (3200, 30000, 512, 0, 1, 2 | 8),
+    "dWo_c2": (512, 30000, 3200, 1, 1, 0),
+    "dHo_c2": (3200, 512, 30000, 0, 0, 2),
+    "ux_c2": (3200, 2048, 512, 0, 1, 0),
+    "dWx_c2": (512, 2048, 3200, 1, 1, 0),
+    "dX_c2": (3200, 512, 2048, 0, 0, 0),
 }
 
 
