@@ -36,7 +36,10 @@ constexpr int NU = NG / 4;
 constexpr int MAX_STAGES = 8;
 constexpr int TMEM_COLS = 512;
 constexpr int D_COLS = 128;    // accumulator columns reserved (N = ROWS <= 128)
-constexpr int MAX_KT = (TMEM_COLS - D_COLS) / 32;  // k-blocks of W_h held in TMEM
+#ifndef CMT_TM_MAX_KT
+#define CMT_TM_MAX_KT ((TMEM_COLS - D_COLS) / 32)
+#endif
+constexpr int MAX_KT = CMT_TM_MAX_KT;  // k-blocks of W_h held in TMEM (the rest in smem)
 constexpr size_t SMEM_LIMIT = 227 * 1024;
 template <int ROWS>
 struct Fwd {

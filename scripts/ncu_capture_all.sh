@@ -10,7 +10,7 @@ cap() {  # name class skip
 cap bptt_pair 1 1
 cap fwd_pair 2 1
 cap logits_gemm 0 0
-cap ux_gemm 3 2
+cap ux_gemm 3 3
 cap dx_gemm 4 2
 cap dw_gemm 5 2
 cap dwo_gemm 11 0
