@@ -280,6 +280,8 @@ def main():
     eng.stage(src, sm, tgt, tm)
     if dist:  # the ranks agree on the embedding rows the step exchanges (dp.exchange_rows)
         dpmod.exchange_rows(eng, dist)
+    # the warm-up steps capture the step graph that the timed steps replay (the
+    # engine captures a shape's second step; data parallel steps stay eager)
     for _ in range(args.warmup):
         eng.run(lr, clip, eps, rng, global_ntok=ntok_global)
 
@@ -290,8 +292,8 @@ def main():
     clocks = ClockSampler(local)
     time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
     clocks.mark()
-    eng.set_option("time_dominant", 7)  # CUDA-event probes: logits GEMM, BPTT scans, forward scans
     l0 = launch_count()
+    g0 = eng.stat("graph_replays")[0]
     eng.record(0)
     for _ in range(args.steps):
         eng.run(lr, clip, eps, rng, global_ntok=ntok_global, asynchronous=True)
@@ -299,9 +301,27 @@ def main():
     r = eng.wait()
     ms_total = eng.elapsed_ms(0, 1)
     launches = (launch_count() - l0) // args.steps
+    graph_replays = int(eng.stat("graph_replays")[0] - g0)
+    ck = clocks.stop()
+
+    # ---- kernel-class probes: the same K steps again, launched eagerly with
+    # CUDA events bracketing the logits GEMM, BPTT-scan and forward-scan launches
+    # on the engine stream (event-record nodes inside the captured graph add
+    # ~0.3 ms to a step, so the headline pass above runs without them) ----
+    eng.set_option("graph", 0)
+    eng.set_option("time_dominant", 7)
+    eng.run(lr, clip, eps, rng, global_ntok=ntok_global)
+    for c in (0, 1, 2):
+        eng.stat(f"probe_ms:{c}")  # drop the warm-up step's probes
+    eng.record(4)
+    for _ in range(args.steps):
+        eng.run(lr, clip, eps, rng, global_ntok=ntok_global, asynchronous=True)
+    eng.record(5)
+    eng.wait()
+    ms_probe_pass = eng.elapsed_ms(4, 5) / args.steps
     probes = {c: eng.stat(f"probe_ms:{c}") for c in (0, 1, 2)}  # (mean ms per launch, launches)
     eng.set_option("time_dominant", 0)
-    ck = clocks.stop()
+    eng.set_option("graph", 1)
 
     # ---- per-launch breakdown of one (untimed) step: CUDA events after every
     # launch on the engine stream (the side-stream overlap is off in this mode) ----
@@ -322,6 +342,9 @@ def main():
     from paper_1802_07170_b200 import training as TR
     TR._ENGINES[model] = eng
     tcfg = types.SimpleNamespace(grad_clip_norm=clip, label_smoothing=eps)
+    if dist is None:  # warm-up of the API path (its first steps capture the step graph)
+        for _ in range(2):
+            TR.train_step(model, batch, tcfg, lr, rng, sync="lazy")
     if dist:
         dist.barrier()
     eng.record(2)
@@ -406,6 +429,12 @@ def main():
         "e2e_pipeline": {"value": pipe_value, "unit": "tgt_tok/s",
                          "api": "Engine.pipeline (host staging of batch i+1 overlaps step i)"},
         "gpu_launches": int(launches),
+        "cuda_graph": {"replays_in_timed_steps": graph_replays, "steps": args.steps,
+                       "note": "each timed step replays the step graph captured in the warm-up "
+                               "(gpu_launches counts the kernel nodes of the replayed graph)"},
+        "probe_pass": {"ms_per_step": ms_probe_pass, "launch": "eager",
+                       "note": "roofline / roofline_classes: CUDA events around the class's launches on the "
+                               "engine stream over K further steps of the same workload"},
         "roofline": None if dom is None else {
             "bound": "tensor", "kernel": classes[dom]["kernel"], "achieved": classes[dom]["achieved"],
             "peak": peak_tf, "unit": "TFLOP/s", "frac": classes[dom]["frac"], "traffic": traffic,

@@ -16,12 +16,14 @@
 #include <cuda_profiler_api.h>
 #include <dlfcn.h>
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <numeric>
 #include <string>
+#include <tuple>
 #include <type_traits>
 #include <vector>
 
@@ -112,7 +114,10 @@ struct NcclApi {
   const char* (*get_error)(int) = nullptr;
   void load() {
     if (h) return;
-    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // the NCCL already in the process (torch's) if any; otherwise a private
+    // copy: RTLD_LOCAL keeps its symbols from binding a later torch import
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!h) throw Error(CMT_ERR_CUDA, std::string("cannot load libnccl.so.2: ") + dlerror());
     get_unique_id = (int (*)(void*))dlsym(h, "ncclGetUniqueId");
     all_reduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclAllReduce");
@@ -315,11 +320,6 @@ struct Pinned {
   }
 };
 
-struct StepScalars {  // device-side step parameters (graph-capture friendly)
-  Pcg pcg;
-  double lr, clip;
-  float eps, inv_ntok;
-};
 struct StepOut {  // device -> host step result
   double loss_sum;
   double scal[2];  // sumsq, norm
@@ -464,6 +464,8 @@ class Engine {
   int* uniq_d[2];
   float* gcomp[2];
   int nuniq[2] = {0, 0};
+  double stage_us[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // host staging phases (debug stat "stage_us:i")
+  int nrows_max[2] = {0, 0};  // the most unique rows a batch of the staged shape can have
   std::vector<unsigned long long> sort_tmp;  // radix-sort scratch of the segment builder
   int nseg_pos[2] = {0, 0};
   double* normpart;
@@ -485,6 +487,7 @@ class Engine {
     rebuild_segs();
   }
   void rebuild_segs() {
+    drop_graphs();  // the update's launches depend on the segments
     segs.clear();
     std::vector<int> wm(layers.size(), 0), bm(layers.size(), 0);
     bool all = true;
@@ -564,6 +567,7 @@ class Engine {
   void set_comm(const void* uid, int rank_, int world_) {
     if (world_ < 1 || rank_ < 0 || rank_ >= world_) throw Error(CMT_ERR_CONFIG, "bad rank/world");
     if (comm) throw Error(CMT_ERR_CONFIG, "communicator already set");
+    drop_graphs();
     g_nccl.load();
     typedef int (*InitFn)(void**, int, NcclUid, int);
     InitFn init = (InitFn)dlsym(g_nccl.h, "ncclCommInitRank");
@@ -660,6 +664,10 @@ class Engine {
   }
   ~Engine() {
     cudaStreamSynchronize(st);
+    drop_graphs();
+    for (cudaEvent_t ev : ev_pool) cudaEventDestroy(ev);
+    for (auto& v : probe_ev)
+      for (auto& pr : v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     cudaFree(dw); cudaFree(dg); cudaFree(dsh); cudaFree(gate_stage_d);
     for (int i = 0; i < 2; ++i) {
       if (i == 0 || !cfg.shared_embeddings) { cudaFree(emb_w[i]); cudaFree(emb_sh[i]); }
@@ -1233,6 +1241,7 @@ class Engine {
     size_t need = layout(nullptr);
     if (need > ws_cap) {
       CMT_CUDA(cudaStreamSynchronize(st));
+      drop_graphs();  // captured steps point into the old workspace
       if (ws) cudaFree(ws);
       ws = nullptr;
       CMT_CUDA(cudaMalloc(&ws, need));
@@ -1248,6 +1257,13 @@ class Engine {
   void stage(const long long* src, const float* smask, int S_, const long long* tgt, const float* tmask, int T_,
              int B_) {
     if (S_ < 1 || T_ < 1 || B_ < 1) throw Error(CMT_ERR_SHAPE, "batch dimensions must be positive");
+    auto tick = [&](int i) {
+      static thread_local std::chrono::steady_clock::time_point t0;
+      auto t1 = std::chrono::steady_clock::now();
+      if (i > 0) stage_us[i - 1] += std::chrono::duration<double, std::micro>(t1 - t0).count();
+      t0 = t1;
+    };
+    tick(0);
     auto bad_id = [&](const long long* ids, long long n, long long& bad) {
       for (long long i = 0; i < n; ++i)
         if (ids[i] < 0 || ids[i] >= V) { bad = ids[i]; return true; }
@@ -1267,7 +1283,9 @@ class Engine {
     ntok_local = ntok;
     if (!(ntok > 0.f) && !allow_empty_targets)
       throw Error(CMT_ERR_CONFIG, "smoothed_loss needs at least one unmasked token");
+    tick(1);
     ensure_ws(S_, T_, B_);
+    tick(2);
     // pinned staging: ids (int32) + masks + segments
     size_t nbytes = (size_t)(NS + 2 * NT) * 4 + (size_t)(NS + NT) * 4 + 2 * (size_t)(3 * (NS + NT) + 2) * 4;
     // two pinned buffers: this batch's host work (conversion, segment sort)
@@ -1292,19 +1310,21 @@ class Engine {
     CMT_CUDA(cudaMemcpyAsync(tgt_out_d, h_tout, NT * 4, cudaMemcpyHostToDevice, st));
     CMT_CUDA(cudaMemcpyAsync(src_mask_d, h_sm, NS * 4, cudaMemcpyHostToDevice, st));
     CMT_CUDA(cudaMemcpyAsync(tgt_mask_d, h_tm, NT * 4, cudaMemcpyHostToDevice, st));
+    tick(3);
     // embedding segments: unique ids (ascending) with their positions in order
     int* q = (int*)(h_tm + NT);
     // (id, position) pairs grouped by id, positions ascending within an id
-    // (= np.add.at order): one 64-bit key per pair, keys are unique, so an
-    // LSD radix sort (11-bit digits) gives the stable order in O(n)
+    // (= np.add.at order): the keys are built in position order and an LSD
+    // radix sort is stable, so sorting on the id bits alone (11-bit digits:
+    // two passes for V <= 2^22) keeps the positions ascending within an id
     auto build = [&](int t, std::vector<unsigned long long>& keys) {
       const int n = (int)keys.size();
       sort_tmp.resize(n);
       unsigned long long* src_k = keys.data();
       unsigned long long* dst_k = sort_tmp.data();
-      const unsigned long long maxkey = ((unsigned long long)(V - 1) << 32) | 0xffffffffull;
-      for (int shift = 0; shift < 64 && (maxkey >> shift); shift += 11) {
-        unsigned cnt[2049] = {0};
+      for (int shift = 32; shift < 64 && ((unsigned long long)(V - 1) >> (shift - 32)); shift += 11) {
+        unsigned cnt[2049];
+        std::memset(cnt, 0, sizeof(cnt));
         for (int i = 0; i < n; ++i) ++cnt[((src_k[i] >> shift) & 2047) + 1];
         for (int d = 0; d < 2048; ++d) cnt[d + 1] += cnt[d];
         for (int i = 0; i < n; ++i) dst_k[cnt[(src_k[i] >> shift) & 2047]++] = src_k[i];
@@ -1319,6 +1339,7 @@ class Engine {
       }
       off[nu] = n;
       nuniq[t] = nu;
+      nrows_max[t] = std::min(n, V);
       nseg_pos[t] = n;
       uniq_h[t].assign(uq, uq + nu);
       CMT_CUDA(cudaMemcpyAsync(seg_off_d[t], off, (nu + 1) * 4, cudaMemcpyHostToDevice, st));
@@ -1331,15 +1352,20 @@ class Engine {
     kb.reserve(NT);
     for (long long i = 0; i < NS; ++i) ka.push_back(((unsigned long long)h_src[i] << 32) | (unsigned)i);
     for (long long i = 0; i < NT; ++i) kb.push_back(((unsigned long long)h_tin[i] << 32) | (unsigned)(NS + i));
+    tick(4);
     if (cfg.shared_embeddings) {
       ka.insert(ka.end(), kb.begin(), kb.end());
       build(0, ka);
       nuniq[1] = 0;
+      nrows_max[1] = 0;
     } else {
       build(0, ka);
       build(1, kb);
     }
+    tick(5);
     CMT_CUDA(cudaEventRecord(pin_ev[k], st));
+    tick(6);
+    stage_us[7] += 1;
     staged = true;
     union_set[0] = union_set[1] = false;  // a new batch: its rows union comes with it
   }
@@ -1425,9 +1451,9 @@ class Engine {
   // dropout site (layers.py:265-296): numpy-exact PCG64 draws by jump-ahead;
   // x2 (optional) is added to x first (the bidirectional sum feeding enc.l2)
   template <typename TI, typename TO>
-  void launch_dropout(const void* x, void* y, uint8_t* keep, int N, unsigned long long base, const Pcg& pcg,
+  void launch_dropout(const void* x, void* y, uint8_t* keep, int N, unsigned long long base, const Pcg* pcg,
                       const void* x2 = nullptr) {
-    ensure_jump(pcg);
+    if (!jump_ok) throw Error(CMT_ERR_INTERNAL, "PCG64 jump table not built");
     dim3 blk(32, 8);
     dim3 grid(ceil_div(H, 32), ceil_div(ceil_div(N, DROP4_DPT), 8));
     float scale = 1.0f / (float)(1.0 - cfg.dropout);
@@ -1909,15 +1935,16 @@ class Engine {
   void embed_grads(int t, bool dp) {
     if (emb_sent[t]) return;
     emb_sent[t] = true;
-    if (nuniq[t]) {
+    if (rows_grid(t)) {
       if (E % 4 == 0) {
         ncu_begin(12);
-        scatter_compact_v4_kernel<<<nuniq[t], SCAT_THREADS, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t],
-                                                                       gcomp[t]);
+        scatter_compact_v4_kernel<<<rows_grid(t), SCAT_THREADS, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t],
+                                                                           nuniq[t], gcomp[t], rows_dev(t));
         ncu_end();
         CMT_LAUNCHED(); tl_mark(st, "scatter_compact_v4_kernel");
       } else {
-        scatter_compact_kernel<<<nuniq[t], 128, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t], gcomp[t]);
+        scatter_compact_kernel<<<rows_grid(t), 128, 0, st>>>(dXemb, E, seg_off_d[t], seg_pos_d[t], nuniq[t], gcomp[t],
+                                                              rows_dev(t));
         CMT_LAUNCHED(); tl_mark(st, "scatter_compact_kernel");
       }
     }
@@ -1936,17 +1963,167 @@ class Engine {
   }
 
   // ---- the step ----
+  // One CUDA graph per (S, T, B, mode): the step's ~115 launches (recurrent
+  // scans, GEMMs, CE, norm, update, side-stream forks) are captured the second
+  // time a shape is run and replayed from then on.  Everything that varies
+  // between batches of one shape is read from device memory: the step scalars
+  // (generator state, lr, clip, smoothing, 1/ntok, embedding row counts;
+  // set_scalars_kernel, launched before the graph) and the staged ids, masks
+  // and segments.  Eager launches are kept for data parallelism (NCCL calls),
+  // the timeline / probe / profiler-marker modes and debug early exits.
+  struct ProbeNode {  // an event-record node of a captured probe (time_dominant)
+    cudaGraphNode_t node;
+    int pair;
+    bool begin;
+  };
+  struct GraphEntry {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long draws = 0, kernels = 0;
+    std::vector<ProbeNode> probe_nodes;
+    std::vector<int> probe_cls;            // class of each captured probe pair
+    std::vector<cudaEvent_t> probe_cap;    // the events recorded at capture
+  };
+  using GraphKey = std::tuple<int, int, int, int, int>;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> cap_probes;  // filled while capturing
+  std::map<GraphKey, GraphEntry> graphs;
+  std::map<GraphKey, int> graph_seen;
+  int use_graph = 1;        // option "graph": 0 off, 1 capture on a shape's second run, 2 on its first
+  bool capturing = false;   // inside a capture: grids sized for the bucket's maximum row counts
+  long long graph_replays = 0;
+  void drop_graphs() {
+    for (auto& kv : graphs) {
+      cudaGraphExecDestroy(kv.second.exec);
+      cudaGraphDestroy(kv.second.graph);
+      for (cudaEvent_t ev : kv.second.probe_cap) cudaEventDestroy(ev);
+    }
+    graphs.clear();
+    graph_seen.clear();
+  }
+  bool graph_ok(bool dp) const {
+    return use_graph && !dp && !g_tl.on && ncu_class < 0 && stop_after == 0 && trace_layer < 0;
+  }
+  // grid for the embedding-row kernels: the batch's count (eager) or the
+  // bucket's maximum (captured; the kernels read the count from the scalars)
+  int rows_grid(int t) const { return capturing ? nrows_max[t] : nuniq[t]; }
+  const int* rows_dev(int t) const { return &scal_d->nrows[t]; }
+
   void run(const cmt_step_args& a, cmt_step_result* res) {
     if (!staged) throw Error(CMT_ERR_INTERNAL, "no batch staged");
     const bool dp = comm != nullptr;  // (a 1-rank communicator exercises the same path)
-    emb_sent[0] = emb_sent[1] = false;
-    const long long NS = (long long)S * B, NT = (long long)T * B, BH = (long long)B * H;
     const bool infer = (a.flags & CMT_FLAG_INFER) != 0;  // dev_entropy pass (training.py:162-182)
     const bool drop = cfg.dropout > 0.0 && !infer;        // INFER mode: dropout is the identity
     Pcg pcg{a.pcg_state_hi, a.pcg_state_lo, a.pcg_inc_hi, a.pcg_inc_lo};
     if (drop) ensure_jump(pcg);  // before any side-stream dropout reads the table
     double ntok = a.global_ntok > 0 ? a.global_ntok : ntok_local;
     float inv_ntok = ntok > 0 ? (float)(1.0 / (double)(float)ntok) : 0.f;
+    StepScalars sv;
+    sv.pcg = pcg;
+    sv.lr = a.lr;
+    sv.clip = a.clip_norm;
+    sv.eps = (float)a.epsilon;
+    sv.inv_ntok = inv_ntok;
+    sv.nrows[0] = nuniq[0];
+    sv.nrows[1] = nuniq[1];
+    set_scalars_kernel<<<1, 1, 0, st>>>(sv, scal_d);
+    CMT_LAUNCHED(); tl_mark(st, "set_scalars_kernel");
+    last_infer = infer;
+    last_ntok = ntok;
+    unsigned long long draws = 0;
+    if (graph_ok(dp)) {
+      const GraphKey key{S, T, B, a.flags & (CMT_FLAG_INFER | CMT_FLAG_NO_UPDATE), time_dominant};
+      auto it = graphs.find(key);
+      if (it == graphs.end() && ++graph_seen[key] >= (use_graph >= 2 ? 1 : 2)) {
+        if (graphs.size() >= 16) drop_graphs();  // many shapes (e.g. beam-search encodes): start over
+        const unsigned long long l0 = g_launches;
+        cudaGraph_t g = nullptr;
+        capturing = true;
+        cap_probes.clear();
+        CMT_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+        try {
+          draws = step_body(a, dp);
+        } catch (...) {
+          cudaStreamEndCapture(st, &g);
+          if (g) cudaGraphDestroy(g);
+          capturing = false;
+          throw;
+        }
+        capturing = false;
+        CMT_CUDA(cudaStreamEndCapture(st, &g));
+        GraphEntry ge;
+        ge.graph = g;
+        cudaError_t err = cudaGraphInstantiate(&ge.exec, g, 0);
+        if (err != cudaSuccess) cudaGraphDestroy(g);
+        CMT_CUDA(err);
+        // probes: each replay records fresh events into the captured record nodes
+        for (size_t i = 0; i < cap_probes.size(); ++i) {
+          ge.probe_cls.push_back(cap_probes[i].first);
+          ge.probe_cap.push_back(cap_probes[i].second.first);
+          ge.probe_cap.push_back(cap_probes[i].second.second);
+        }
+        if (!cap_probes.empty()) {
+          size_t n = 0;
+          CMT_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+          std::vector<cudaGraphNode_t> nodes(n);
+          CMT_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+          for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            CMT_CUDA(cudaGraphNodeGetType(nd, &ty));
+            if (ty != cudaGraphNodeTypeEventRecord) continue;
+            cudaEvent_t ev;
+            CMT_CUDA(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+            for (size_t i = 0; i < cap_probes.size(); ++i) {
+              if (ev == cap_probes[i].second.first) ge.probe_nodes.push_back({nd, (int)i, true});
+              if (ev == cap_probes[i].second.second) ge.probe_nodes.push_back({nd, (int)i, false});
+            }
+          }
+          if (ge.probe_nodes.size() != 2 * cap_probes.size())
+            throw Error(CMT_ERR_INTERNAL, "captured probe events not found in the step graph");
+        }
+        cap_probes.clear();
+        ge.draws = draws;
+        ge.kernels = g_launches - l0;
+        g_launches = l0;
+        it = graphs.emplace(key, ge).first;
+      }
+      if (it != graphs.end()) {
+        GraphEntry& ge = it->second;
+        if (!ge.probe_cls.empty()) {
+          std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs(ge.probe_cls.size());
+          for (auto& pr : evs) {
+            pr.first = pooled_event();
+            pr.second = pooled_event();
+          }
+          for (const ProbeNode& pn : ge.probe_nodes)
+            CMT_CUDA(cudaGraphExecEventRecordNodeSetEvent(ge.exec, pn.node,
+                                                          pn.begin ? evs[pn.pair].first : evs[pn.pair].second));
+          for (size_t i = 0; i < evs.size(); ++i) probe_ev[ge.probe_cls[i]].push_back(evs[i]);
+        }
+        CMT_CUDA(cudaGraphLaunch(it->second.exec, st));
+        g_launches += it->second.kernels;
+        ++graph_replays;
+        draws = it->second.draws;
+      } else {
+        draws = step_body(a, dp);
+      }
+    } else {
+      draws = step_body(a, dp);
+    }
+    last_draws = draws;
+    if (res) {
+      res->draws = draws;
+      res->status = CMT_OK;
+      if (!(a.flags & CMT_FLAG_ASYNC)) wait(res);
+    }
+  }
+
+  // the step's launches (captured into a graph or issued eagerly); returns the draws
+  unsigned long long step_body(const cmt_step_args& a, bool dp) {
+    emb_sent[0] = emb_sent[1] = false;
+    const long long NS = (long long)S * B, NT = (long long)T * B, BH = (long long)B * H;
+    const bool infer = (a.flags & CMT_FLAG_INFER) != 0;
+    const bool drop = cfg.dropout > 0.0 && !infer;
+    const Pcg* pcg = &scal_d->pcg;
     CMT_CUDA(cudaMemsetAsync(out_d, 0, sizeof(StepOut), st));
     // every recurrent launch of the step owns one flag region (forward layer l:
     // region l, BPTT: region nlayers + l): one memset instead of one per launch
@@ -2192,47 +2369,39 @@ class Engine {
       gemm((int)NT, V, H, Mat{hin, H, 0}, Mat{wv(off_wo), V, 1}, e);
       probe_end(0, e0);
     }
-    if (stop_after == 1) { CMT_CUDA(cudaStreamSynchronize(st)); return; }
+    if (stop_after == 1) { CMT_CUDA(cudaStreamSynchronize(st)); return 0; }
     // fused log-softmax + smoothed CE + grad (training.py:96-120, tensor.py:146-151)
     const bool fused_ce = use_ce2() && cepart;
     if (fused_ce) {
       ncu_begin(6);
-      ce_stats_kernel<<<(int)NT, CES_THREADS, 0, st>>>((const bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon,
-                                                       inv_ntok, cfg.output_tanh, losstok, status_d, cerow);
+      ce_stats_kernel<<<(int)NT, CES_THREADS, 0, st>>>((const bf16*)Y, V, tgt_out_d, tgt_mask_d, scal_d,
+                                                       cfg.output_tanh, losstok, status_d, cerow);
       ncu_end();
       CMT_LAUNCHED(); tl_mark(st, "ce_stats_kernel");
       const int chunks = (int)ceil_div(NT, CEG_ROWS);
       ncu_begin(7);
       ce_grad_kernel<<<dim3(ceil_div(V, CEG_COLS), chunks), CEG_THREADS, 0, st>>>((bf16*)Y, V, (int)NT, tgt_out_d,
-                                                                                  cerow, (float)a.epsilon,
+                                                                                  cerow, scal_d,
                                                                                   cfg.output_tanh, cepart);
       ncu_end();
       CMT_LAUNCHED(); tl_mark(st, "ce_grad_kernel");
       colsum_final_kernel<<<ceil_div(V, 256), 256, 0, st>>>(cepart, chunks, V, dg + off_bo);
       CMT_LAUNCHED(); tl_mark(st, "colsum_final_kernel");
     } else {
-      if (bf) ce_kernel<bf16><<<(int)NT, CE_THREADS, 0, st>>>((bf16*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon,
-                                                              inv_ntok, cfg.output_tanh, losstok, status_d);
-      else ce_kernel<float><<<(int)NT, CE_THREADS, 0, st>>>((float*)Y, V, tgt_out_d, tgt_mask_d, (float)a.epsilon,
-                                                            inv_ntok, cfg.output_tanh, losstok, status_d);
+      if (bf) ce_kernel<bf16><<<(int)NT, CE_THREADS, 0, st>>>((bf16*)Y, V, tgt_out_d, tgt_mask_d, scal_d,
+                                                              cfg.output_tanh, losstok, status_d);
+      else ce_kernel<float><<<(int)NT, CE_THREADS, 0, st>>>((float*)Y, V, tgt_out_d, tgt_mask_d, scal_d,
+                                                            cfg.output_tanh, losstok, status_d);
       CMT_LAUNCHED(); tl_mark(st, "ce_kernel");
     }
     sum_to_double_kernel<<<1, 1024, 0, st>>>(losstok, (int)NT, losssum_d);
     CMT_LAUNCHED(); tl_mark(st, "sum_to_double_kernel");
 
-    if (stop_after == 2) { CMT_CUDA(cudaStreamSynchronize(st)); return; }
-    last_infer = infer;
+    if (stop_after == 2) { CMT_CUDA(cudaStreamSynchronize(st)); return 0; }
     if (infer) {  // forward only: loss sum and token count, no backward, no update, no draws
       CMT_CUDA(cudaGetLastError());
       CMT_CUDA(cudaMemcpyAsync(out_h, out_d, sizeof(StepOut), cudaMemcpyDeviceToHost, st));
-      last_draws = 0;
-      last_ntok = ntok;
-      if (res) {
-        res->draws = 0;
-        res->status = CMT_OK;
-        if (!(a.flags & CMT_FLAG_ASYNC)) wait(res);
-      }
-      return;
+      return 0;
     }
     // ===== backward =====
     // output projection (layers.py:64-73): dW_o, db_o, dH_o (+ dropout bwd + tanh' of H_o)
@@ -2486,15 +2655,15 @@ class Engine {
       nparts += NORM_BLOCKS;
     }
     for (int t = 0; t < n_tables; ++t) {
-      const int rows = dp ? nunion[t] : nuniq[t];
+      const int rows = dp ? nunion[t] : rows_grid(t);
       if (!table_learn[t] || rows == 0) continue;
       const float* gsrc = dp ? ubuf[t] : gcomp[t];
       long long gn = (long long)rows * E;
-      sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(gsrc, gn, normpart + nparts, 15);
+      sumsq_partial_kernel<<<NORM_BLOCKS, 256, 0, st>>>(gsrc, gn, normpart + nparts, 15, dp ? nullptr : rows_dev(t), E);
       CMT_LAUNCHED(); tl_mark(st, "sumsq_partial_kernel");
       nparts += NORM_BLOCKS;
     }
-    clip_scale_kernel<<<1, CLIP_THREADS, 0, st>>>(normpart, nparts, a.lr, a.clip_norm, normscal_d, s32_d, status_d);
+    clip_scale_kernel<<<1, CLIP_THREADS, 0, st>>>(normpart, nparts, scal_d, normscal_d, s32_d, status_d);
     CMT_LAUNCHED(); tl_mark(st, "clip_scale_kernel");
     if (!(a.flags & CMT_FLAG_NO_UPDATE)) {
       for (const GradSeg& sg : segs) {
@@ -2514,21 +2683,15 @@ class Engine {
           CMT_LAUNCHED(); tl_mark(st, "sgd_rows_kernel");
           continue;
         }
-        if (nuniq[t] == 0) continue;
-        sgd_rows_kernel<<<nuniq[t], 128, 0, st>>>(emb_w[t], bf ? emb_sh[t] : nullptr, E, uniq_d[t], nuniq[t], gcomp[t],
-                                                   s32_d, status_d);
+        if (rows_grid(t) == 0) continue;
+        sgd_rows_kernel<<<rows_grid(t), 128, 0, st>>>(emb_w[t], bf ? emb_sh[t] : nullptr, E, uniq_d[t], nuniq[t],
+                                                       gcomp[t], s32_d, status_d, rows_dev(t));
         CMT_LAUNCHED(); tl_mark(st, "sgd_rows_kernel");
       }
     }
     CMT_CUDA(cudaGetLastError());
     CMT_CUDA(cudaMemcpyAsync(out_h, out_d, sizeof(StepOut), cudaMemcpyDeviceToHost, st));
-    last_draws = draw;
-    last_ntok = ntok;
-    if (res) {
-      res->draws = draw;
-      res->status = CMT_OK;
-      if (!(a.flags & CMT_FLAG_ASYNC)) wait(res);
-    }
+    return draw;
   }
   // debug: copy an internal buffer (converted to fp32) to the host
   long long debug_buffer(const std::string& name, float* out, long long cap) {
@@ -2596,21 +2759,34 @@ class Engine {
     ncu_on = false;
     ncu_done = true;
   }
+  std::vector<cudaEvent_t> ev_pool;  // probe events, reused (destroyed with the engine)
+  cudaEvent_t pooled_event() {
+    if (ev_pool.empty()) {
+      cudaEvent_t e;
+      CMT_CUDA(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
   cudaEvent_t probe_begin(int cls) {
     ncu_begin(cls);
     if (!((time_dominant >> cls) & 1)) return nullptr;
-    cudaEvent_t e0;
-    CMT_CUDA(cudaEventCreate(&e0));
-    CMT_CUDA(cudaEventRecord(e0, st));
+    cudaEvent_t e0 = capturing ? nullptr : pooled_event();
+    if (capturing) CMT_CUDA(cudaEventCreate(&e0));  // owned by the captured graph
+    // inside a capture the record becomes a graph node (its event is swapped per replay)
+    CMT_CUDA(cudaEventRecordWithFlags(e0, st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
     return e0;
   }
   void probe_end(int cls, cudaEvent_t e0) {
     ncu_end();
     if (!e0) return;
-    cudaEvent_t e1;
-    CMT_CUDA(cudaEventCreate(&e1));
-    CMT_CUDA(cudaEventRecord(e1, st));
-    probe_ev[cls].push_back({e0, e1});
+    cudaEvent_t e1 = capturing ? nullptr : pooled_event();
+    if (capturing) CMT_CUDA(cudaEventCreate(&e1));
+    CMT_CUDA(cudaEventRecordWithFlags(e1, st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+    if (capturing) cap_probes.push_back({cls, {e0, e1}});
+    else probe_ev[cls].push_back({e0, e1});
   }
   // mean duration (ms) of the probed launches of class cls since the last call
   double probe_ms(int cls, double* count) {
@@ -2621,8 +2797,10 @@ class Engine {
       float ms = 0;
       CMT_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
       tot += ms;
-      cudaEventDestroy(p.first);
-      cudaEventDestroy(p.second);
+      // back to the pool, not destroyed: a replayed graph's record nodes may
+      // still name them until their next replay swaps in other events
+      ev_pool.push_back(p.first);
+      ev_pool.push_back(p.second);
     }
     *count = (double)probe_ev[cls].size();
     double r = probe_ev[cls].empty() ? 0.0 : tot / probe_ev[cls].size();
@@ -2841,10 +3019,12 @@ int cmt_test_dropout(unsigned long long sh, unsigned long long sl, unsigned long
     dim3 blk(32, 8), grid(cmt::ceil_div(H, 32), cmt::ceil_div(cmt::ceil_div(N, 32), 8));
     (void)grid;
     cmt::PcgJump* jt = nullptr;
-    CMT_CUDA(cudaMalloc(&jt, sizeof(cmt::PcgJump)));
+    CMT_CUDA(cudaMalloc(&jt, sizeof(cmt::PcgJump) + sizeof(cmt::Pcg)));
+    cmt::Pcg* pcg_d = (cmt::Pcg*)(jt + 1);
+    CMT_CUDA(cudaMemcpy(pcg_d, &pcg, sizeof(pcg), cudaMemcpyHostToDevice));
     cmt::pcg_jump_table_kernel<<<1, 1>>>(jt, ih, il);
     dim3 grid4(cmt::ceil_div(H, 32), cmt::ceil_div(cmt::ceil_div(N, cmt::DROP4_DPT), 8));
-    cmt::dropout_fwd_kernel4<float, float><<<grid4, blk>>>(x, y, keep, N, H, pcg, jt, base, cmt::dropout_threshold(p),
+    cmt::dropout_fwd_kernel4<float, float><<<grid4, blk>>>(x, y, keep, N, H, pcg_d, jt, base, cmt::dropout_threshold(p),
                                                             1.0f / (float)(1.0 - p));
     cudaError_t err = cudaDeviceSynchronize();
     cudaFree(jt);
@@ -2896,7 +3076,13 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
       CMT_CUDA(cudaMemset(e->eng->trace_d, 0, 4096 * 8));
     }
     else if (k == "stop_after") e->eng->stop_after = (int)value;
+    else if (k == "graph") e->eng->use_graph = (int)value;
     else throw Error(cmt::CMT_ERR_CONFIG, "unknown option " + k);
+    // options select launch configurations: captured steps are re-captured
+    if (e && e->eng) {
+      CMT_CUDA(cudaStreamSynchronize(e->eng->st));
+      e->eng->drop_graphs();
+    }
   });
 }
 // Timeline of the launches recorded since the option "timeline" was set:
@@ -2925,6 +3111,13 @@ int cmt_get_stat(cmt_engine* e, const char* key, double* value, double* count) {
   return guard(e, [&] {
     std::string k(key);
     if (k == "dominant_ms") *value = e->eng->probe_ms(0, count);
+    else if (k.rfind("stage_us:", 0) == 0) {
+      int i = std::stoi(k.substr(9)) & 7;
+      *value = e->eng->stage_us[i];
+      *count = e->eng->stage_us[7];
+      e->eng->stage_us[i] = 0;
+    }
+    else if (k == "graph_replays") { *value = (double)e->eng->graph_replays; *count = (double)e->eng->graphs.size(); }
     else if (k.rfind("probe_ms:", 0) == 0) *value = e->eng->probe_ms(std::stoi(k.substr(9)), count);
     else if (k.rfind("trace:", 0) == 0) {
       int i = std::stoi(k.substr(6));

@@ -51,8 +51,10 @@ __global__ void gather_rows_kernel(const T* __restrict__ table, int E, const int
 // gout[u][:] = sum over positions p of segment u (in position order) of dX[pos[p]][:]
 // — the deterministic equivalent of np.add.at(table_grad, ids, dX.T).
 __global__ void scatter_compact_kernel(const float* __restrict__ dX, int E, const int* __restrict__ seg_off,
-                                       const int* __restrict__ seg_pos, int nseg, float* __restrict__ gout) {
+                                       const int* __restrict__ seg_pos, int nseg, float* __restrict__ gout,
+                                       const int* __restrict__ nseg_d = nullptr) {
   int u = blockIdx.x;
+  if (nseg_d) nseg = *nseg_d;
   if (u >= nseg) return;
   const int b = seg_off[u], e_ = seg_off[u + 1];
   // up to 8 columns per thread and 4 positions per iteration in flight (long
@@ -100,8 +102,10 @@ constexpr int SCAT_THREADS = 256;
 __global__ void __launch_bounds__(SCAT_THREADS) scatter_compact_v4_kernel(const float* __restrict__ dX, int E,
                                                                           const int* __restrict__ seg_off,
                                                                           const int* __restrict__ seg_pos, int nseg,
-                                                                          float* __restrict__ gout) {
+                                                                          float* __restrict__ gout,
+                                                                          const int* __restrict__ nseg_d = nullptr) {
   const int u = blockIdx.x;
+  if (nseg_d) nseg = *nseg_d;  // the count from the step scalars (grid sized for the bucket's maximum)
   if (u >= nseg) return;
   const int b = seg_off[u], e_ = seg_off[u + 1];
   const int E4 = E >> 2;
@@ -208,6 +212,16 @@ typedef unsigned __int128 u128;
 struct Pcg {
   unsigned long long state_hi, state_lo, inc_hi, inc_lo;
 };
+// The per-step values the kernels of a train step read from device memory
+// (written by set_scalars_kernel at the start of each step), so that one
+// captured CUDA graph serves every batch of a shape bucket.
+struct StepScalars {
+  Pcg pcg;              // generator state before the step's first draw
+  double lr, clip;      // SGD rate, global-norm clip (NaN / < 0: none)
+  float eps, inv_ntok;  // label smoothing, 1 / target tokens
+  int nrows[2];         // unique embedding rows of the batch per table
+};
+__global__ void set_scalars_kernel(StepScalars v, StepScalars* __restrict__ d) { *d = v; }
 CMT_D u128 pcg_mult() {
   return ((u128)0x2360ed051fc65da4ULL << 64) | (u128)0x4385df649fccf645ULL;
 }
@@ -271,11 +285,13 @@ inline unsigned long long dropout_threshold(double p) { return (unsigned long lo
 constexpr int DROP4_DPT = CMT_DROP_DPT;  // draws per thread: one jump-ahead amortised over them
 template <typename TI, typename TO>
 __global__ void dropout_fwd_kernel4(const TI* __restrict__ x, TO* __restrict__ y, uint8_t* __restrict__ keep, int N,
-                                    int H, Pcg pcg, const PcgJump* __restrict__ jt, unsigned long long base,
-                                    unsigned long long thr, float scale, const TI* __restrict__ x2 = nullptr) {
+                                    int H, const Pcg* __restrict__ pcgp, const PcgJump* __restrict__ jt,
+                                    unsigned long long base, unsigned long long thr, float scale,
+                                    const TI* __restrict__ x2 = nullptr) {
   const int h = blockIdx.x * 32 + threadIdx.x;
   const int n0 = (blockIdx.y * blockDim.y + threadIdx.y) * DROP4_DPT;
   if (h >= H || n0 >= N) return;
+  const Pcg pcg = *pcgp;
   const u128 s0 = pcg_jump(jt, ((u128)pcg.state_hi << 64) | pcg.state_lo, base + (unsigned long long)h * N + n0);
   unsigned long long sh = (unsigned long long)(s0 >> 64), sl = (unsigned long long)s0;
   const unsigned long long MH = 0x2360ed051fc65da4ULL, ML = 0x4385df649fccf645ULL;
@@ -488,9 +504,10 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_bwd_kernel(const T* __restri
 constexpr int CE_THREADS = 512;
 template <typename T>
 __global__ void __launch_bounds__(CE_THREADS) ce_kernel(T* __restrict__ Y, int V, const int* __restrict__ tgt,
-                                                        const float* __restrict__ tmask, float eps, float inv_ntok,
-                                                        int tanh_on, float* __restrict__ losstok,
-                                                        int* __restrict__ status) {
+                                                        const float* __restrict__ tmask,
+                                                        const StepScalars* __restrict__ sc, int tanh_on,
+                                                        float* __restrict__ losstok, int* __restrict__ status) {
+  const float eps = sc->eps, inv_ntok = sc->inv_ntok;
   __shared__ float red_m[CE_THREADS / 32], red_s[CE_THREADS / 32], red_y[CE_THREADS / 32];
   __shared__ float bc[2];
   const long long n = blockIdx.x;
@@ -586,10 +603,11 @@ CMT_D float ex2f(float x) {  // 2^x (MUFU.EX2)
 constexpr int CES_THREADS = 512;
 __global__ void __launch_bounds__(CES_THREADS) ce_stats_kernel(const bf16* __restrict__ Y, int V,
                                                                const int* __restrict__ tgt,
-                                                               const float* __restrict__ tmask, float eps,
-                                                               float inv_ntok, int tanh_on,
+                                                               const float* __restrict__ tmask,
+                                                               const StepScalars* __restrict__ sc, int tanh_on,
                                                                float* __restrict__ losstok,
                                                                int* __restrict__ status, float2* __restrict__ rowst) {
+  const float eps = sc->eps, inv_ntok = sc->inv_ntok;
   __shared__ float red_m[CES_THREADS / 32], red_s[CES_THREADS / 32], red_y[CES_THREADS / 32];
   const int n = blockIdx.x;
   const int nv = V >> 3;
@@ -669,8 +687,10 @@ constexpr int CEG_COLS = 8 * CEG_THREADS;
 constexpr int CEG_ROWS = 64;
 __global__ void __launch_bounds__(CEG_THREADS) ce_grad_kernel(bf16* __restrict__ Y, int V, int rows,
                                                               const int* __restrict__ tgt,
-                                                              const float2* __restrict__ rowst, float eps,
-                                                              int tanh_on, float* __restrict__ part) {
+                                                              const float2* __restrict__ rowst,
+                                                              const StepScalars* __restrict__ sc, int tanh_on,
+                                                              float* __restrict__ part) {
+  const float eps = sc->eps;
   const int c = blockIdx.x * CEG_COLS + threadIdx.x * 8;
   const int r0 = blockIdx.y * CEG_ROWS, r1 = min(rows, r0 + CEG_ROWS);
   if (c >= V) return;
@@ -815,8 +835,10 @@ __global__ void gate_copy_kernel(float* __restrict__ inter, float* __restrict__ 
 
 // lanes: 4-bit gate mask; element i (from g) counts iff bit (i & 3) is set
 // (15 = every element; in a gate-interleaved LSTM region i & 3 is the gate)
+// nrows_d (optional): n = *nrows_d * rowlen, the embedding rows of the step
 __global__ void sumsq_partial_kernel(const float* __restrict__ g, long long n, double* __restrict__ part,
-                                     int lanes) {
+                                     int lanes, const int* __restrict__ nrows_d = nullptr, int rowlen = 0) {
+  if (nrows_d) n = (long long)*nrows_d * rowlen;
   __shared__ double red[32];
   float a = 0.f;
   double ad = 0.0;
@@ -869,8 +891,9 @@ __global__ void sumsq_partial_kernel(const float* __restrict__ g, long long n, d
 }
 
 // scal[0] = sum of squares, scal[1] = norm; s32 = fp32(lr * scale)
-__global__ void clip_scale_kernel(const double* __restrict__ part, int nparts, double lr, double clip,
+__global__ void clip_scale_kernel(const double* __restrict__ part, int nparts, const StepScalars* __restrict__ sc,
                                   double* __restrict__ scal, float* __restrict__ s32, int* __restrict__ status) {
+  const double lr = sc->lr, clip = sc->clip;
   // fixed-shape reduction (strided per-thread sums, then a fixed tree), so the
   // norm is deterministic; launched with CLIP_THREADS threads
   __shared__ double red[32];
@@ -957,9 +980,11 @@ __global__ void sgd_dense_kernel(float* __restrict__ w, const float* __restrict_
 
 __global__ void sgd_rows_kernel(float* __restrict__ table, bf16* __restrict__ shadow, int E,
                                 const int* __restrict__ ids, int nrows, const float* __restrict__ gc,
-                                const float* __restrict__ s32, const int* __restrict__ status) {
+                                const float* __restrict__ s32, const int* __restrict__ status,
+                                const int* __restrict__ nrows_d = nullptr) {
   if (*status & ST_ABORT) return;
   int u = blockIdx.x;
+  if (nrows_d) nrows = *nrows_d;
   if (u >= nrows) return;
   const float s = *s32;
   long long r = (long long)ids[u] * E;

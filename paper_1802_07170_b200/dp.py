@@ -49,7 +49,15 @@ def global_ntok(tgt_mask, dist=None):
     return float(t.item())
 
 
+def _load_torch_nccl():
+    """Import torch before the engine first touches NCCL: the engine then binds
+    the libnccl.so.2 torch links (already in the process) instead of loading
+    another copy under the same soname, which a later torch import would reuse."""
+    import torch  # noqa: F401
+
+
 def nccl_unique_id() -> bytes:
+    _load_torch_nccl()
     buf = ctypes.create_string_buffer(128)
     lib = _lib.load()
     rc = lib.cmt_nccl_unique_id(buf)
@@ -60,6 +68,7 @@ def nccl_unique_id() -> bytes:
 
 def attach(engine, dist, rank, world):
     """Create the engine's NCCL communicator (rank 0's unique id broadcast via torch.distributed)."""
+    _load_torch_nccl()
     obj = [nccl_unique_id() if rank == 0 else None]
     if world > 1:
         dist.broadcast_object_list(obj, src=0)

@@ -8,6 +8,7 @@
 #include <cuda.h>
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include "ptx.cuh"
 
@@ -22,7 +23,7 @@ __device__ unsigned long long gt() {
 }
 
 __global__ void probe(const __grid_constant__ CUtensorMap tm, bf16* X, unsigned* flag, unsigned long long* out,
-                      int mode) {
+                      int mode, int nc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t bar;
@@ -37,7 +38,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap tm, bf16* X, unsigned*
     if (blockIdx.x == 0) {  // producer
       if (r > 0) {
         if (tid == 0)
-          while (ptx::ld_acquire(flag + 1) < (unsigned)r) {
+          while (ptx::ld_acquire(flag + 1) < (unsigned)(r * nc)) {
           }
         __syncthreads();
       }
@@ -65,7 +66,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap tm, bf16* X, unsigned*
               ptx::tma_load_2d(&tm, &bar, sm + (q * (ROWS / 128) + h) * 16384, q * 64, h * 128);
           ptx::mbar_wait(&bar, phase);
           phase ^= 1;
-          out[(r * 2 + pass)] = gt() - t0;
+          if (blockIdx.x == 1) out[(r * 2 + pass)] = gt() - t0;
         }
         atomicAdd(flag + 1, 1u);
       }
@@ -74,7 +75,8 @@ __global__ void probe(const __grid_constant__ CUtensorMap tm, bf16* X, unsigned*
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int nc = argc > 1 ? atoi(argv[1]) : 1;  // consumer CTAs reading the same block
   bf16* X;
   unsigned* flag;
   unsigned long long* out;
@@ -94,7 +96,7 @@ int main() {
   const char* names[3] = {"fresh (rewritten every round)", "fresh, second read", "stale (never rewritten)"};
   for (int mode : {0, 2}) {
     cudaMemset(flag, 0, 8);
-    probe<<<2, 256, smem>>>(tm, X, flag, out, mode);
+    probe<<<1 + nc, 256, smem>>>(tm, X, flag, out, mode, nc);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
     std::vector<unsigned long long> h(ROUNDS * 2);
@@ -103,7 +105,7 @@ int main() {
     for (int r = 4; r < ROUNDS; ++r) { a.push_back(h[2 * r]); b.push_back(h[2 * r + 1]); }
     std::sort(a.begin(), a.end());
     std::sort(b.begin(), b.end());
-    printf("mode %d: 128 KB TMA load, first read %llu ns (%s), second read %llu ns (%s)\n", mode, a[a.size() / 2],
+    printf("consumers %d, mode %d: 128 KB TMA load, first read %llu ns (%s), second read %llu ns (%s)\n", nc, mode, a[a.size() / 2],
            mode == 0 ? names[0] : names[2], b[b.size() / 2], mode == 0 ? names[1] : names[2]);
   }
   return 0;
