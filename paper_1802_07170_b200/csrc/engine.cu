@@ -466,6 +466,12 @@ class Engine {
   int nuniq[2] = {0, 0};
   double stage_us[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // host staging phases (debug stat "stage_us:i")
   int nrows_max[2] = {0, 0};  // the most unique rows a batch of the staged shape can have
+  // embedding segments built on the device (segments_kernel, in the step) or
+  // on the host at staging (data parallel: the ranks exchange their row sets)
+  bool seg_dev = false;
+  int use_seg_dev = 1;            // option "seg_dev"
+  bool seg_host_ok[2] = {false, false};
+  std::vector<int> seg_ids_h[2];  // device-segment mode: this batch's ids per table (host copy)
   std::vector<unsigned long long> sort_tmp;  // radix-sort scratch of the segment builder
   int nseg_pos[2] = {0, 0};
   double* normpart;
@@ -538,6 +544,7 @@ class Engine {
   void set_union(int t, const int* ids, int n) {
     if (t < 0 || t >= n_tables) throw Error(CMT_ERR_SHAPE, "table index out of range");
     if (!staged) throw Error(CMT_ERR_CONFIG, "stage the batch before setting its rows union");
+    host_segments(t);
     std::vector<int> map((size_t)nuniq[t]);
     int j = 0;
     for (int i = 0; i < n; ++i) {
@@ -822,7 +829,7 @@ class Engine {
       } else {
         std::memset(h, 0, (size_t)rows * cols * 4);
         int t = b.table;
-        int n = nuniq[t];
+        int n = host_rows(t);
         if (n > 0) {
           std::vector<float> gc((size_t)n * E);
           copy_sync(gc.data(), gcomp[t], gc.size() * 4, cudaMemcpyDeviceToHost);
@@ -1347,12 +1354,35 @@ class Engine {
       CMT_CUDA(cudaMemcpyAsync(uniq_d[t], uq, nu * 4, cudaMemcpyHostToDevice, st));
       q = uq + nu;
     };
+    const long long nmax_t = cfg.shared_embeddings ? NS + NT : std::max(NS, NT);
+    seg_dev = use_seg_dev && !comm && nmax_t <= SEG_MAX_N;
+    tick(4);
+    if (seg_dev) {  // built by segments_kernel inside the step; host copies of the ids for host-side readers
+      seg_ids_h[0].assign(h_src, h_src + NS);
+      if (cfg.shared_embeddings) seg_ids_h[0].insert(seg_ids_h[0].end(), h_tin, h_tin + NT);
+      else seg_ids_h[1].assign(h_tin, h_tin + NT);
+      for (int t = 0; t < 2; ++t) {
+        const long long n = t == 0 ? (cfg.shared_embeddings ? NS + NT : NS) : (cfg.shared_embeddings ? 0 : NT);
+        nrows_max[t] = (int)std::min<long long>(n, V);
+        nseg_pos[t] = (int)n;
+        nuniq[t] = nrows_max[t];  // upper bound; the step reads the count from the device
+        seg_host_ok[t] = false;
+        uniq_h[t].clear();
+      }
+      tick(5);
+      CMT_CUDA(cudaEventRecord(pin_ev[k], st));
+      tick(6);
+      stage_us[7] += 1;
+      staged = true;
+      union_set[0] = union_set[1] = false;
+      return;
+    }
     std::vector<unsigned long long> ka, kb;
     ka.reserve(NS + NT);
     kb.reserve(NT);
     for (long long i = 0; i < NS; ++i) ka.push_back(((unsigned long long)h_src[i] << 32) | (unsigned)i);
     for (long long i = 0; i < NT; ++i) kb.push_back(((unsigned long long)h_tin[i] << 32) | (unsigned)(NS + i));
-    tick(4);
+    seg_host_ok[0] = seg_host_ok[1] = true;
     if (cfg.shared_embeddings) {
       ka.insert(ka.end(), kb.begin(), kb.end());
       build(0, ka);
@@ -2005,7 +2035,42 @@ class Engine {
   }
   // grid for the embedding-row kernels: the batch's count (eager) or the
   // bucket's maximum (captured; the kernels read the count from the scalars)
-  int rows_grid(int t) const { return capturing ? nrows_max[t] : nuniq[t]; }
+  int rows_grid(int t) const { return (capturing || seg_dev) ? nrows_max[t] : nuniq[t]; }
+  // host view of a table's unique rows (device-segment mode: from the staged ids)
+  void host_segments(int t) {
+    if (!seg_dev || seg_host_ok[t]) return;
+    std::vector<int> u = seg_ids_h[t];
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    uniq_h[t] = u;
+    nuniq[t] = (int)u.size();
+    seg_host_ok[t] = true;
+  }
+  int host_rows(int t) {
+    host_segments(t);
+    return (int)uniq_h[t].size();
+  }
+  void launch_segments() {
+    const long long NS = (long long)S * B, NT = (long long)T * B;
+    SegJob j[2];
+    for (int t = 0; t < 2; ++t) {
+      j[t].off = seg_off_d[t]; j[t].pos = seg_pos_d[t]; j[t].uq = uniq_d[t]; j[t].nrows = &scal_d->nrows[t];
+      j[t].ids1 = nullptr; j[t].n1 = 0;
+    }
+    j[0].ids0 = src_ids_d; j[0].n0 = (int)NS; j[0].pos_base = 0;
+    if (cfg.shared_embeddings) { j[0].ids1 = tgt_in_d; j[0].n1 = (int)NT; }
+    j[1].ids0 = tgt_in_d; j[1].n0 = (int)NT; j[1].pos_base = (int)NS;
+    int bits = 0;
+    while (bits < 31 && ((long long)(V - 1) >> bits)) ++bits;
+    const int nmax = (int)std::max<long long>(j[0].n0 + j[0].n1, n_tables > 1 ? j[1].n0 : 0);
+    static bool attr = false;
+    if (!attr) {
+      CMT_CUDA(cudaFuncSetAttribute(segments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)seg_smem(SEG_MAX_N)));
+      attr = true;
+    }
+    segments_kernel<<<n_tables, SEG_THREADS, seg_smem(nmax), st>>>(j[0], j[1], bits);
+    CMT_LAUNCHED(); tl_mark(st, "segments_kernel");
+  }
   const int* rows_dev(int t) const { return &scal_d->nrows[t]; }
 
   void run(const cmt_step_args& a, cmt_step_result* res) {
@@ -2124,6 +2189,7 @@ class Engine {
     const bool infer = (a.flags & CMT_FLAG_INFER) != 0;
     const bool drop = cfg.dropout > 0.0 && !infer;
     const Pcg* pcg = &scal_d->pcg;
+    bool seg_pending = seg_dev && !infer;  // the embedding segments, before the backward needs them
     CMT_CUDA(cudaMemsetAsync(out_d, 0, sizeof(StepOut), st));
     // every recurrent launch of the step owns one flag region (forward layer l:
     // region l, BPTT: region nlayers + l): one memset instead of one per launch
@@ -2210,6 +2276,10 @@ class Engine {
           g_grid_cap = idle;
           fwd_prep(d1);
           g_grid_cap = 0;
+          if (seg_pending) {  // two CTAs on the SMs the enc.l1 scans leave idle
+            launch_segments();
+            seg_pending = false;
+          }
         });
       }
       // with dropout the summed top is only the input of enc.l2's dropout site:
@@ -2265,6 +2335,10 @@ class Engine {
         dec_init(k);
         scan_fwd(L + k, x, k == 1 ? E : H, T, false, nullptr);
       }
+    }
+    if (seg_pending) {
+      launch_segments();
+      seg_pending = false;
     }
     const void* Hs = (L == 1) ? top : views(L, false).ybase;
     const void* Ht = views(2 * L, false).ybase;
@@ -2924,6 +2998,7 @@ int cmt_staged_rows(cmt_engine* e, int table, int* ids, int cap, int* n) {
   return guard(e, [&] {
     cmt::Engine& g = *e->eng;
     if (table < 0 || table >= g.n_tables) throw Error(cmt::CMT_ERR_SHAPE, "table index out of range");
+    g.host_segments(table);
     *n = (int)g.uniq_h[table].size();
     if (ids) {
       if (cap < *n) throw Error(cmt::CMT_ERR_SHAPE, "id buffer too small");
@@ -3077,6 +3152,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     }
     else if (k == "stop_after") e->eng->stop_after = (int)value;
     else if (k == "graph") e->eng->use_graph = (int)value;
+    else if (k == "seg_dev") e->eng->use_seg_dev = (int)value;
     else throw Error(cmt::CMT_ERR_CONFIG, "unknown option " + k);
     // options select launch configurations: captured steps are re-captured
     if (e && e->eng) {

@@ -136,6 +136,117 @@ __global__ void __launch_bounds__(SCAT_THREADS) scatter_compact_v4_kernel(const 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Embedding segments on the device, equal to the host staging path's result:
+// the positions of one table's ids sorted stably by id (LSD radix, 4-bit
+// digits; positions stay ascending within an id = np.add.at order), the
+// unique ids in ascending order, their segment offsets and their count.  One
+// CTA of SEG_THREADS per table: positions in shared memory (two buffers),
+// per-thread digit counts as 16-bit counters, chunks of consecutive elements
+// per thread so the scatter is stable.
+// ---------------------------------------------------------------------------
+constexpr int SEG_THREADS = 1024;
+constexpr int SEG_MAX_N = 24576;  // elements per table (offsets fit 16 bits)
+struct SegJob {
+  const int* ids0;  // positions [0, n0): ids0[p]
+  const int* ids1;  // positions [n0, n0 + n1): ids1[p - n0]
+  int n0, n1, pos_base;
+  int* off;    // [nu + 1]
+  int* pos;    // [n] global positions, grouped by id
+  int* uq;     // [nu] ascending unique ids
+  int* nrows;  // nu
+};
+inline size_t seg_smem(int n) { return (size_t)2 * n * 4 + (size_t)16 * SEG_THREADS * 2 + 48 * 4; }
+// exclusive prefix sum over the CTA (SEG_THREADS threads); *total = the sum
+CMT_D int seg_excl_scan(int v, int* sh, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    const int s0 = sh[lane];
+    int t = s0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    sh[lane] = t - s0;
+    if (lane == 31) sh[32] = t;
+  }
+  __syncthreads();
+  const int r = sh[w] + x - v;
+  *total = sh[32];
+  __syncthreads();
+  return r;
+}
+__global__ void __launch_bounds__(SEG_THREADS) segments_kernel(SegJob j0, SegJob j1, int bits) {
+  const SegJob J = blockIdx.x ? j1 : j0;
+  const int n = J.n0 + J.n1;
+  extern __shared__ int segsm[];
+  int* A = segsm;
+  int* Bf = A + n;
+  unsigned short* hist = (unsigned short*)(Bf + n);  // [16][SEG_THREADS]
+  int* sh = (int*)(hist + 16 * SEG_THREADS);
+  const int t = threadIdx.x;
+  auto idof = [&](int p) { return p < J.n0 ? __ldg(J.ids0 + p) : __ldg(J.ids1 + (p - J.n0)); };
+  const int c = (n + SEG_THREADS - 1) / SEG_THREADS;
+  const int b0 = min(n, t * c), b1 = min(n, b0 + c);
+  for (int i = t; i < n; i += SEG_THREADS) A[i] = i;
+  __syncthreads();
+  for (int shift = 0; shift < bits; shift += 4) {
+#pragma unroll
+    for (int d = 0; d < 16; ++d) hist[d * SEG_THREADS + t] = 0;
+    for (int i = b0; i < b1; ++i) ++hist[((idof(A[i]) >> shift) & 15) * SEG_THREADS + t];
+    __syncthreads();
+    // exclusive offsets over the digit-major order (digit, thread): thread t owns entries [16 t, 16 t + 16)
+    int loc[16], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      loc[k] = sum;
+      sum += hist[16 * t + k];
+    }
+    int tot;
+    const int base = seg_excl_scan(sum, sh, &tot);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) hist[16 * t + k] = (unsigned short)(base + loc[k]);
+    __syncthreads();
+    for (int i = b0; i < b1; ++i) {
+      const int p = A[i];
+      unsigned short& o = hist[((idof(p) >> shift) & 15) * SEG_THREADS + t];
+      Bf[o] = p;
+      ++o;
+    }
+    __syncthreads();
+    int* tmp = A;
+    A = Bf;
+    Bf = tmp;
+  }
+  // segments: a new one starts where the id changes
+  int nf = 0;
+  for (int i = b0; i < b1; ++i) nf += (i == 0 || idof(A[i]) != idof(A[i - 1])) ? 1 : 0;
+  int nu;
+  int u = seg_excl_scan(nf, sh, &nu);
+  for (int i = b0; i < b1; ++i) {
+    const int id = idof(A[i]);
+    J.pos[i] = J.pos_base + A[i];
+    if (i == 0 || id != idof(A[i - 1])) {
+      J.off[u] = i;
+      J.uq[u] = id;
+      ++u;
+    }
+  }
+  if (t == 0) {
+    J.off[nu] = n;
+    *J.nrows = nu;
+  }
+}
+
 // dense[ids[u]][:] = rows[u][:]   (compact embedding grads -> dense, for DP all-reduce)
 __global__ void scatter_rows_kernel(const float* __restrict__ rows, int E, const int* __restrict__ ids, int n,
                                     float* __restrict__ dense) {

@@ -141,3 +141,36 @@ def test_graph_probes_record_every_replay():
         for (ms, n), (ms2, n2) in zip(counts[graph], again):
             assert n > 0 and ms > 0 and n2 * 5 == n * 3 and ms2 > 0
     assert [n for _, n in counts[0]] == [n for _, n in counts[2]]
+
+
+@pytest.mark.parametrize("shared", [False, True])
+def test_device_segments_equal_host_segments(shared):
+    """Embedding segments built in the step (segments_kernel: stable radix sort
+    of the positions by id, unique ids, offsets) give the same embedding grads
+    and updates as the host staging sort (np.add.at order, tensor.py:191-205)."""
+    from paper_1802_07170_b200.engine import Engine
+    from paper_1802_07170_b200.model import Batch
+    V = 304
+    d = O.Dims(V, 128, 256, 1, 0.0, shared_embeddings=shared)
+    params = scaled_params(d, 15, 0.1)
+    batches = _batches(V, [(9, 7, 16), (9, 7, 16), (5, 12, 24)], 500)
+    res = {}
+    for seg_dev in (0, 1):
+        eng = Engine(cfg_of(d), mode="bf16")
+        eng.set_option("seg_dev", seg_dev)
+        eng.upload(params)
+        gen = np.random.Generator(np.random.PCG64(2))
+        out = []
+        for src, sm, tgt, tm in batches:
+            out.append(eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, gen))
+        src, sm, tgt, tm = batches[0]
+        eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, gen, update=False)
+        rows = [eng.staged_rows(t) for t in range(eng.n_tables)]
+        res[seg_dev] = (out, eng.grads(), eng.params(), rows)
+        eng.close()
+    assert res[0][0] == res[1][0]
+    for k in res[0][1]:
+        assert np.array_equal(res[0][1][k], res[1][1][k]), k
+        assert np.array_equal(res[0][2][k], res[1][2][k]), k
+    for a, b in zip(res[0][3], res[1][3]):
+        assert np.array_equal(a, b)
