@@ -345,6 +345,16 @@ class Engine {
   int n_ev_ar = 0;
   int ar_overlap = 1;  // option: bucketed all-reduce overlapped with the backward (0: one all-reduce at the end)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // dropout masks generated ahead of their sites on the SMs a scan leaves idle
+  struct MaskSite {
+    int id;
+    uint8_t* keep;
+    int N;
+    unsigned long long base;
+  };
+  std::vector<MaskSite> mask_queue;  // generated beside the next recurrent launch
+  cudaEvent_t ev_mask[130] = {};
+  int mask_ahead = 1;  // option "mask_ahead"
   // background stream: the first columns of a BPTT level's weight grads run
   // here, grid-capped to the SMs the next level's scans leave idle
   cudaStream_t stb = nullptr;
@@ -661,6 +671,7 @@ class Engine {
     CMT_CUDA(cudaEventCreateWithFlags(&ev_bgj, cudaEventDisableTiming));
     CMT_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     CMT_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    for (auto& e : ev_mask) CMT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : pin_ev) CMT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : ev) CMT_CUDA(cudaEventCreate(&e));
     build_registry();
@@ -1494,6 +1505,40 @@ class Engine {
     CMT_LAUNCHED(); tl_mark(st, "dropout_fwd_kernel4");
   }
 
+  // masks queued for generation beside the next recurrent launch of scan_ctas
+  // CTAs (one mask CTA per idle SM, on the side stream); ev_mask[id] marks each
+  void flush_masks(int scan_ctas) {
+    if (mask_queue.empty()) return;
+    const int idle = g_num_sms - scan_ctas;
+    if (idle < 1) throw Error(CMT_ERR_INTERNAL, "no idle SMs for the dropout masks");
+    static bool attr = false;
+    if (!attr) {
+      CMT_CUDA(cudaFuncSetAttribute(dropout_mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DMASK_SMEM));
+      attr = true;
+    }
+    fork();
+    on_side_stream([&]() {
+      for (const MaskSite& m : mask_queue) {
+        ncu_begin(8);
+        dropout_mask_kernel<<<idle, DMASK_THREADS, DMASK_SMEM, st>>>(m.keep, m.N, H, &scal_d->pcg, jump_d, m.base,
+                                                                     dropout_threshold(cfg.dropout));
+        ncu_end();
+        CMT_LAUNCHED(); tl_mark(st, "dropout_mask_kernel");
+        CMT_CUDA(cudaEventRecord(ev_mask[m.id], st));
+      }
+    });
+    mask_queue.clear();
+  }
+  // a site whose mask was generated ahead: wait for it, then y = x * keep / (1 - p)
+  template <typename TI, typename TO>
+  void apply_dropout(int id, const void* x, const void* x2, const uint8_t* keep, void* y, long long n) {
+    CMT_CUDA(cudaStreamWaitEvent(st, ev_mask[id], 0));
+    const float scale = 1.0f / (float)(1.0 - cfg.dropout);
+    dropout_apply_kernel<TI, TO><<<grid_for(n / 8), 256, 0, st>>>((const TI*)x, (const TI*)x2, keep, (TO*)y, n,
+                                                                  scale);
+    CMT_LAUNCHED(); tl_mark(st, "dropout_apply_kernel");
+  }
+
   // ---- persistent recurrent kernels (bf16) ----
   // ---- LSTM scans ----
   struct ScanViews {
@@ -1590,6 +1635,7 @@ class Engine {
     at[0].val.cooperative = g_coop;
     c.attrs = at;
     c.numAttrs = 1;
+    flush_masks(c.gridDim.x);
     cudaEvent_t p0 = probe_begin(2);
     CMT_CUDA(cudaLaunchKernelEx(&c, k, tmap[0], tmap[1], tmap[2], tmap[3], m));
     probe_end(2, p0);
@@ -1618,6 +1664,7 @@ class Engine {
     at[0].val.cooperative = g_coop;
     c.attrs = at;
     c.numAttrs = 1;
+    flush_masks(c.gridDim.x);
     cudaEvent_t p0 = probe_begin(2);
     CMT_CUDA(cudaLaunchKernelEx(&c, k, tm[0], tm[1], tm[2], tm[3], m));
     probe_end(2, p0);
@@ -1649,6 +1696,7 @@ class Engine {
     at[0].val.cooperative = g_coop;
     c.attrs = at;
     c.numAttrs = 1;
+    flush_masks(c.gridDim.x);
     cudaEvent_t p0 = probe_begin(2);
     CMT_CUDA(cudaLaunchKernelEx(&c, k, tm[0], tm[1], tm[0], tm[1], m));
     probe_end(2, p0);
@@ -2209,6 +2257,13 @@ class Engine {
     auto enc_base = [&](int k) { return (unsigned long long)(k - 2) * NS * H; };
     auto dec_base = [&](int k) { return (unsigned long long)(L - 1) * NS * H + (unsigned long long)(k - 2) * NT * H; };
     unsigned long long draw = drop ? (unsigned long long)(L - 1) * (NS + NT) * H : 0;
+    // masks ahead of the sites (bf16, paired TMEM scans, side stream available):
+    // site ids: encoder k -> k, decoder k -> L + k, H_o -> 2L + 1
+    const bool ahead = drop && mask_ahead && bf && use_dual_fwd() && use_overlap() && dual_tm();
+    mask_queue.clear();
+    auto queue_mask = [&](int id, uint8_t* keep, long long n, unsigned long long base) {
+      if (ahead) mask_queue.push_back({id, keep, (int)n, base});
+    };
     auto dropout_site = [&](const void* in, void* out, uint8_t* keep, long long n, unsigned long long base) {
       if (bf) launch_dropout<bf16, bf16>(in, out, keep, (int)n, base, pcg);
       else launch_dropout<float, float>(in, out, keep, (int)n, base, pcg);
@@ -2226,18 +2281,21 @@ class Engine {
       if (k == 1) return Xt;
       const void* prev = views(L + k - 1, false).ybase;
       if (!drop) { drop_dec[k] = const_cast<void*>(prev); return prev; }
-      dropout_site(prev, drop_dec[k], keep_dec[k], NT, dec_base(k));
+      if (ahead) apply_dropout<bf16, bf16>(L + k, prev, nullptr, keep_dec[k], drop_dec[k], NT * H);
+      else dropout_site(prev, drop_dec[k], keep_dec[k], NT, dec_base(k));
       return drop_dec[k];
     };
     auto enc_input = [&](int k, const void* cur) -> const void* {
       if (!drop) { drop_enc[k] = const_cast<void*>(cur); return cur; }
-      dropout_site(cur, drop_enc[k], keep_enc[k], NS, enc_base(k));
+      if (ahead) apply_dropout<bf16, bf16>(k, cur, nullptr, keep_enc[k], drop_enc[k], NS * H);
+      else dropout_site(cur, drop_enc[k], keep_enc[k], NS, enc_base(k));
       return drop_enc[k];
     };
     // enc.l2's input: dropout(y_f + y_b) in one pass (the sum is not stored)
     auto enc_input_l1sum = [&]() -> const void* {
       ScanViews f = views(0, false), r = views(1, true);
-      if (bf) launch_dropout<bf16, bf16>(f.ybase, drop_enc[2], keep_enc[2], (int)NS, enc_base(2), pcg, r.ybase);
+      if (ahead) apply_dropout<bf16, bf16>(2, f.ybase, r.ybase, keep_enc[2], drop_enc[2], NS * H);
+      else if (bf) launch_dropout<bf16, bf16>(f.ybase, drop_enc[2], keep_enc[2], (int)NS, enc_base(2), pcg, r.ybase);
       else launch_dropout<float, float>(f.ybase, drop_enc[2], keep_enc[2], (int)NS, enc_base(2), pcg, r.ybase);
       return drop_enc[2];
     };
@@ -2270,6 +2328,7 @@ class Engine {
       const bool dec1_early = early_dec1 && use_overlap() && L >= 2 && idle >= 8;
       FwdScan d1{L + 1, Xt, E, T, false, nullptr, ux3};
       if (dec1_early) fork();
+      if (L >= 2) queue_mask(2, keep_enc[2], NS, enc_base(2));  // enc.l2's input, beside the enc.l1 scans
       fwd_pair(a, b);
       if (dec1_early) {
         on_side_stream([&]() {
@@ -2313,12 +2372,16 @@ class Engine {
         } else {
           fwd_prep(d);
         }
+        if (k + 1 <= L) queue_mask(k + 1, keep_enc[k + 1], NS, enc_base(k + 1));
+        queue_mask(L + k, keep_dec[k], NT, dec_base(k));  // dec.lk's input, applied at the next level
         fwd_pair(e, d);
         cur = views(k, false).ybase;
       }
       const void* xd = dec_input(L);
       dec_init(L);
+      queue_mask(2 * L + 1, keep_o, NT, draw);  // H_o, beside the dec.lL scan
       scan_fwd(2 * L, xd, L == 1 ? E : H, T, false, nullptr);
+      flush_masks(0);  // (a scan path without a persistent launch: generate them here)
     } else {
       scan_fwd(0, Xs, E, S, false, src_mask_d);
       scan_fwd(1, Xs, E, S, true, src_mask_d);
@@ -2422,7 +2485,8 @@ class Engine {
     }
     const void* hin = ho;
     if (drop) {
-      if (bf) launch_dropout<float, bf16>(ho, hod, keep_o, (int)NT, draw, pcg);
+      if (ahead) apply_dropout<float, bf16>(2 * L + 1, ho, nullptr, keep_o, hod, NT * H);
+      else if (bf) launch_dropout<float, bf16>(ho, hod, keep_o, (int)NT, draw, pcg);
       else launch_dropout<float, float>(ho, hod, keep_o, (int)NT, draw, pcg);
       draw += (unsigned long long)NT * H;
       hin = hod;
@@ -3153,6 +3217,7 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     else if (k == "stop_after") e->eng->stop_after = (int)value;
     else if (k == "graph") e->eng->use_graph = (int)value;
     else if (k == "seg_dev") e->eng->use_seg_dev = (int)value;
+    else if (k == "mask_ahead") e->eng->mask_ahead = (int)value;
     else throw Error(cmt::CMT_ERR_CONFIG, "unknown option " + k);
     // options select launch configurations: captured steps are re-captured
     if (e && e->eng) {

@@ -427,6 +427,90 @@ __global__ void dropout_fwd_kernel4(const TI* __restrict__ x, TO* __restrict__ y
   }
 }
 
+// Dropout masks ahead of their sites: the keep bytes of a site depend only
+// on the generator state and the site's draw base, not on the data, so the
+// step generates them on the SMs a running recurrent scan leaves idle (a few
+// persistent CTAs, one per SM) and the site itself becomes a memory-bound
+// apply.  Same draws and the same keep test as dropout_fwd_kernel4.
+constexpr int DMASK_THREADS = 1024;
+constexpr int DMASK_SMEM = 120 * 1024;  // one CTA per SM: a scan CTA never shares the SM
+__global__ void __launch_bounds__(DMASK_THREADS, 1)
+    dropout_mask_kernel(uint8_t* __restrict__ keep, int N, int H, const Pcg* __restrict__ pcgp,
+                        const PcgJump* __restrict__ jt, unsigned long long base, unsigned long long thr) {
+  const Pcg pcg = *pcgp;
+  const unsigned long long MH = 0x2360ed051fc65da4ULL, ML = 0x4385df649fccf645ULL;
+  const unsigned long long ih = pcg.inc_hi, il = pcg.inc_lo;
+  const int chunks = (N + DROP4_DPT - 1) / DROP4_DPT;
+  const long long items = (long long)chunks * H;  // item w: unit h = w % H, draws n0 = (w / H) * DPT
+  for (long long w = blockIdx.x * (long long)DMASK_THREADS + threadIdx.x; w < items;
+       w += (long long)gridDim.x * DMASK_THREADS) {
+    const int h = (int)(w % H);
+    const int n0 = (int)(w / H) * DROP4_DPT;
+    const u128 s0 = pcg_jump(jt, ((u128)pcg.state_hi << 64) | pcg.state_lo, base + (unsigned long long)h * N + n0);
+    unsigned long long sh = (unsigned long long)(s0 >> 64), sl = (unsigned long long)s0;
+    const int nend = min(N, n0 + DROP4_DPT);
+    long long i = (long long)n0 * H + h;
+#pragma unroll 4
+    for (int n = n0; n < nend; ++n, i += H) {
+      const unsigned long long lo = sl * ML;
+      const unsigned long long hi = __umul64hi(sl, ML) + sl * MH + sh * ML;
+      sl = lo + il;
+      sh = hi + ih + (sl < lo ? 1ull : 0ull);
+      const unsigned rot = (unsigned)(sh >> 58);
+      const unsigned long long xr = sh ^ sl;
+      const unsigned long long r = (xr >> rot) | (xr << ((64 - rot) & 63));
+      keep[i] = (r >> 11) >= thr;
+    }
+  }
+}
+// y = x * keep / (1 - p) with the masks above (x + x2 first for the
+// bidirectional sum feeding enc.l2, rounded to TI as add2_kernel stores it)
+template <typename TI, typename TO>
+__global__ void dropout_apply_kernel(const TI* __restrict__ x, const TI* __restrict__ x2,
+                                     const uint8_t* __restrict__ keep, TO* __restrict__ y, long long n, float scale) {
+  const long long n8 = n >> 3;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n8; v += (long long)gridDim.x * blockDim.x) {
+    const uint2 kb = ((const uint2*)keep)[v];
+    const uint8_t* k8 = (const uint8_t*)&kb;
+    float xv[8];
+    if constexpr (sizeof(TI) == 2) {
+      const uint4 a = ((const uint4*)x)[v];
+      const TI* a8 = (const TI*)&a;
+      if (x2) {
+        const uint4 b = ((const uint4*)x2)[v];
+        const TI* b8 = (const TI*)&b;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xv[j] = to_f<TI>(from_f<TI>(to_f<TI>(a8[j]) + to_f<TI>(b8[j])));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) xv[j] = to_f<TI>(a8[j]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float a = to_f<TI>(x[v * 8 + j]);
+        xv[j] = x2 ? to_f<TI>(from_f<TI>(a + to_f<TI>(x2[v * 8 + j]))) : a;
+      }
+    }
+    TO o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = from_f<TO>(k8[j] ? xv[j] * scale : xv[j] * 0.f);
+    if constexpr (sizeof(TO) == 2) {
+      ((uint4*)y)[v] = *(const uint4*)o;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) y[v * 8 + j] = o[j];
+    }
+  }
+  // tail (n % 8)
+  for (long long i = n8 * 8 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float a = to_f<TI>(x[i]);
+    if (x2) a = to_f<TI>(from_f<TI>(a + to_f<TI>(x2[i])));
+    y[i] = from_f<TO>(keep[i] ? a * scale : a * 0.f);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Luong "general" attention, one CTA per sentence b (attention.py:46-84,
 // layers.py:183-215).  Hs rows n = s*B+b, queries n = t*B+b.

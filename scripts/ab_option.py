@@ -1,0 +1,36 @@
+"""A/B of an engine option on the c3 step: device ms/step (CUDA events, graph
+replay), alternating the values several times in one process.
+
+python scripts/ab_option.py OPTION V0 V1 [reps] [steps]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_1802_07170_b200.engine import Engine  # noqa: E402
+from paper_1802_07170_b200.model import Model, ModelConfig, Rng  # noqa: E402
+
+opt, v0, v1 = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+steps = int(sys.argv[5]) if len(sys.argv) > 5 else 20
+V, E, H, L, B, S, T = bench.CONFIGS[os.environ.get("AB_CONFIG", "c3")]
+cfg = ModelConfig(V, E, H, L, 0.2)
+eng = Engine(cfg, mode="bf16")
+eng.upload(Model.new(cfg, Rng(1)).params)
+src, sm, tgt, tm = bench.synthetic_batch(V, S, T, B, seed=0)
+eng.stage(src, sm, tgt, tm)
+rng = Rng(5)
+res = {v0: [], v1: []}
+for r in range(reps):
+    for v in (v0, v1):
+        eng.set_option(opt, v)
+        for _ in range(3):
+            eng.run(1.0, 5.0, 0.1, rng)
+        eng.record(0)
+        for _ in range(steps):
+            eng.run(1.0, 5.0, 0.1, rng, asynchronous=True)
+        eng.record(1)
+        eng.wait()
+        res[v].append(eng.elapsed_ms(0, 1) / steps)
+for v in (v0, v1):
+    print(f"{opt}={v}: " + " ".join(f"{x:.4f}" for x in res[v]) + f"  min {min(res[v]):.4f} ms/step", flush=True)

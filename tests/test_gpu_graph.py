@@ -174,3 +174,28 @@ def test_device_segments_equal_host_segments(shared):
         assert np.array_equal(res[0][2][k], res[1][2][k]), k
     for a, b in zip(res[0][3], res[1][3]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("L", [1, 3])
+def test_masks_ahead_equal_fused_dropout(L):
+    """Dropout masks generated beside the recurrent scans (dropout_mask_kernel on
+    the idle SMs) and applied at the sites (dropout_apply_kernel) equal the fused
+    draw-and-apply kernel bit for bit: losses, generator advance, weights."""
+    from paper_1802_07170_b200.engine import Engine
+    from paper_1802_07170_b200.model import Batch
+    V = 304
+    d = O.Dims(V, 128, 256, L, 0.3)
+    params = scaled_params(d, 16, 0.1)
+    batches = _batches(V, [(9, 7, 16), (9, 7, 16), (9, 7, 16)], 600)
+    res = {}
+    for ahead in (0, 1):
+        eng = Engine(cfg_of(d), mode="bf16")
+        eng.set_option("mask_ahead", ahead)
+        eng.upload(params)
+        gen = np.random.Generator(np.random.PCG64(4))
+        out = [eng.step(Batch(src, tgt, sm, tm), 1.0, 5.0, 0.1, gen) for src, sm, tgt, tm in batches]
+        res[ahead] = (out, gen.bit_generator.state["state"]["state"], eng.params())
+        eng.close()
+    assert res[0][0] == res[1][0] and res[0][1] == res[1][1]
+    for k in res[0][2]:
+        assert np.array_equal(res[0][2][k], res[1][2][k]), k
