@@ -1,7 +1,8 @@
-"""A/B of an engine option on the c3 step: device ms/step (CUDA events, graph
-replay), alternating the values several times in one process.
+"""A/B of engine options on the c3 step: device ms/step (CUDA events, graph
+replay), alternating the two settings several times in one process.
 
-python scripts/ab_option.py OPTION V0 V1 [reps] [steps]"""
+python scripts/ab_option.py OPTION V0 V1 [reps] [steps]
+python scripts/ab_option.py - "opt=v,opt2=v2" "opt=v,opt2=v2" [reps] [steps]"""
 import os
 import sys
 
@@ -10,7 +11,16 @@ import bench  # noqa: E402
 from paper_1802_07170_b200.engine import Engine  # noqa: E402
 from paper_1802_07170_b200.model import Model, ModelConfig, Rng  # noqa: E402
 
-opt, v0, v1 = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+opt = sys.argv[1]
+
+
+def setting(x):
+    if opt != "-":
+        return ((opt, int(x)),)
+    return tuple((kv.split("=")[0], int(kv.split("=")[1])) for kv in x.split(","))
+
+
+v0, v1 = setting(sys.argv[2]), setting(sys.argv[3])
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 steps = int(sys.argv[5]) if len(sys.argv) > 5 else 20
 V, E, H, L, B, S, T = bench.CONFIGS[os.environ.get("AB_CONFIG", "c3")]
@@ -23,7 +33,8 @@ rng = Rng(5)
 res = {v0: [], v1: []}
 for r in range(reps):
     for v in (v0, v1):
-        eng.set_option(opt, v)
+        for k_, x_ in v:
+            eng.set_option(k_, x_)
         for _ in range(3):
             eng.run(1.0, 5.0, 0.1, rng)
         eng.record(0)
@@ -33,4 +44,4 @@ for r in range(reps):
         eng.wait()
         res[v].append(eng.elapsed_ms(0, 1) / steps)
 for v in (v0, v1):
-    print(f"{opt}={v}: " + " ".join(f"{x:.4f}" for x in res[v]) + f"  min {min(res[v]):.4f} ms/step", flush=True)
+    print(f"{','.join(f'{k_}={x_}' for k_, x_ in v)}: " + " ".join(f"{x:.4f}" for x in res[v]) + f"  min {min(res[v]):.4f} ms/step", flush=True)
