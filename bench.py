@@ -142,7 +142,8 @@ def step_breakdown(tl):
     GEMM launches (label 'gemm MxNxK tile') for the GEMM-only roofline."""
     tot = sum(ms for _, ms in tl)
     cls = {"recurrent scans": 0.0, "tcgen05 GEMMs": 0.0, "CE + column sums": 0.0, "SGD + norm": 0.0,
-           "attention core": 0.0, "dropout": 0.0, "other": 0.0}
+           "attention core": 0.0, "dropout": 0.0, "dropout masks (beside the scans in the timed step)": 0.0,
+           "other": 0.0}
     gemms = []
     for lab, ms in tl:
         if lab.startswith("gemm "):
@@ -157,6 +158,8 @@ def step_breakdown(tl):
             cls["SGD + norm"] += ms
         elif lab.startswith("attn"):
             cls["attention core"] += ms
+        elif lab.startswith("dropout_mask"):
+            cls["dropout masks (beside the scans in the timed step)"] += ms
         elif lab.startswith("dropout"):
             cls["dropout"] += ms
         else:
@@ -191,8 +194,13 @@ def hbm_classes(tl, cfg_t, peak_hbm):
         "CE (ce_stats + ce_grad)": (("ce_stats", "ce_grad"), 3 * 2.0 * NT * V),
         # norm (fp32 grad read) + SGD (fp32 w, g read, w write, bf16 shadow write), dense part only
         "norm + SGD (dense)": (("sumsq", "sgd_dense", "clip"), (4 + 14) * float(dense)),
-        # dropout: read x (bf16), write y (bf16) and the keep byte, per element of each site
-        "dropout (7 sites)": (("dropout",), 5.0 * H * ((L - 1) * NS + (L - 1) * NT + NT)),
+        # dropout sites with their masks generated ahead (dropout_mask_kernel beside the
+        # recurrent scans): read x (bf16; enc.l2's site x and x2; H_o's fp32) and the keep
+        # byte, write y (bf16)
+        "dropout apply (7 sites)": (("dropout_apply",),
+                                    float(H) * (NS * (7 + 5 * (L - 2)) + NT * 5 * (L - 1) + NT * 7)),
+        # fused draw-and-apply (fp32 mode / schedules without the side stream): x, y, keep
+        "dropout fused (7 sites)": (("dropout_fwd",), 5.0 * H * ((L - 1) * NS + (L - 1) * NT + NT)),
     }
     out = {}
     for name, (prefixes, nbytes) in cls.items():

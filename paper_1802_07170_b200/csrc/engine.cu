@@ -1519,15 +1519,17 @@ class Engine {
   // CTAs (one mask CTA per idle SM, on the side stream); ev_mask[id] marks each
   void flush_masks(int scan_ctas) {
     if (mask_queue.empty()) return;
-    const int idle = g_num_sms - scan_ctas;
+    // side stream beside the scan; single-stream schedules (timeline) run them
+    // on the main stream with the whole GPU
+    const bool side = use_overlap();
+    const int idle = side ? g_num_sms - scan_ctas : g_num_sms;
     if (idle < 1) throw Error(CMT_ERR_INTERNAL, "no idle SMs for the dropout masks");
     static bool attr = false;
     if (!attr) {
       CMT_CUDA(cudaFuncSetAttribute(dropout_mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DMASK_SMEM));
       attr = true;
     }
-    fork();
-    on_side_stream([&]() {
+    auto gen = [&]() {
       for (const MaskSite& m : mask_queue) {
         ncu_begin(8);
         dropout_mask_kernel<<<idle, DMASK_THREADS, DMASK_SMEM, st>>>(m.keep, m.N, H, &scal_d->pcg, jump_d, m.base,
@@ -1536,7 +1538,13 @@ class Engine {
         CMT_LAUNCHED(); tl_mark(st, "dropout_mask_kernel");
         CMT_CUDA(cudaEventRecord(ev_mask[m.id], st));
       }
-    });
+    };
+    if (side) {
+      fork();
+      on_side_stream(gen);
+    } else {
+      gen();
+    }
     mask_queue.clear();
   }
   // a site whose mask was generated ahead: wait for it, then y = x * keep / (1 - p)
@@ -1544,8 +1552,10 @@ class Engine {
   void apply_dropout(int id, const void* x, const void* x2, const uint8_t* keep, void* y, long long n) {
     CMT_CUDA(cudaStreamWaitEvent(st, ev_mask[id], 0));
     const float scale = 1.0f / (float)(1.0 - cfg.dropout);
+    ncu_begin(13);
     dropout_apply_kernel<TI, TO><<<grid_for(n / 8), 256, 0, st>>>((const TI*)x, (const TI*)x2, keep, (TO*)y, n,
                                                                   scale);
+    ncu_end();
     CMT_LAUNCHED(); tl_mark(st, "dropout_apply_kernel");
   }
 
@@ -2126,7 +2136,9 @@ class Engine {
       CMT_CUDA(cudaFuncSetAttribute(segments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)seg_smem(SEG_MAX_N)));
       attr = true;
     }
+    ncu_begin(14);
     segments_kernel<<<n_tables, SEG_THREADS, seg_smem(nmax), st>>>(j[0], j[1], bits);
+    ncu_end();
     CMT_LAUNCHED(); tl_mark(st, "segments_kernel");
   }
   const int* rows_dev(int t) const { return &scal_d->nrows[t]; }
@@ -2269,7 +2281,7 @@ class Engine {
     unsigned long long draw = drop ? (unsigned long long)(L - 1) * (NS + NT) * H : 0;
     // masks ahead of the sites (bf16, paired TMEM scans, side stream available):
     // site ids: encoder k -> k, decoder k -> L + k, H_o -> 2L + 1
-    const bool ahead = drop && mask_ahead && bf && use_dual_fwd() && use_overlap() && dual_tm();
+    const bool ahead = drop && mask_ahead && bf && use_dual_fwd() && dual_tm();
     mask_queue.clear();
     auto queue_mask = [&](int id, uint8_t* keep, long long n, unsigned long long base) {
       if (ahead) mask_queue.push_back({id, keep, (int)n, base});

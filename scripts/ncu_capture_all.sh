@@ -16,7 +16,9 @@ cap dw_gemm 5 2
 cap dwo_gemm 11 0
 cap ce_stats 6 0
 cap ce_grad 7 0
-cap dropout 8 2
+cap dropout_mask 8 2
+cap dropout_apply 13 2
+cap segments 14 0
 cap att_scores 9 0
 cap sgd_dense 10 0
 cap scatter 12 0

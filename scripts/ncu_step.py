@@ -7,7 +7,8 @@ The engine wraps the first launch of CLASS in the profiled step with
 cudaProfilerStart/Stop (engine option ncu_class), so `-c 1` captures exactly
 that kernel: 0 logits GEMM, 1 BPTT scan, 2 forward scan, 3 Ux GEMM, 4 dX GEMM,
 5 dW GEMM, 6 ce_stats, 7 ce_grad, 8 dropout, 9 attention scores GEMM,
-10 dense SGD, 11 dW_o GEMM, 12 embedding scatter.  One warm step runs first
+10 dense SGD, 11 dW_o GEMM, 12 embedding scatter, 13 dropout apply, 14 embedding
+segments (8 is the dropout mask kernel when masks are generated ahead).  One warm step runs first
 (unmarked), so the capture sees a hot engine.  Under ncu the recurrent scans
 launch non-cooperatively (the engine detects the profiler).
 """
