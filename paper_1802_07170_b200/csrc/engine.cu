@@ -234,7 +234,7 @@ static int g_splitk = 1;  // option: split-K (TMA reduce-add) for linear fp32 ep
 static int pick_ks(int M, int N, int K, int BN, int CG) {
   if (!g_splitk) return 1;
   const long long tiles = (long long)ceil_div(M, 128 * CG) * ceil_div(N, BN);
-  const long long units = g_num_sms / CG;
+  const long long units = (g_grid_cap > 0 ? std::min(g_num_sms, g_grid_cap) : g_num_sms) / CG;
   const int nkb = ceil_div(K, 64);
   double t1 = (double)((tiles + units - 1) / units);  // in whole-tile times
   int best = 1;

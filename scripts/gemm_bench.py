@@ -26,6 +26,7 @@ SHAPES = {
     "ux": (6400, 4096, 1024, 0, 1, 0),                 # X W_x + b (hoisted input projection)
     "dWx": (1024, 4096, 6400, 1, 1, 0),                # X^T dU
     "dX": (6400, 1024, 4096, 0, 0, 0),                 # dU W_x^T
+    "dWx75": (1024, 3072, 6400, 1, 1, 0),              # the main-stream 75 % of a level's dW columns
     # c2 (2x512, V=30k, B=64, S=T=50): K = 512 products
     "logits_c2": (3200, 30000, 512, 0, 1, 2 | 4),
     "logits_c2_plain": (3200, 30000, 512, 0, 1, 2 | 8),
@@ -79,9 +80,12 @@ if __name__ == "__main__":
     ap.add_argument("--iters", type=int, default=7)
     ap.add_argument("--tiles", default="128,256,129,257")
     ap.add_argument("--opt", type=int, default=None, help="engine gemm_opt bits (1: natural K order, 2: N-fastest)")
+    ap.add_argument("--splitk", type=int, default=None, help="engine splitk bits (1 split-K 2, 2 owner/helper, 4 stream-K)")
     a = ap.parse_args()
     if a.opt is not None:
         assert _lib.load().cmt_set_option(None, b"gemm_opt", a.opt) == 0
+    if a.splitk is not None:
+        assert _lib.load().cmt_set_option(None, b"splitk", a.splitk) == 0
     tiles = [int(x) for x in a.tiles.split(",")]
     for n in SHAPES:
         if a.only and n not in a.only.split(","):
