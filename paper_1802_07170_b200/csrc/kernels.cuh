@@ -887,7 +887,10 @@ __global__ void __launch_bounds__(CEG_THREADS) ce_grad_kernel(bf16* __restrict__
                                                               float* __restrict__ part) {
   const float eps = sc->eps;
   const int c = blockIdx.x * CEG_COLS + threadIdx.x * 8;
-  const int r0 = blockIdx.y * CEG_ROWS, r1 = min(rows, r0 + CEG_ROWS);
+  // row chunks from the last: ce_stats_kernel has just read the logits in row
+  // order, so the last rows are still in L2
+  const int chunk = gridDim.y - 1 - blockIdx.y;
+  const int r0 = chunk * CEG_ROWS, r1 = min(rows, r0 + CEG_ROWS);
   if (c >= V) return;
   const float eV = eps / (float)V;
   float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -917,7 +920,7 @@ __global__ void __launch_bounds__(CEG_THREADS) ce_grad_kernel(bf16* __restrict__
       __stcs((uint4*)(Y + (long long)r * V + c), *(const uint4*)o);
     }
   }
-  float4* pp = (float4*)(part + (long long)blockIdx.y * V + c);
+  float4* pp = (float4*)(part + (long long)chunk * V + c);
   pp[0] = make_float4(cs[0], cs[1], cs[2], cs[3]);
   pp[1] = make_float4(cs[4], cs[5], cs[6], cs[7]);
 }
@@ -1151,7 +1154,8 @@ __global__ void sgd_dense_kernel(float* __restrict__ w, const float* __restrict_
   const long long n4 = n >> 2;
   float4* w4 = (float4*)w;
   const float4* g4 = (const float4*)g;
-  for (long long i = tid; i < n4; i += stride) {
+  for (long long i0 = tid; i0 < n4; i0 += stride) {
+    const long long i = n4 - 1 - i0;  // from the end: the norm pass has just read it (L2)
     const float4 wv = w4[i], gv = __ldcs(g4 + i);
     float4 nw;
     nw.x = l0 ? __fsub_rn(wv.x, __fmul_rn(s, gv.x)) : wv.x;
