@@ -176,7 +176,6 @@ static std::string gemm_label(int M, int N, int K, int BN, int CG) {
 }
 
 static int g_gemm_opt = 0;  // option: bit 0 natural K order, bit 1 N-fastest tile order
-static int g_pdl = 0;  // option "pdl": GEMMs launch with programmatic stream serialization (A/B neutral, off)
 template <int BN, int AMN, int BMN, class Epi, int CG = 1, int ST = 0>
 static void launch_tc_impl(cudaStream_t st, int M, int N, int K, Mat A, Mat B, const Epi& e, int ks = 1) {
   using C = tc::Cfg<BN, CG, ST>;
@@ -203,18 +202,13 @@ static void launch_tc_impl(cudaStream_t st, int M, int N, int K, Mat A, Mat B, c
   c.blockDim = dim3(tc::NUM_THREADS);
   c.dynamicSmemBytes = C::SMEM;
   c.stream = st;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[1];
   int na = 0;
   if (CG > 1) {
     at[na].id = cudaLaunchAttributeClusterDimension;
     at[na].val.clusterDim.x = CG;
     at[na].val.clusterDim.y = 1;
     at[na].val.clusterDim.z = 1;
-    ++na;
-  }
-  if (g_pdl) {  // may start while the previous kernel drains (griddepcontrol.wait in the kernel)
-    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
   c.attrs = at;
@@ -3225,7 +3219,6 @@ int cmt_set_option(cmt_engine* e, const char* key, long long value) {
     }
     else if (k == "tma_store") cmt::g_tma_store = (int)value;
     else if (k == "gemm_opt") cmt::g_gemm_opt = (int)value;
-    else if (k == "pdl") cmt::g_pdl = (int)value;
     else if (k == "splitk") cmt::g_splitk = (int)value;
     else if (k == "timeline") {
       cmt::g_tl.on = value != 0;

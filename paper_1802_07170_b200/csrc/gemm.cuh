@@ -459,12 +459,6 @@ __global__ void __launch_bounds__(tc::NUM_THREADS, 1)
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // programmatic dependent launch: the prologue above (barriers, TMEM, tensor
-  // map prefetch) overlaps the previous kernel's tail; no memory the earlier
-  // kernels write is read or written before this wait.  The next kernel may
-  // then be scheduled onto SMs this grid no longer needs.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (opt & 4) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0 && num_kb > 0) {
