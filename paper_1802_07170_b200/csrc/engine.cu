@@ -2258,6 +2258,10 @@ class Engine {
     // every recurrent launch of the step owns one flag region (forward layer l:
     // region l, BPTT: region nlayers + l): one memset instead of one per launch
     CMT_CUDA(cudaMemsetAsync(flags, 0, flag_words() * 4, st));
+    if (g_tl.on) {
+      hold_kernel<<<1, 1, 0, st>>>(20000000ull);  // 20 ms: the host enqueues the step meanwhile
+      CMT_LAUNCHED();
+    }
     tl_mark(st, "<start>");
 
     // ===== forward =====

@@ -333,6 +333,18 @@ struct StepScalars {
   int nrows[2];         // unique embedding rows of the batch per table
 };
 __global__ void set_scalars_kernel(StepScalars v, StepScalars* __restrict__ d) { *d = v; }
+// timeline mode: hold the stream while the host enqueues the whole step, so the
+// per-launch events measure device time, not the host's launch rate
+__global__ void hold_kernel(unsigned long long ns) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (t - t0 >= ns) break;
+    __nanosleep(1000);
+  }
+}
 CMT_D u128 pcg_mult() {
   return ((u128)0x2360ed051fc65da4ULL << 64) | (u128)0x4385df649fccf645ULL;
 }
