@@ -808,7 +808,10 @@ CMT_D float ex2f(float x) {  // 2^x (MUFU.EX2)
 // Pass 1, one CTA per token row: log-sum-exp, smoothed per-token loss and the
 // row's (lse*log2e, mask/ntok) for pass 2 (training.py:96-120, tensor.py:146-151).
 constexpr int CES_THREADS = 512;
-__global__ void __launch_bounds__(CES_THREADS) ce_stats_kernel(const bf16* __restrict__ Y, int V,
+#ifndef CMT_CES_MINB
+#define CMT_CES_MINB 1  // (3 CTAs per SM forces spills: 147.5 -> 151.6 us)
+#endif
+__global__ void __launch_bounds__(CES_THREADS, CMT_CES_MINB) ce_stats_kernel(const bf16* __restrict__ Y, int V,
                                                                const int* __restrict__ tgt,
                                                                const float* __restrict__ tmask,
                                                                const StepScalars* __restrict__ sc, int tanh_on,
@@ -890,9 +893,12 @@ __global__ void __launch_bounds__(CES_THREADS) ce_stats_kernel(const bf16* __res
 // and keeps the 8 column sums (the bias grad, layers.py:72-73) in registers;
 // part[chunk][v] is reduced by colsum_final_kernel in chunk order.
 constexpr int CEG_THREADS = 256;
+#ifndef CMT_CEG_MINB
+#define CMT_CEG_MINB 6  // 48 warps per SM: 233.5 -> 221.2 us per c3 step
+#endif
 constexpr int CEG_COLS = 8 * CEG_THREADS;
 constexpr int CEG_ROWS = 64;
-__global__ void __launch_bounds__(CEG_THREADS) ce_grad_kernel(bf16* __restrict__ Y, int V, int rows,
+__global__ void __launch_bounds__(CEG_THREADS, CMT_CEG_MINB) ce_grad_kernel(bf16* __restrict__ Y, int V, int rows,
                                                               const int* __restrict__ tgt,
                                                               const float2* __restrict__ rowst,
                                                               const StepScalars* __restrict__ sc, int tanh_on,
