@@ -178,7 +178,8 @@ def test_c_abi_train_step_matches_engine_step(mode):
     """cmt_train_step, the reference-facing C entry point (host ids/masks in,
     loss out; include/cytonmt_b200.h), called through ctypes exactly as the
     INTEGRATION.md binding does, equals Engine.step (stage + run) bit for bit,
-    and advances the caller's PCG64 state by the reported draws."""
+    and advances the caller's PCG64 state by the reported draws -- including
+    the calls that capture and replay the step graph."""
     import ctypes
 
     from paper_1802_07170_b200 import _lib
@@ -186,29 +187,37 @@ def test_c_abi_train_step_matches_engine_step(mode):
     from paper_1802_07170_b200.model import Batch
     d = O.Dims(96, 32, 256, 2, 0.2)
     params = scaled_params(d, 6, 0.1)
-    src, sm, tgt, tm = O.synthetic_batch(96, 7, 6, 8, seed=3, ragged=True)
+    # three batches of one shape: the ABI engine captures its step graph on the
+    # second call and replays it on the third; the reference engine stays eager
+    batches = [O.synthetic_batch(96, 7, 6, 8, seed=3 + i, ragged=True) for i in range(3)]
     out = []
     for via_abi in (False, True):
         eng = Engine(cfg_of(d), mode=mode)
+        if not via_abi:
+            eng.set_option("graph", 0)
         eng.upload(params)
         gen = np.random.Generator(np.random.PCG64(11))
-        if via_abi:
-            s, sm_, t, tm_ = (np.ascontiguousarray(x) for x in (src.astype(np.int64), sm.astype(np.float32),
-                                                                 tgt.astype(np.int64), tm.astype(np.float32)))
-            st = pcg_state(gen)
-            args = _lib.StepArgs(1.0, 0.5, 0.1, st[0], st[1], st[2], st[3], 0.0, 0)
-            res = _lib.StepResult()
-            llp, fp = ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_float)
-            rc = eng.lib.cmt_train_step(eng.h, s.ctypes.data_as(llp), sm_.ctypes.data_as(fp), s.shape[0],
-                                        t.ctypes.data_as(llp), tm_.ctypes.data_as(fp), t.shape[0], s.shape[1],
-                                        ctypes.byref(args), ctypes.byref(res))
-            assert rc == 0, eng.lib.cmt_last_error(eng.h)
-            gen.bit_generator.advance(int(res.draws))
-            loss, norm = res.loss, res.grad_norm
-        else:
-            loss, norm = eng.step(Batch(src, tgt, sm, tm), 1.0, 0.5, 0.1, gen)
-        out.append((loss, norm, eng.params(), gen.bit_generator.state))
+        losses = []
+        for src, sm, tgt, tm in batches:
+            if via_abi:
+                s, sm_, t, tm_ = (np.ascontiguousarray(x) for x in (src.astype(np.int64), sm.astype(np.float32),
+                                                                     tgt.astype(np.int64), tm.astype(np.float32)))
+                st = pcg_state(gen)
+                args = _lib.StepArgs(1.0, 0.5, 0.1, st[0], st[1], st[2], st[3], 0.0, 0)
+                res = _lib.StepResult()
+                llp, fp = ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_float)
+                rc = eng.lib.cmt_train_step(eng.h, s.ctypes.data_as(llp), sm_.ctypes.data_as(fp), s.shape[0],
+                                            t.ctypes.data_as(llp), tm_.ctypes.data_as(fp), t.shape[0], s.shape[1],
+                                            ctypes.byref(args), ctypes.byref(res))
+                assert rc == 0, eng.lib.cmt_last_error(eng.h)
+                gen.bit_generator.advance(int(res.draws))
+                losses.append((res.loss, res.grad_norm))
+            else:
+                losses.append(eng.step(Batch(src, tgt, sm, tm), 1.0, 0.5, 0.1, gen))
+        replays = eng.stat("graph_replays")[0]
+        out.append((losses, eng.params(), gen.bit_generator.state, replays))
         eng.close()
-    assert out[0][0] == out[1][0] and out[0][1] == out[1][1] and out[0][3] == out[1][3]
-    for n in out[0][2]:
-        assert np.array_equal(out[0][2][n], out[1][2][n]), n
+    assert out[0][3] == 0 and out[1][3] == 2
+    assert out[0][0] == out[1][0] and out[0][2] == out[1][2]
+    for n in out[0][1]:
+        assert np.array_equal(out[0][1][n], out[1][1][n]), n
