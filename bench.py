@@ -423,7 +423,12 @@ def main():
         except Exception:
             traffic = None
     fstep = flops_per_step(*cfg_t)
-    h2d = (S * B * 4 + 2 * T * B * 4 + S * B * 4 + T * B * 4) + 4 * (3 * (S + T) * B + 2)
+    # per step: int32 source ids, shifted and gold target ids, fp32 masks; the
+    # embedding segments are sorted on the device (host-built and copied only
+    # in data-parallel steps)
+    h2d = S * B * 4 + 2 * T * B * 4 + S * B * 4 + T * B * 4
+    if dist:
+        h2d += 4 * (3 * (S + T) * B + 2)
     out = {
         "metric": METRIC, "value": value, "unit": "tgt_tok/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
