@@ -436,7 +436,7 @@ def main():
         "config": {"workload": args.config, "vocab": V, "emb": E, "hidden": H, "depth": L, "batch_per_gpu": B,
                    "global_batch": B * world, "src_len": S, "tgt_len": T, "dropout": 0.2, "label_smoothing": eps,
                    "clip": clip, "parallelism": f"dp{world}",
-                   "l2": "working set > L2 (bf16 logits alone 0.64 GB per step)"},
+                   "l2": f"working set > L2 (bf16 logits alone {T * B * V * 2 / 1e9:.2f} GB per step)"},
         "e2e": {"value": e2e_value, "unit": "tgt_tok/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 40,
                 "api": e2e_api},
         "e2e_pipeline": {"value": pipe_value, "unit": "tgt_tok/s",
